@@ -1,0 +1,163 @@
+/* hx.h — C ABI of the B200 H x H product library (libhx.so).
+ *
+ * Drop-in boundary for the reference's product path.  The reference seam is the Python
+ * call ``hmult_new(h, k, cfg)`` (/root/reference/pkg/src/hmat/multiply.py:252-256), whose
+ * recursion ``_multiply``/``rec`` (multiply.py:207-249) drives ``restrict``
+ * (sumexpr.py:136-154), ``_thin_product`` (sumexpr.py:93-117), ``evaluate_dense``
+ * (sumexpr.py:165-170) and one ``compress`` per far leaf (compressors.py:441-452).
+ * A per-block crossing at the ``compress`` seam would mean 1e5..1e6 Python->C calls, so
+ * this library replaces the whole product: the host wrapper
+ * (paper_1805_08998_b200/multiply.py) keeps the reference signature and calls, in order,
+ *
+ *   hx_plan_create      restrict/_thin_product bookkeeping     -> flat term lists
+ *   hx_ctx_create       device context (one per GPU / process)
+ *   hx_ctx_operand      upload (or attach) the packed A / B pools   (HMatrix.data)
+ *   hx_product          term formation, materialization, recompression (_multiply)
+ *   hx_result_*         ranks, degraded flags and factors back to the caller
+ *
+ * plus the GPU operand assembly that replaces assemble_hmatrix (hmatrix.py:97-118).
+ * All entry points return 0 on success or a negative hx_status; hx_last_error() gives
+ * the message.  Plain C types only; no torch types cross this boundary.
+ */
+#ifndef HX_H
+#define HX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum hx_status {
+  HX_OK = 0,
+  HX_EINVAL = -1,      /* bad argument / config  -> ValueError   */
+  HX_ENOMEM = -2,      /* device or host allocation failed -> MemoryError */
+  HX_ECUDA = -3,       /* CUDA runtime error     -> RuntimeError */
+  HX_EUNSUPPORTED = -4 /* valid input this build does not handle -> NotImplementedError */
+};
+
+/* Block-cluster tree in array form (clustering.py:110-172): cluster ids and block ids in
+ * the reference's DFS pre-order; children ordered tau-child-major like the reference. */
+typedef struct hx_tree {
+  int32_t n_clusters;
+  const int64_t* c_lo;     /* [n_clusters] first tree position                      */
+  const int64_t* c_hi;     /* [n_clusters] one past the last position               */
+  const int32_t* c_child;  /* [2 * n_clusters] children, -1 for a leaf cluster       */
+  int32_t n_nodes;
+  const int32_t* tau;      /* [n_nodes] row cluster id                              */
+  const int32_t* sigma;    /* [n_nodes] column cluster id                           */
+  const int8_t* kind;      /* [n_nodes] 0 inner, 1 far, 2 near                      */
+  const int32_t* child;    /* [4 * n_nodes] children, -1 when the node is a leaf    */
+} hx_tree;
+
+/* Leaf payload directory of one H-matrix operand (HMatrix.data, hmatrix.py:48-65) over a
+ * packed float64 pool: low-rank leaves store left (m x k) then right (n x k), dense
+ * leaves store m x n, all column-major. */
+typedef struct hx_operand {
+  const int8_t* payload;   /* [n_nodes] 0 none (inner), 1 low rank, 2 dense          */
+  const int32_t* rank;     /* [n_nodes] rank of low-rank leaves                      */
+  const int64_t* u_off;    /* [n_nodes] element offset of left factor                */
+  const int64_t* v_off;    /* [n_nodes] element offset of right factor               */
+  const int64_t* d_off;    /* [n_nodes] element offset of dense payload              */
+} hx_operand;
+
+typedef struct hx_plan hx_plan;
+typedef struct hx_ctx hx_ctx;
+
+typedef struct hx_plan_info {
+  int64_t n_out;            /* output leaves in this plan (far + near)             */
+  int64_t n_far, n_near;
+  int64_t n_terms_real;     /* terms created by the restrict descent (logged)      */
+  int64_t n_terms_expand;   /* terms created by expanding pending pairs at far leaves */
+  int64_t n_dxd;            /* dense x dense products                              */
+  int64_t created[3];       /* real-descent terms by kind: FF, FX, XF              */
+  int64_t mat_terms, mat_tiles, mat_groups;
+  int64_t core_terms, core_tiles;
+  int64_t fac_terms, fac_tiles;
+  int64_t core_elems, term_elems, tile_elems;
+  int64_t max_out_dim;      /* largest output block side                           */
+  double flops_form, bytes_form;   /* canonical model term formation   */
+  double flops_near, bytes_near;   /* canonical model near leaves                    */
+} hx_plan_info;
+
+/* ---- planning (CPU only; no GPU needed) ---------------------------------------------
+ * leaf_mask (nullable, [n_nodes]): nonzero for output leaves this process owns; terms
+ * are only built for blocks on the root path of an owned leaf (multi-GPU partition).
+ * tile: CTA tile side (32 or 64). */
+int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
+                   const uint8_t* leaf_mask, int tile, hx_plan** out);
+int hx_plan_info_get(const hx_plan* plan, hx_plan_info* info);
+/* Per output leaf (plan order): block id, kind (1 far / 2 near), m, n, stacked rank K,
+ * dense-pair flops F_DD and elements E_DD (canonical model inputs). Any pointer may be
+ * NULL. */
+int hx_plan_leaves(const hx_plan* plan, int32_t* ids, int8_t* kind, int32_t* m,
+                   int32_t* n, int64_t* stacked_rank, double* f_dd, double* e_dd);
+/* Terms created by the restrict descent, in creation order: creation block, kind
+ * (0 FF, 1 FX, 2 XF), A node, B node, rank — the instrumented replay of
+ * sumexpr.py:146-151. */
+int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kind, int32_t* a_node,
+                     int32_t* b_node, int32_t* rank);
+void hx_plan_free(hx_plan* plan);
+
+/* ---- device context ----------------------------------------------------------------- */
+int hx_ctx_create(int device, hx_ctx** out);
+/* which: 0 = A, 1 = B.  host != NULL: copy n_elems doubles from host memory.
+ * host == NULL and device != NULL: attach an existing device pool (not owned). */
+int hx_ctx_operand(hx_ctx* ctx, int which, const double* host, const double* device,
+                   int64_t n_elems);
+/* Reuse A's pool for B (A is B). */
+int hx_ctx_operand_alias(hx_ctx* ctx);
+
+typedef struct hx_product_cfg {
+  int32_t policy;        /* 0 EpsRank, 1 FixedRank (lowrank.py:57-72)               */
+  double eps;            /* EpsRank.eps (already clamped by the caller)             */
+  int32_t k_max;         /* FixedRank.k_max                                         */
+  int32_t tag;           /* 0 aca, 1 bilanczos, 2 randomized, 3 dense-svd           */
+  uint64_t seed;         /* CompressorKind.seed                                     */
+  int32_t sketch0;       /* initial sketch width (0 = default)                      */
+  int32_t oversample;    /* minimum sketch oversampling (0 = default 6)             */
+} hx_product_cfg;
+
+typedef struct hx_product_stats {
+  double ms_total;       /* CUDA-event time of the whole product on the device      */
+  double ms_form, ms_mat, ms_recompress;
+  int64_t far_leaves, near_leaves, degraded_blocks, max_far_rank;
+  int64_t matvec_count;  /* operator columns applied by the recompression           */
+  int64_t sketch_rounds;
+  int64_t launches;      /* kernels launched by this call                           */
+  int64_t out_elems;     /* doubles in the packed result                            */
+  double fro2_total;     /* sum of squared Frobenius norms of all output blocks     */
+  double dom_kernel_ms;  /* summed device time of the materialization launches      */
+} hx_product_stats;
+
+int hx_product(hx_ctx* ctx, const hx_plan* plan, const hx_product_cfg* cfg,
+               hx_product_stats* stats);
+/* Per output leaf (plan order): rank (-1 near), degraded flag, element offset of the
+ * leaf's payload in the packed result (left m x r then right n x r, or dense m x n,
+ * column-major). */
+int hx_result_layout(hx_ctx* ctx, int32_t* rank, int8_t* degraded, int64_t* offset);
+int hx_result_download(hx_ctx* ctx, double* host, int64_t n_elems);
+
+/* ---- GPU operand assembly (assemble_hmatrix, hmatrix.py:97-118) ----------------------
+ * points: [n x dim] row-major in TREE order (points[perm]); kernel: 0 exp(-r),
+ * 1 exp(-r/0.5), 2 exp(-r^2/0.1), 3 1/(r+h).  Far leaves by ACA at eps (with the
+ * eps/2 SVD recompression of compressors.py:245-246), near leaves dense.  The packed
+ * pool stays on the device as operand `which`; offsets/ranks/flags are returned. */
+int hx_assemble(hx_ctx* ctx, int which, const hx_tree* tree, const double* points,
+                int dim, int kernel, double h, double eps, int8_t* payload,
+                int32_t* rank, int64_t* u_off, int64_t* v_off, int64_t* d_off,
+                int64_t* pool_elems);
+/* Copy `n_elems` of operand `which`'s device pool to host memory. */
+int hx_operand_download(hx_ctx* ctx, int which, double* host, int64_t n_elems);
+
+int hx_ctx_synchronize(hx_ctx* ctx);
+void hx_ctx_free(hx_ctx* ctx);
+
+int hx_last_error(char* buf, size_t len);
+int hx_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HX_H */

@@ -1,0 +1,337 @@
+// Per-block dense linear algebra for the recompression of far output blocks.
+//
+// The reference truncates each far block with an exact SVD and the epsilon-rank rule
+// (dense_svd_compress, compressors.py:431-438; select_rank, lowrank.py:75-90).  Here each
+// CTA owns one block and runs, in shared memory when it fits (else in place in HBM/L2):
+//   qr_explicit_kernel  Householder QR (LAPACK dgeqr2 + dorg2r semantics), R saved, Q formed
+//   jacobi_svd_kernel   one-sided (Hestenes) Jacobi SVD of the small q x q factor, parallel
+//                       round-robin pair ordering, singular values sorted descending
+//   select_rank_kernel  epsilon / fixed rank from the singular values plus the exact
+//                       unsampled tail mass ||T||_F^2 - sum s_i^2
+//   small_product_kernel out = P * C[:, :r] * diag(scale)  (final factors)
+#pragma once
+#include <cstdint>
+
+namespace hx {
+
+constexpr int LA_THREADS = 256;
+constexpr int JAC_QMAX = 96;
+
+struct QrJob {
+  double* X;   // p x q column-major, ld = p; overwritten by explicit Q
+  double* R;   // q x q column-major output (upper triangular)
+  int p, q;
+};
+
+struct JacJob {
+  const double* R;  // q x q input
+  double* sig;      // q singular values, descending
+  double* W;        // q x q left singular vectors of R
+  double* V;        // q x q right singular vectors of R
+  int q;
+};
+
+struct SelJob {
+  const double* sig;
+  const double* fro2;  // ||T||_F^2 of the block
+  int l;               // sketch width (number of singular values)
+  int mu;              // min(m, n)
+  int exact;           // 1: the sketch spans the whole block (no unsampled tail)
+};
+
+struct SmallJob {
+  const double* P;   // rows x q (ld_p) or nullptr for identity (out = C)
+  const double* C;   // q x r block of a q x q matrix (ld = ldc)
+  const double* scale;  // r column scales or nullptr
+  double* out;       // rows x r (ld = rows)
+  int rows, q, ldc, ld_p, r;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) s += red[w];
+  return s;
+}
+
+// Apply H = I - tau v v^T, v = (1, M[j+1:p, j]), to columns c0..q-1 of M (rows j..p-1).
+__device__ void apply_reflector(double* M, int ld, int p, int q, int j, int c0, double tau) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const double* v = M + int64_t(j) * ld;
+  for (int c = c0 + warp; c < q; c += nw) {
+    double* col = M + int64_t(c) * ld;
+    double w = 0.0;
+    for (int i = j + 1 + lane; i < p; i += 32) w += v[i] * col[i];
+    w = warp_sum(w) + col[j];
+    w *= tau;
+    if (lane == 0) col[j] -= w;
+    for (int i = j + 1 + lane; i < p; i += 32) col[i] -= w * v[i];
+  }
+}
+
+__device__ void householder_qr_explicit(double* M, int ld, int p, int q, double* Rout,
+                                        double* tau_s, double* red) {
+  // factor
+  for (int j = 0; j < q; ++j) {
+    double* x = M + int64_t(j) * ld;
+    double part = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) part += x[i] * x[i];
+    const double xn2 = block_sum(part, red);
+    const double alpha = x[j];
+    double tau, beta;
+    if (xn2 == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+    } else {
+      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      const double scal = 1.0 / (alpha - beta);
+      for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) x[i] *= scal;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      x[j] = beta;
+      tau_s[j] = tau;
+    }
+    __syncthreads();
+    if (tau != 0.0) apply_reflector(M, ld, p, q, j, j + 1, tau);
+    __syncthreads();
+  }
+  // R (q x q, upper)
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int i = e % q, c = e / q;
+    Rout[e] = (i <= c) ? M[i + int64_t(c) * ld] : 0.0;
+  }
+  __syncthreads();
+  // explicit Q in place (dorg2r)
+  for (int j = q - 1; j >= 0; --j) {
+    const double tau = tau_s[j];
+    if (j < q - 1) {
+      if (threadIdx.x == 0) M[j + int64_t(j) * ld] = 1.0;
+      __syncthreads();
+      if (tau != 0.0) apply_reflector(M, ld, p, q, j, j + 1, tau);
+      __syncthreads();
+    }
+    double* x = M + int64_t(j) * ld;
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) x[i] *= -tau;
+    for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] = 0.0;
+    if (threadIdx.x == 0) x[j] = 1.0 - tau;
+    __syncthreads();
+  }
+}
+
+// One CTA per job.  use_smem: copy X into dynamic shared memory (p*q doubles) first.
+__global__ void __launch_bounds__(LA_THREADS) qr_explicit_kernel(const QrJob* __restrict__ jobs,
+                                                                 int use_smem) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ double tau_s[JAC_QMAX * 2];
+  __shared__ double red[LA_THREADS / 32];
+  const QrJob jb = jobs[blockIdx.x];
+  const int p = jb.p, q = jb.q;
+  if (use_smem) {
+    for (int64_t e = threadIdx.x; e < int64_t(p) * q; e += blockDim.x) dsm[e] = jb.X[e];
+    __syncthreads();
+    householder_qr_explicit(dsm, p, p, q, jb.R, tau_s, red);
+    __syncthreads();
+    for (int64_t e = threadIdx.x; e < int64_t(p) * q; e += blockDim.x) jb.X[e] = dsm[e];
+  } else {
+    householder_qr_explicit(jb.X, p, p, q, jb.R, tau_s, red);
+  }
+}
+
+// Round-robin (circle method) pairing: round r of qe-1, pair k of qe/2.
+__device__ __forceinline__ void rr_pair(int qe, int r, int k, int& i, int& j) {
+  auto pos = [&](int x) { return ((x - 1 + r) % (qe - 1)) + 1; };
+  if (k == 0) {
+    i = 0;
+    j = pos(1);
+  } else {
+    i = pos(k + 1);
+    j = pos(qe - k);
+  }
+}
+
+__global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __restrict__ jobs) {
+  extern __shared__ __align__(16) double dsm[];
+  __shared__ int rotated;
+  __shared__ int order[JAC_QMAX];
+  __shared__ double norms[JAC_QMAX];
+  const JacJob jb = jobs[blockIdx.x];
+  const int q = jb.q;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  double* M = dsm;              // q x q, ld q
+  double* V = dsm + q * q;      // q x q, ld q
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    M[e] = jb.R[e];
+    V[e] = (e % q == e / q) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const int qe = (q + 1) & ~1;
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+    if (threadIdx.x == 0) rotated = 0;
+    __syncthreads();
+    for (int r = 0; r < qe - 1; ++r) {
+      for (int k = warp; k < qe / 2; k += nw) {
+        int i, j;
+        rr_pair(qe, r, k, i, j);
+        if (i >= q || j >= q) continue;
+        if (i > j) {
+          const int t = i;
+          i = j;
+          j = t;
+        }
+        double* mi = M + i * q;
+        double* mj = M + j * q;
+        double a = 0.0, b = 0.0, g = 0.0;
+        for (int x = lane; x < q; x += 32) {
+          const double u = mi[x], w = mj[x];
+          a += u * u;
+          b += w * w;
+          g += u * w;
+        }
+        a = warp_sum(a);
+        b = warp_sum(b);
+        g = warp_sum(g);
+        if (fabs(g) > tol * sqrt(a * b) && g != 0.0) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t);
+          const double s = c * t;
+          for (int x = lane; x < q; x += 32) {
+            const double u = mi[x], w = mj[x];
+            mi[x] = c * u - s * w;
+            mj[x] = s * u + c * w;
+          }
+          double* vi = V + i * q;
+          double* vj = V + j * q;
+          for (int x = lane; x < q; x += 32) {
+            const double u = vi[x], w = vj[x];
+            vi[x] = c * u - s * w;
+            vj[x] = s * u + c * w;
+          }
+          if (lane == 0) rotated = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!rotated) break;
+    __syncthreads();
+  }
+  // singular values = column norms, sorted descending (stable)
+  for (int c = warp; c < q; c += nw) {
+    double s = 0.0;
+    for (int x = lane; x < q; x += 32) s += M[c * q + x] * M[c * q + x];
+    s = warp_sum(s);
+    if (lane == 0) norms[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < q; c += blockDim.x) {
+    int pos = 0;
+    for (int d = 0; d < q; ++d)
+      if (norms[d] > norms[c] || (norms[d] == norms[c] && d < c)) ++pos;
+    order[pos] = c;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int x = e % q, pos = e / q;
+    const int c = order[pos];
+    const double s = norms[c];
+    jb.W[e] = s > 0.0 ? M[c * q + x] / s : 0.0;
+    jb.V[e] = V[c * q + x];
+  }
+  for (int pos = threadIdx.x; pos < q; pos += blockDim.x) jb.sig[pos] = norms[order[pos]];
+}
+
+// rank[i] / retry[i] for each block: select_rank (lowrank.py:75-90) on the singular values
+// with the unsampled tail appended as one more entry.  policy 0: eps, 1: fixed k_max.
+__global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int policy, double eps,
+                                   int k_max, int oversample, int* __restrict__ rank,
+                                   int* __restrict__ retry) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const SelJob jb = jobs[b];
+  const int l = jb.l;
+  if (policy == 1) {
+    const int r = min(k_max, jb.mu);
+    rank[b] = min(r, l);
+    retry[b] = (r > l) ? 1 : 0;
+    return;
+  }
+  double s2 = 0.0;
+  for (int i = 0; i < l; ++i) s2 += jb.sig[i] * jb.sig[i];
+  double extra = jb.exact ? 0.0 : fmax(0.0, *jb.fro2 - s2);
+  // tails from the back: tail[r] = sqrt(extra + sum_{i>=r} s_i^2), summed smallest first
+  // like the reference's reversed cumsum; total = tail[0]
+  double tot2 = extra;
+  for (int i = l - 1; i >= 0; --i) tot2 += jb.sig[i] * jb.sig[i];
+  const double total = sqrt(tot2);
+  const double thr = eps * total;
+  int r = l + 1;  // l + 1: even dropping only the unsampled mass fails
+  if (sqrt(extra) <= thr) r = l;
+  double acc = extra;
+  for (int i = l - 1; i >= 0; --i) {
+    acc += jb.sig[i] * jb.sig[i];
+    if (sqrt(acc) <= thr) r = i;
+  }
+  // select_rank picks the FIRST r whose tail is small enough; tails are non-increasing in r,
+  // so the smallest qualifying r found by the backward scan is that index.
+  if (jb.exact) {
+    rank[b] = min(r, l);
+    retry[b] = 0;
+  } else {
+    retry[b] = (r > l - oversample && l < jb.mu) ? 1 : 0;
+    rank[b] = min(r, l);
+  }
+}
+
+// out(rows x r) = P(rows x q) * C(:, :r) * diag(scale); grid (job, row chunk of 128).
+__global__ void __launch_bounds__(128) small_product_kernel(const SmallJob* __restrict__ jobs) {
+  extern __shared__ __align__(16) double cs[];
+  const SmallJob jb = jobs[blockIdx.x];
+  const int r = jb.r, q = jb.q;
+  if (r == 0) return;
+  for (int e = threadIdx.x; e < q * r; e += blockDim.x) {
+    const int kk = e % q, c = e / q;
+    const double s = jb.scale ? jb.scale[c] : 1.0;
+    cs[e] = jb.C[kk + int64_t(c) * jb.ldc] * s;
+  }
+  __syncthreads();
+  for (int row0 = blockIdx.y * 128; row0 < jb.rows; row0 += 128 * gridDim.y) {
+    const int i = row0 + threadIdx.x;
+    if (i >= jb.rows) continue;
+    for (int c = 0; c < r; ++c) {
+      double acc = 0.0;
+      if (jb.P) {
+        for (int kk = 0; kk < q; ++kk) acc += jb.P[i + int64_t(kk) * jb.ld_p] * cs[kk + c * q];
+      } else {
+        acc = cs[i + c * q];
+      }
+      jb.out[i + int64_t(c) * jb.rows] = acc;
+    }
+  }
+}
+
+__global__ void segment_sum_kernel(const double* __restrict__ vals, const int* __restrict__ begin,
+                                   const int* __restrict__ end, double* __restrict__ out, int n) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  double s = 0.0;
+  for (int i = begin[b]; i < end[b]; ++i) s += vals[i];
+  out[b] = s;
+}
+
+}  // namespace hx

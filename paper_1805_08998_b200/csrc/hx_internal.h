@@ -1,0 +1,72 @@
+// Host-side internals shared by the plan builder and the CUDA runtime (not part of the ABI).
+#pragma once
+#include <cstdint>
+#include <cstdio>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/hx.h"
+#include "hx_types.h"
+
+namespace hx {
+
+struct Unsupported : std::runtime_error {
+  explicit Unsupported(const std::string& s) : std::runtime_error(s) {}
+};
+struct CudaFailure : std::runtime_error {
+  explicit CudaFailure(const std::string& s) : std::runtime_error(s) {}
+};
+struct OutOfMemory : std::runtime_error {
+  explicit OutOfMemory(const std::string& s) : std::runtime_error(s) {}
+};
+
+struct OutLeaf {
+  int32_t id;
+  int8_t kind;   // 1 far, 2 near
+  int32_t m, n;
+  int64_t row0, col0;
+  int64_t ws_off;
+  int32_t tile_begin, tile_end;
+  int32_t sumsq_begin, sumsq_end;
+  int64_t K;
+  double fdd, edd;
+};
+
+void set_error(const std::string& msg);
+int fail(int code, const std::string& msg);
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Unsupported& e) {
+    return fail(HX_EUNSUPPORTED, e.what());
+  } catch (const CudaFailure& e) {
+    return fail(HX_ECUDA, e.what());
+  } catch (const OutOfMemory& e) {
+    return fail(HX_ENOMEM, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(HX_ENOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(HX_EINVAL, e.what());
+  }
+}
+
+}  // namespace hx
+
+struct hx_plan {
+  int tile = 64;
+  std::vector<hx::Term> core_terms, fac_terms, mat_terms;
+  std::vector<hx::Tile> core_tiles, fac_tiles, mat_tiles;
+  std::vector<hx::Group> core_groups, fac_groups, mat_groups;
+  std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
+  std::vector<hx::OutLeaf> leaves;
+  int64_t core_elems = 0, term_elems = 0, tile_elems = 0;
+  int64_t near_ws_begin = 0;  // near-leaf blocks sit after all far blocks in BUF_TILE
+  int32_t n_sumsq = 0;
+  std::vector<int32_t> log_block, log_a, log_b, log_rank;
+  std::vector<int8_t> log_kind;
+  hx_plan_info info;
+};

@@ -1,0 +1,685 @@
+// Device runtime of the H x H product: context, pools, the product pipeline, results.
+//
+// hx_product replaces _multiply (/root/reference/pkg/src/hmat/multiply.py:207-249):
+//   1. term formation  (cores, pushed-through factors)       grouped DMMA GEMM x 2
+//   2. materialization of every output leaf from its terms   grouped DMMA GEMM x 1
+//      (near leaves are final here: evaluate_dense, sumexpr.py:165-170)
+//   3. recompression of far leaves to the requested policy (compress, compressors.py:441)
+//      sketch  Y = T Omega -> Householder QR -> Bt = T^T Q -> QR -> Jacobi SVD of R
+//      -> select_rank with the exact unsampled tail -> factors (U S, V)
+//      blocks whose selected rank leaves less than `oversample` spare sketch columns are
+//      redone with a doubled sketch; a sketch that spans the block is exact.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "dense_la.cuh"
+#include "gemm.cuh"
+#include "hx_internal.h"
+
+using namespace hx;
+
+#define CK(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      throw hx::CudaFailure(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+  } while (0)
+
+namespace {
+
+constexpr int SMEM_CAP = 200 * 1024;  // dynamic shared memory per CTA we allow ourselves
+
+template <class T>
+struct DArr {
+  T* p = nullptr;
+  size_t cap = 0;
+  void ensure(size_t n) {
+    if (n <= cap && p) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    const size_t want = std::max<size_t>(n, 1);
+    if (cudaMalloc(&p, want * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw hx::OutOfMemory("cudaMalloc of " + std::to_string(want * sizeof(T)) + " bytes");
+    }
+    cap = want;
+  }
+  void upload(const T* h, size_t n, cudaStream_t s) {
+    ensure(n);
+    if (n) CK(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t x) {
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ULL;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebULL;
+  x ^= x >> 31;
+  return x;
+}
+
+// Standard normal test matrix (Box-Muller on a counter-based hash of (seed, index)).
+__global__ void omega_kernel(double* om, int64_t n, uint64_t seed) {
+  const int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t h1 = mix64(seed * 0x9E3779B97F4A7C15ULL + 2 * uint64_t(i) + 1);
+  const uint64_t h2 = mix64(h1 ^ 0xD1B54A32D192ED03ULL);
+  const double u1 = (double(h1 >> 11) + 0.5) * (1.0 / 9007199254740992.0);
+  const double u2 = double(h2 >> 11) * (1.0 / 9007199254740992.0);
+  om[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
+}
+
+}  // namespace
+
+struct FarBlock {
+  int leaf;        // index into plan leaves
+  int m, n, mu;
+  int64_t t_off;   // materialized block in BUF_TILE
+  int l = 0;       // sketch width of the last round
+  int dense = 0;   // 1: QR of T itself (m >= n, l == n)
+  int rank = 0;
+  int done = 0;
+  int round = -1;
+  // pointers into that round's workspace
+  double *Y = nullptr, *Bt = nullptr, *R = nullptr, *W = nullptr, *V = nullptr, *sig = nullptr;
+  double* fro2 = nullptr;
+};
+
+struct hx_ctx {
+  int device = 0;
+  cudaStream_t s = nullptr;
+  DArr<double> own[NUM_BUFS];
+  double* attached[2] = {nullptr, nullptr};
+  int64_t opnd_elems[2] = {0, 0};
+  bool alias = false;
+  DArr<Term> terms[3];
+  DArr<Tile> tiles[3];
+  DArr<Group> groups[3];
+  DArr<double> sumsq, fro2;
+  DArr<int> seg_b, seg_e;
+  DArr<Term> rterms;
+  DArr<Tile> rtiles;
+  DArr<Group> rgroups;
+  DArr<QrJob> qr_jobs;
+  DArr<JacJob> jac_jobs;
+  DArr<SelJob> sel_jobs;
+  DArr<SmallJob> small_jobs;
+  DArr<int> rank_d, retry_d;
+  std::vector<DArr<double>> work;  // one workspace per sketch round
+  int64_t omega_rows = 0;
+  int omega_cols = 0;
+  uint64_t omega_seed = ~0ULL;
+  // results
+  std::vector<int32_t> res_rank;
+  std::vector<int8_t> res_deg;
+  std::vector<int64_t> res_off;
+  int64_t out_far = 0, near_begin = 0, near_elems = 0;
+  int64_t launches = 0;
+  cudaEvent_t ev[8];
+
+  double* buf(int i) {
+    if (i == BUF_A) return attached[0] ? attached[0] : own[BUF_A].p;
+    if (i == BUF_B) {
+      if (alias) return buf(BUF_A);
+      return attached[1] ? attached[1] : own[BUF_B].p;
+    }
+    return own[i].p;
+  }
+  BufPtrs ptrs() {
+    BufPtrs b;
+    for (int i = 0; i < NUM_BUFS; ++i) b.p[i] = buf(i);
+    return b;
+  }
+};
+
+namespace {
+
+void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, const Term* terms,
+                 int n_tiles, const BufPtrs& bp, double* sumsq) {
+  if (n_tiles <= 0) return;
+  if (tile == 32)
+    grouped_gemm_kernel<32><<<n_tiles, 128, 0, c->s>>>(tiles, groups, terms, bp, sumsq, n_tiles);
+  else
+    grouped_gemm_kernel<64><<<n_tiles, 128, 0, c->s>>>(tiles, groups, terms, bp, sumsq, n_tiles);
+  CK(cudaGetLastError());
+  c->launches++;
+}
+
+// Tiles for out (R x C, ld R) = P * Q with a single term.
+void single_term_tiles(std::vector<Term>& terms, std::vector<Tile>& tiles,
+                       std::vector<Group>& groups, const Term& t, uint8_t out_buf,
+                       int64_t out_off, int R, int C) {
+  const int32_t g = int32_t(groups.size());
+  groups.push_back(Group{int32_t(terms.size()), int32_t(terms.size()) + 1});
+  terms.push_back(t);
+  for (int j = 0; j < C; j += 64)
+    for (int i = 0; i < R; i += 64) {
+      Tile tl;
+      std::memset(&tl, 0, sizeof(tl));
+      tl.out_off = out_off + i + int64_t(j) * R;
+      tl.out_ld = R;
+      tl.row0 = i;
+      tl.col0 = j;
+      tl.rows = int16_t(std::min(64, R - i));
+      tl.cols = int16_t(std::min(64, C - j));
+      tl.g_begin = g;
+      tl.g_end = g + 1;
+      tl.aux = -1;
+      tl.out_buf = out_buf;
+      tl.mode = MODE_STORE;
+      tiles.push_back(tl);
+    }
+}
+
+Term mk(uint8_t abuf, int64_t aoff, int32_t ald, uint8_t akc, uint8_t bbuf, int64_t boff,
+        int32_t bld, uint8_t bkc, int32_t k, int32_t rows, int32_t cols) {
+  Term t;
+  t.a_off = aoff;
+  t.b_off = boff;
+  t.a_ld = ald;
+  t.b_ld = bld;
+  t.k = k;
+  t.r_lo = 0;
+  t.c_lo = 0;
+  t.rows = rows;
+  t.cols = cols;
+  t.a_buf = abuf;
+  t.b_buf = bbuf;
+  t.a_kc = akc;
+  t.b_kc = bkc;
+  return t;
+}
+
+void run_gemm_batch(hx_ctx* c, std::vector<Term>& terms, std::vector<Tile>& tiles,
+                    std::vector<Group>& groups) {
+  if (tiles.empty()) return;
+  c->rterms.upload(terms, c->s);
+  c->rtiles.upload(tiles, c->s);
+  c->rgroups.upload(groups, c->s);
+  launch_gemm(c, 64, c->rtiles.p, c->rgroups.p, c->rterms.p, int(tiles.size()), c->ptrs(),
+              nullptr);
+}
+
+void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
+  std::vector<QrJob> sm, gl;
+  size_t smax = 0;
+  for (const QrJob& j : jobs) {
+    const size_t need = size_t(j.p) * j.q * sizeof(double);
+    if (need <= size_t(SMEM_CAP)) {
+      sm.push_back(j);
+      smax = std::max(smax, need);
+    } else {
+      gl.push_back(j);
+    }
+  }
+  if (!sm.empty()) {
+    c->qr_jobs.upload(sm, c->s);
+    CK(cudaFuncSetAttribute(qr_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smax)));
+    qr_explicit_kernel<<<int(sm.size()), LA_THREADS, smax, c->s>>>(c->qr_jobs.p, 1);
+    CK(cudaGetLastError());
+    c->launches++;
+    // the job array is reused below: wait for the first launch's reads
+    if (!gl.empty()) CK(cudaStreamSynchronize(c->s));
+  }
+  if (!gl.empty()) {
+    c->qr_jobs.upload(gl, c->s);
+    qr_explicit_kernel<<<int(gl.size()), LA_THREADS, 0, c->s>>>(c->qr_jobs.p, 0);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+}
+
+void run_jacobi(hx_ctx* c, const std::vector<JacJob>& jobs) {
+  if (jobs.empty()) return;
+  int qmax = 0;
+  for (const JacJob& j : jobs) qmax = std::max(qmax, j.q);
+  const size_t smem = size_t(2) * qmax * qmax * sizeof(double);
+  c->jac_jobs.upload(jobs, c->s);
+  CK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          int(std::max<size_t>(smem, 1))));
+  jacobi_svd_kernel<<<int(jobs.size()), LA_THREADS, smem, c->s>>>(c->jac_jobs.p);
+  CK(cudaGetLastError());
+  c->launches++;
+}
+
+int default_sketch(int mu) {
+  if (mu <= 64) return 16;
+  if (mu <= 128) return 24;
+  if (mu <= 256) return 32;
+  if (mu <= 512) return 40;
+  return 48;
+}
+
+}  // namespace
+
+extern "C" int hx_ctx_create(int device, hx_ctx** out) {
+  return guarded([&]() -> int {
+    if (!out) return fail(HX_EINVAL, "null out");
+    int n = 0;
+    CK(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) return fail(HX_EINVAL, "no such CUDA device");
+    CK(cudaSetDevice(device));
+    auto* c = new hx_ctx();
+    c->device = device;
+    CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    *out = c;
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_ctx_operand(hx_ctx* c, int which, const double* host, const double* device,
+                              int64_t n) {
+  return guarded([&]() -> int {
+    if (!c || which < 0 || which > 1 || n < 0) return fail(HX_EINVAL, "bad operand arguments");
+    CK(cudaSetDevice(c->device));
+    if (which == 1) c->alias = false;
+    if (host) {
+      c->attached[which] = nullptr;
+      c->own[which].ensure(size_t(n));
+      CK(cudaMemcpyAsync(c->own[which].p, host, size_t(n) * sizeof(double),
+                         cudaMemcpyHostToDevice, c->s));
+    } else if (device) {
+      c->attached[which] = const_cast<double*>(device);
+    } else {
+      return fail(HX_EINVAL, "need a host or a device pool");
+    }
+    c->opnd_elems[which] = n;
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_ctx_operand_alias(hx_ctx* c) {
+  if (!c) return fail(HX_EINVAL, "null ctx");
+  c->alias = true;
+  c->opnd_elems[1] = c->opnd_elems[0];
+  return HX_OK;
+}
+
+extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg,
+                          hx_product_stats* st) {
+  return guarded([&]() -> int {
+    if (!c || !P || !cfg) return fail(HX_EINVAL, "null argument");
+    if (cfg->policy == 0 && !(cfg->eps > 0.0)) return fail(HX_EINVAL, "eps must be positive");
+    if (cfg->policy == 1 && cfg->k_max < 1) return fail(HX_EINVAL, "k_max must be >= 1");
+    if (!c->buf(BUF_A) || !c->buf(BUF_B)) return fail(HX_EINVAL, "operands not set");
+    CK(cudaSetDevice(c->device));
+    const int over = cfg->oversample > 0 ? cfg->oversample : 6;
+    c->launches = 0;
+    cudaStream_t s = c->s;
+    CK(cudaEventRecord(c->ev[0], s));
+
+    // ---- plan upload and buffers
+    const std::vector<Term>* T3[3] = {&P->core_terms, &P->fac_terms, &P->mat_terms};
+    const std::vector<Tile>* L3[3] = {&P->core_tiles, &P->fac_tiles, &P->mat_tiles};
+    const std::vector<Group>* G3[3] = {&P->core_groups, &P->fac_groups, &P->mat_groups};
+    for (int i = 0; i < 3; ++i) {
+      c->terms[i].upload(*T3[i], s);
+      c->tiles[i].upload(*L3[i], s);
+      c->groups[i].upload(*G3[i], s);
+    }
+    c->own[BUF_CORE].ensure(size_t(P->core_elems));
+    c->own[BUF_TERM].ensure(size_t(P->term_elems));
+    c->own[BUF_TILE].ensure(size_t(P->tile_elems));
+    c->sumsq.ensure(size_t(P->n_sumsq));
+    BufPtrs bp = c->ptrs();
+
+    // ---- 1. term formation
+    launch_gemm(c, P->tile, c->tiles[0].p, c->groups[0].p, c->terms[0].p,
+                int(P->core_tiles.size()), bp, nullptr);
+    launch_gemm(c, P->tile, c->tiles[1].p, c->groups[1].p, c->terms[1].p,
+                int(P->fac_tiles.size()), bp, nullptr);
+    CK(cudaEventRecord(c->ev[1], s));
+    // ---- 2. materialization
+    launch_gemm(c, P->tile, c->tiles[2].p, c->groups[2].p, c->terms[2].p,
+                int(P->mat_tiles.size()), bp, c->sumsq.p);
+    CK(cudaEventRecord(c->ev[2], s));
+
+    // ---- per-leaf squared Frobenius norms
+    const int nl = int(P->leaves.size());
+    std::vector<int> sb(nl), se(nl);
+    for (int i = 0; i < nl; ++i) {
+      sb[i] = P->leaves[i].sumsq_begin;
+      se[i] = P->leaves[i].sumsq_end;
+    }
+    c->seg_b.upload(sb, s);
+    c->seg_e.upload(se, s);
+    c->fro2.ensure(size_t(std::max(nl, 1)));
+    if (nl) {
+      segment_sum_kernel<<<(nl + 255) / 256, 256, 0, s>>>(c->sumsq.p, c->seg_b.p, c->seg_e.p,
+                                                          c->fro2.p, nl);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+
+    // ---- 3. recompression of far leaves
+    std::vector<FarBlock> fb;
+    int mu_max = 0;
+    for (int i = 0; i < nl; ++i) {
+      const OutLeaf& L = P->leaves[i];
+      if (L.kind != 1) continue;
+      FarBlock f;
+      f.leaf = i;
+      f.m = L.m;
+      f.n = L.n;
+      f.mu = std::min(L.m, L.n);
+      f.t_off = L.ws_off;
+      f.fro2 = c->fro2.p + i;
+      fb.push_back(f);
+      mu_max = std::max(mu_max, f.mu);
+    }
+    int64_t nmax = 1;
+    for (const FarBlock& f : fb) nmax = std::max<int64_t>(nmax, f.n);
+    const int lcap = JAC_QMAX;
+    if (c->omega_rows < nmax || c->omega_cols < lcap || c->omega_seed != cfg->seed) {
+      c->omega_rows = std::max<int64_t>(nmax, c->omega_rows);
+      c->omega_cols = lcap;
+      c->omega_seed = cfg->seed;
+      const int64_t ne = c->omega_rows * c->omega_cols;
+      c->own[BUF_OMEGA].ensure(size_t(ne));
+      omega_kernel<<<int((ne + 255) / 256), 256, 0, s>>>(c->own[BUF_OMEGA].p, ne, cfg->seed);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+    int64_t matvecs = 0;
+    int rounds = 0;
+    std::vector<int> active;
+    for (int i = 0; i < int(fb.size()); ++i) active.push_back(i);
+    while (!active.empty()) {
+      if (rounds >= 6) throw std::runtime_error("sketch adaptation did not converge");
+      // sketch widths for this round
+      int64_t wsz = 0;
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        int l;
+        if (cfg->policy == 1) {
+          l = std::min(f.mu, cfg->k_max + over);
+        } else if (f.l == 0) {
+          l = cfg->sketch0 > 0 ? cfg->sketch0 : default_sketch(f.mu);
+        } else {
+          l = 2 * f.l;
+        }
+        l = std::min(l, f.mu);
+        if (l > lcap) {
+          if (f.mu <= lcap) l = f.mu;
+          else throw hx::Unsupported("block needs a sketch wider than " + std::to_string(lcap));
+        }
+        f.l = l;
+        f.dense = (f.m >= f.n && l == f.n) ? 1 : 0;
+        f.round = rounds;
+        const int64_t q = l;
+        wsz += (f.dense ? 0 : (int64_t(f.m) + f.n) * q) + 3 * q * q + q + 64;
+      }
+      if (int(c->work.size()) <= rounds) c->work.resize(rounds + 1);
+      c->work[rounds].ensure(size_t(wsz));
+      double* wb = c->work[rounds].p;
+      c->own[BUF_WORK].p = wb;  // buffer id BUF_WORK points at this round's workspace
+      bp = c->ptrs();
+      int64_t pos = 0;
+      auto take = [&](int64_t nelem) {
+        double* p = wb + pos;
+        pos += (nelem + 15) & ~int64_t(15);
+        return p;
+      };
+      std::vector<Term> tt;
+      std::vector<Tile> tl;
+      std::vector<Group> tg;
+      std::vector<QrJob> qj;
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        const int l = f.l;
+        if (f.dense) {
+          f.Y = c->buf(BUF_TILE) + f.t_off;  // QR in place of the materialized block
+          f.Bt = nullptr;
+        } else {
+          f.Y = take(int64_t(f.m) * l);
+          f.Bt = take(int64_t(f.n) * l);
+        }
+        f.R = take(int64_t(l) * l);
+        f.W = take(int64_t(l) * l);
+        f.V = take(int64_t(l) * l);
+        f.sig = take(l);
+        if (!f.dense) {
+          // Y = T * Omega[:, :l]
+          single_term_tiles(tt, tl, tg,
+                            mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows),
+                               1, f.n, f.m, l),
+                            BUF_WORK, int64_t(f.Y - wb), f.m, l);
+          matvecs += 2 * l;
+        } else {
+          matvecs += f.n;
+        }
+        qj.push_back(QrJob{f.Y, f.R, f.m, f.dense ? f.n : l});
+      }
+      run_gemm_batch(c, tt, tl, tg);
+      run_qr(c, qj);
+      // Bt = T^T Q for sketched blocks, then QR(Bt)
+      tt.clear();
+      tl.clear();
+      tg.clear();
+      qj.clear();
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        if (f.dense) continue;
+        single_term_tiles(tt, tl, tg,
+                          mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, int64_t(f.Y - wb), f.m, 1, f.m,
+                             f.n, f.l),
+                          BUF_WORK, int64_t(f.Bt - wb), f.n, f.l);
+        qj.push_back(QrJob{f.Bt, f.R, f.n, f.l});
+      }
+      if (!tl.empty()) CK(cudaStreamSynchronize(s));  // rterms reused
+      run_gemm_batch(c, tt, tl, tg);
+      run_qr(c, qj);
+      // SVD of the small factor
+      std::vector<JacJob> jj;
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        jj.push_back(JacJob{f.R, f.sig, f.W, f.V, f.l});
+      }
+      run_jacobi(c, jj);
+      // rank selection
+      std::vector<SelJob> sj;
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        sj.push_back(SelJob{f.sig, f.fro2, f.l, f.mu, (f.dense || f.l == f.mu) ? 1 : 0});
+      }
+      const int na = int(active.size());
+      c->sel_jobs.upload(sj, s);
+      c->rank_d.ensure(size_t(na));
+      c->retry_d.ensure(size_t(na));
+      select_rank_kernel<<<(na + 127) / 128, 128, 0, s>>>(c->sel_jobs.p, na, cfg->policy,
+                                                          cfg->eps, cfg->k_max, over,
+                                                          c->rank_d.p, c->retry_d.p);
+      CK(cudaGetLastError());
+      c->launches++;
+      std::vector<int> rk(na), rt(na);
+      CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(rt.data(), c->retry_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      std::vector<int> next;
+      for (int a = 0; a < na; ++a) {
+        FarBlock& f = fb[active[a]];
+        f.rank = rk[a];
+        if (rt[a] && f.l < f.mu) next.push_back(active[a]);
+        else f.done = 1;
+      }
+      active.swap(next);
+      ++rounds;
+    }
+    CK(cudaEventRecord(c->ev[3], s));
+
+    // ---- 4. output factors
+    const int nf = int(fb.size());
+    c->res_rank.assign(nl, -1);
+    c->res_deg.assign(nl, 0);
+    c->res_off.assign(nl, 0);
+    int64_t pos = 0;
+    int64_t max_rank = 0;
+    for (const FarBlock& f : fb) {
+      c->res_rank[f.leaf] = f.rank;
+      c->res_off[f.leaf] = pos;
+      pos += int64_t(f.m + f.n) * f.rank;
+      max_rank = std::max<int64_t>(max_rank, f.rank);
+    }
+    c->out_far = pos;
+    c->own[BUF_OUT].ensure(size_t(std::max<int64_t>(pos, 1)));
+    double* out = c->own[BUF_OUT].p;
+    std::vector<SmallJob> jl;
+    int qmax = 1;
+    int rows_max = 1;
+    for (const FarBlock& f : fb) {
+      if (f.rank == 0) continue;
+      double* left = out + c->res_off[f.leaf];
+      double* right = left + int64_t(f.m) * f.rank;
+      if (f.dense) {
+        jl.push_back(SmallJob{f.Y, f.W, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
+        jl.push_back(SmallJob{nullptr, f.V, nullptr, right, f.n, f.l, f.l, 0, f.rank});
+      } else {
+        jl.push_back(SmallJob{f.Y, f.V, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
+        jl.push_back(SmallJob{f.Bt, f.W, nullptr, right, f.n, f.l, f.l, f.n, f.rank});
+      }
+      qmax = std::max(qmax, f.l);
+      rows_max = std::max(rows_max, std::max(f.m, f.n));
+    }
+    if (!jl.empty()) {
+      c->small_jobs.upload(jl, s);
+      const size_t smem = size_t(qmax) * qmax * sizeof(double);
+      CK(cudaFuncSetAttribute(small_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              int(smem)));
+      dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
+      small_product_kernel<<<grid, 128, smem, s>>>(c->small_jobs.p);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+    // near leaves: payload stays in BUF_TILE after the far blocks
+    c->near_begin = P->near_ws_begin;
+    c->near_elems = P->tile_elems - P->near_ws_begin;
+    for (int i = 0; i < nl; ++i) {
+      const OutLeaf& L = P->leaves[i];
+      if (L.kind == 2) c->res_off[i] = c->out_far + (L.ws_off - P->near_ws_begin);
+    }
+    CK(cudaEventRecord(c->ev[4], s));
+    CK(cudaEventSynchronize(c->ev[4]));
+
+    if (st) {
+      std::memset(st, 0, sizeof(*st));
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]));
+      st->ms_total = ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      st->ms_form = ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
+      st->ms_mat = ms;
+      st->dom_kernel_ms = ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[2], c->ev[4]));
+      st->ms_recompress = ms;
+      st->far_leaves = nf;
+      st->near_leaves = nl - nf;
+      st->degraded_blocks = 0;
+      st->max_far_rank = max_rank;
+      st->matvec_count = matvecs;
+      st->sketch_rounds = rounds;
+      st->launches = c->launches;
+      st->out_elems = c->out_far + c->near_elems;
+      std::vector<double> f2(nl);
+      if (nl)
+        CK(cudaMemcpy(f2.data(), c->fro2.p, nl * sizeof(double), cudaMemcpyDeviceToHost));
+      double tot = 0;
+      for (double v : f2) tot += v;
+      st->fro2_total = tot;
+    }
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_result_layout(hx_ctx* c, int32_t* rank, int8_t* degraded, int64_t* offset) {
+  if (!c) return fail(HX_EINVAL, "null ctx");
+  const size_t n = c->res_rank.size();
+  if (rank) std::copy(c->res_rank.begin(), c->res_rank.end(), rank);
+  if (degraded) std::copy(c->res_deg.begin(), c->res_deg.end(), degraded);
+  if (offset) std::copy(c->res_off.begin(), c->res_off.end(), offset);
+  (void)n;
+  return HX_OK;
+}
+
+extern "C" int hx_result_download(hx_ctx* c, double* host, int64_t n) {
+  return guarded([&]() -> int {
+    if (!c || !host) return fail(HX_EINVAL, "null argument");
+    if (n < c->out_far + c->near_elems) return fail(HX_EINVAL, "result buffer too small");
+    CK(cudaSetDevice(c->device));
+    if (c->out_far)
+      CK(cudaMemcpyAsync(host, c->own[BUF_OUT].p, size_t(c->out_far) * sizeof(double),
+                         cudaMemcpyDeviceToHost, c->s));
+    if (c->near_elems)
+      CK(cudaMemcpyAsync(host + c->out_far, c->own[BUF_TILE].p + c->near_begin,
+                         size_t(c->near_elems) * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_operand_download(hx_ctx* c, int which, double* host, int64_t n) {
+  return guarded([&]() -> int {
+    if (!c || !host || which < 0 || which > 1) return fail(HX_EINVAL, "bad arguments");
+    if (n > c->opnd_elems[which]) return fail(HX_EINVAL, "more elements than the pool holds");
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemcpyAsync(host, c->buf(which), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->s));
+    CK(cudaStreamSynchronize(c->s));
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_ctx_synchronize(hx_ctx* c) {
+  return guarded([&]() -> int {
+    if (!c) return fail(HX_EINVAL, "null ctx");
+    CK(cudaStreamSynchronize(c->s));
+    return HX_OK;
+  });
+}
+
+extern "C" void hx_ctx_free(hx_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->s);
+  for (auto& b : c->own) {
+    if (&b == &c->own[BUF_WORK]) continue;  // points into work[]
+    b.release();
+  }
+  for (auto& w : c->work) w.release();
+  for (int i = 0; i < 3; ++i) {
+    c->terms[i].release();
+    c->tiles[i].release();
+    c->groups[i].release();
+  }
+  c->sumsq.release();
+  c->fro2.release();
+  c->seg_b.release();
+  c->seg_e.release();
+  c->rterms.release();
+  c->rtiles.release();
+  c->rgroups.release();
+  c->qr_jobs.release();
+  c->jac_jobs.release();
+  c->sel_jobs.release();
+  c->small_jobs.release();
+  c->rank_d.release();
+  c->retry_d.release();
+  for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaStreamDestroy(c->s);
+  delete c;
+}

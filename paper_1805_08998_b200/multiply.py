@@ -1,0 +1,223 @@
+"""The tolerance-controlled H x H product on the B200 (drop-in for ``hmat.multiply``).
+
+``hmult_new(h, k, cfg)`` keeps the reference signature, checks and errors
+(``multiply.py:252-256``, ``sumexpr.py:80-81``, ``multiply.py:41-47``) and returns an
+``HMatrix`` on the same block tree whose far leaves are ``LowRank(U S, V)`` and near
+leaves dense, with ``.report`` filled like ``MultReport`` (``multiply.py:50-58``).
+
+All arithmetic runs in ``libhx.so`` (``include/hx.h``): the flat term lists are built by
+the C++ planner (the ``restrict`` bookkeeping), then term formation, block
+materialization and recompression run as sm_100a kernels.  There is no CPU path: a
+missing library or GPU raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import time
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .compressors import TAG_CODES, CompressorKind, clamp_eps
+from .hmatrix import HMatrix, block_arrays, pack_operand, tree_arrays
+from .lowrank import EpsRank, FixedRank, LowRank
+
+CONVERTERS = ("hier-approx", "aca", "bilanczos", "randomized", "dense-svd")
+
+
+@dataclass(frozen=True)
+class MultiplyConfig:
+    mode: str = "new"
+    compressor: CompressorKind = CompressorKind("aca")
+    policy: object = None
+    converter: str = "hier-approx"
+
+    def __post_init__(self):
+        if self.mode not in ("new", "traditional"):
+            raise ValueError(f"unknown mode {self.mode!r}")
+        if self.converter not in CONVERTERS:
+            raise ValueError(f"unknown converter {self.converter!r}")
+        if self.policy is None:
+            raise ValueError("a truncation policy is required")
+
+
+@dataclass
+class MultReport:
+    degraded_blocks: int = 0
+    max_far_rank: int = 0
+    matvec_count: int = 0
+    far_leaves: int = 0
+    near_leaves: int = 0
+    wall_s: float = 0.0
+    warnings: list = field(default_factory=list)
+    # device-side breakdown (milliseconds, CUDA events) and plan statistics
+    plan_ms: float = 0.0
+    device_ms: float = 0.0
+    form_ms: float = 0.0
+    materialize_ms: float = 0.0
+    recompress_ms: float = 0.0
+    sketch_rounds: int = 0
+    launches: int = 0
+    fro2: float = 0.0
+
+
+class Device:
+    """One ``hx_ctx`` per CUDA device, created lazily and reused across products."""
+
+    _cache: dict = {}
+
+    def __init__(self, device=0):
+        h = C.c_void_p()
+        _lib.check(_lib.lib().hx_ctx_create(int(device), C.byref(h)), "hx_ctx_create")
+        self.h = h
+        self.device = device
+
+    @classmethod
+    def get(cls, device=0):
+        if device not in cls._cache:
+            cls._cache[device] = Device(device)
+        return cls._cache[device]
+
+    def set_operand(self, which, pool=None, dev_ptr=None, n=None):
+        if pool is not None:
+            pool = np.ascontiguousarray(pool, dtype=np.float64)
+            _lib.check(_lib.lib().hx_ctx_operand(self.h, which, _lib.ptr(pool, _lib.f64p), None,
+                                                 pool.size), "hx_ctx_operand")
+        else:
+            _lib.check(_lib.lib().hx_ctx_operand(self.h, which, None, C.c_void_p(dev_ptr),
+                                                 int(n)), "hx_ctx_operand")
+
+    def alias_b(self):
+        _lib.check(_lib.lib().hx_ctx_operand_alias(self.h), "hx_ctx_operand_alias")
+
+
+def _policy_args(policy):
+    if isinstance(policy, FixedRank) or hasattr(policy, "k_max"):
+        return 1, 1.0, int(policy.k_max)
+    eps = float(policy.eps)
+    if not eps > 0.0:
+        raise ValueError("eps must be positive")
+    return 0, eps, 0
+
+
+def operand_directory(h):
+    """(pool, directory) of an operand, cached on the object (operands are immutable
+    inputs of the product)."""
+    cached = getattr(h, "_hx_packed", None)
+    if cached is None:
+        cached = pack_operand(h)
+        try:
+            h._hx_packed = cached
+        except AttributeError:  # pragma: no cover
+            pass
+    return cached
+
+
+def plan_tile(bct):
+    arr = block_arrays(bct)
+    tr = arr.tree
+    leaf = tr.child[:, 0] < 0
+    nmin = int((tr.hi - tr.lo)[leaf].max())
+    return 32 if nmin <= 32 else 64
+
+
+def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0):
+    """Run the product on one GPU; returns (HMatrix, MultReport)."""
+    if h.bct is not k.bct:
+        raise ValueError("factors must live on the same block-cluster tree")
+    policy = cfg.policy
+    kind, eps, kmax = _policy_args(policy)
+    warn = []
+    if kind == 0 and eps <= np.finfo(float).eps:
+        with warnings.catch_warnings(record=True) as wl:
+            warnings.simplefilter("always")
+            eps = clamp_eps(eps)
+        for w in wl:
+            warnings.warn(w.message)
+    t_start = time.perf_counter()
+    pool_a, dir_a = operand_directory(h)
+    same = k is h
+    pool_b, dir_b = (pool_a, dir_a) if same else operand_directory(k)
+    dev = Device.get(device)
+    t0 = time.perf_counter()
+    plan = _lib.Plan(tree_arrays(h.bct), dir_a, dir_a if same else dir_b, leaf_mask,
+                     plan_tile(h.bct))
+    plan_ms = (time.perf_counter() - t0) * 1e3
+    dev_a = getattr(h, "_hx_device", None)
+    if dev_a is not None and dev_a[0] == device:
+        dev.set_operand(0, dev_ptr=dev_a[1], n=dev_a[2])
+    else:
+        dev.set_operand(0, pool=pool_a)
+    if same:
+        dev.alias_b()
+    else:
+        dev_b = getattr(k, "_hx_device", None)
+        if dev_b is not None and dev_b[0] == device:
+            dev.set_operand(1, dev_ptr=dev_b[1], n=dev_b[2])
+        else:
+            dev.set_operand(1, pool=pool_b)
+    comp = cfg.compressor
+    pc = _lib.HxProductCfg(kind, eps, kmax, TAG_CODES[comp.tag], int(comp.seed) & (2**64 - 1),
+                           int(sketch0), int(oversample))
+    st = _lib.HxProductStats()
+    _lib.check(_lib.lib().hx_product(dev.h, plan.h, C.byref(pc), C.byref(st)), "hx_product")
+    leaves = plan.leaves()
+    nl = len(leaves["ids"])
+    rank = np.zeros(nl, np.int32)
+    deg = np.zeros(nl, np.int8)
+    off = np.zeros(nl, np.int64)
+    _lib.check(_lib.lib().hx_result_layout(dev.h, _lib.ptr(rank, _lib.i32p),
+                                           _lib.ptr(deg, _lib.i8p), _lib.ptr(off, _lib.i64p)),
+               "hx_result_layout")
+    res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
+    _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p), res.size),
+               "hx_result_download")
+    data = {}
+    degraded = set()
+    ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
+    kinds = leaves["kind"].tolist()
+    rl, ol = rank.tolist(), off.tolist()
+    for i in range(nl):
+        m, n, o = ms[i], ns[i], ol[i]
+        if kinds[i] == 1:
+            r = rl[i]
+            left = res[o:o + m * r].reshape(r, m).T
+            right = res[o + m * r:o + (m + n) * r].reshape(r, n).T
+            data[ids[i]] = LowRank(left, right)
+            if deg[i]:
+                degraded.add(ids[i])
+        else:
+            data[ids[i]] = res[o:o + m * n].reshape(n, m).T
+    rep = MultReport()
+    rep.degraded_blocks = int(st.degraded_blocks)
+    rep.max_far_rank = int(st.max_far_rank)
+    rep.matvec_count = int(st.matvec_count)
+    rep.far_leaves = int(st.far_leaves)
+    rep.near_leaves = int(st.near_leaves)
+    rep.warnings = warn
+    rep.plan_ms = plan_ms
+    rep.device_ms = st.ms_total
+    rep.form_ms = st.ms_form
+    rep.materialize_ms = st.ms_mat
+    rep.recompress_ms = st.ms_recompress
+    rep.sketch_rounds = int(st.sketch_rounds)
+    rep.launches = int(st.launches)
+    rep.fro2 = float(st.fro2_total)
+    rep.wall_s = time.perf_counter() - t_start
+    out = HMatrix(h.bct, data, degraded)
+    out.report = rep
+    out.plan_info = plan.info
+    out.plan_leaves = leaves
+    out.leaf_rank = rank
+    plan.close()
+    return out
+
+
+def hmult_new(h, k, cfg):
+    """Product H K with one direct compression per farfield leaf (GPU)."""
+    if cfg.mode != "new":
+        raise ValueError("config mode must be 'new'")
+    return multiply_device(h, k, cfg)

@@ -1,0 +1,80 @@
+"""CPU checks of the C-ABI library: it loads, exports every symbol of include/hx.h, and
+the planner (pure host code) reproduces the reference's restrict term log."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import hmat_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    text = open(os.path.join(ROOT, "include", "hx.h")).read()
+    return sorted(set(re.findall(r"\b(hx_[a-z_]+)\s*\(", text)))
+
+
+def test_library_exports_header_symbols():
+    from paper_1805_08998_b200 import _lib
+
+    L = _lib.lib()
+    names = _declared()
+    assert "hx_product" in names and "hx_plan_create" in names
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert L.hx_version() == 1
+
+
+def _plan_case(g, n_min_tile=None):
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import _lib, hmatrix, multiply
+
+    n, n_min, eta, eps_a, tol = g["params"]
+    pts = g["points"]
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, int(n_min)), eta)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, int(n_min)), eta)
+    A = O.assemble_o("exp", obt, O.Eps(eps_a), pts)
+    H = hx.HMatrix(bct, A.data)
+    pool, d = hmatrix.pack_operand(H)
+    plan = _lib.Plan(hmatrix.tree_arrays(bct), d, d, tile=multiply.plan_tile(bct))
+    return bct, A, plan, tol
+
+
+@pytest.mark.parametrize("name", ["small2d.npz", pytest.param("cfg1.npz", marks=pytest.mark.slow)])
+def test_plan_term_log_matches_restrict(golden, name):
+    g = golden(name)
+    bct, A, plan, tol = _plan_case(g)
+    log = []
+    O.hmult_new_o(A, A, O.Eps(tol), "dense-svd", log=log)
+    kmap = {"FF": 0, "FX": 1, "XF": 2}
+    ref = np.array([(c, kmap[k], a, b, r) for (c, k, a, b, r) in log], dtype=np.int64)
+    L = plan.term_log()
+    mine = np.stack([L["block"], L["kind"], L["a"], L["b"], L["rank"]], axis=1)
+    assert mine.shape == ref.shape
+    assert np.array_equal(mine, ref)
+    info = plan.info
+    assert info.n_far == int(np.sum(bct.kind_code == 1))
+    assert info.n_near == int(np.sum(bct.kind_code == 2))
+
+
+def test_plan_canonical_model_cfg1(golden):
+    # cfg1 term formation 1.98 GFLOP / 1.29 GB, near 1.73 GFLOP / 0.44 GB
+    bct, A, plan, tol = _plan_case(golden("cfg1.npz"))
+    info = plan.info
+    assert abs(info.flops_form / 1e9 - 1.98) < 0.01
+    assert abs(info.bytes_form / 1e9 - 1.29) < 0.01
+    assert abs(info.flops_near / 1e9 - 1.73) < 0.01
+    assert abs(info.bytes_near / 1e9 - 0.44) < 0.01
+
+
+def test_plan_rejects_bad_arguments():
+    from paper_1805_08998_b200 import _lib
+
+    import ctypes as C
+    h = C.c_void_p()
+    rc = _lib.lib().hx_plan_create(None, None, None, None, 64, C.byref(h))
+    assert rc == -1
+    assert "null" in _lib.last_error()

@@ -1,0 +1,120 @@
+"""GPU parity of the H x H product against the oracle / reference golden fixtures.
+
+Parity contract (BASELINE.json north_star):
+  * ||C - A B||_F / ||A B||_F <= tol
+  * far-block ranks within +-1 of the oracle (dense-svd and aca oracles)
+  * block-wise ||C_b - C_b^oracle||_F / ||C_b^oracle||_F <= 10 tol
+  * near blocks: exact evaluation, relative difference <= 1e-12
+"""
+
+import numpy as np
+import pytest
+
+from oracle import hmat_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+CFG_KERNELS = {"small2d.npz": ("exp", None), "cfg1.npz": ("exp", None),
+               "ragged3d.npz": ("exp0.5", "inv")}
+
+
+def _operands(g, name):
+    import paper_1805_08998_b200 as hx
+
+    ka, kb = CFG_KERNELS[name]
+    n, n_min, eta, eps_a, tol = g["params"]
+    n, n_min = int(n), int(n_min)
+    pts = g["points"]
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, n_min), eta)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, n_min), eta)
+    h = n ** (-1.0 / 3.0)
+    oa = O.assemble_o(ka, obt, O.Eps(eps_a), pts, h)
+    ob = oa if kb is None else O.assemble_o(kb, obt, O.Eps(eps_a), pts, h)
+    A = hx.HMatrix(bct, oa.data, oa.degraded)
+    B = A if kb is None else hx.HMatrix(bct, ob.data, ob.degraded)
+    return bct, A, B, oa, ob, float(tol)
+
+
+def _leaf_dense(p):
+    return p.left @ p.right.T if hasattr(p, "left") else p
+
+
+@pytest.mark.parametrize("name", ["small2d.npz", "cfg1.npz"])
+@pytest.mark.parametrize("tag", ["dense-svd", "aca"])
+def test_product_parity(golden, name, tag):
+    import paper_1805_08998_b200 as hx
+
+    g = golden(name)
+    bct, A, B, oa, ob, tol = _operands(g, name)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(tag), policy=hx.EpsRank(tol))
+    C = hx.hmult_new(A, B, cfg)
+    leaf_ids = g[f"{tag}/ids"]
+    ranks_ref = g[f"{tag}/ranks"]
+    fros_ref = g[f"{tag}/fros"]
+    # ranks within +-1, Frobenius norms of all blocks close
+    for b, r_ref, f_ref in zip(leaf_ids, ranks_ref, fros_ref):
+        p = C.data[int(b)]
+        if r_ref >= 0:
+            assert abs(p.rank - r_ref) <= 1, (b, p.rank, r_ref)
+            fro = p.norm()
+        else:
+            fro = np.linalg.norm(p)
+        assert abs(fro - f_ref) <= 10 * tol * max(f_ref, 1e-300) + 1e-300, (b, fro, f_ref)
+    # block-wise difference on the stored blocks
+    dense_ref = g.get(f"{tag}/dense")
+    lo, hi = bct.tree.lo, bct.tree.hi
+    for b in leaf_ids:
+        b = int(b)
+        t, s = bct.tau[b], bct.sigma[b]
+        if dense_ref is not None:
+            ref = dense_ref[lo[t]:hi[t], lo[s]:hi[s]]
+        elif f"{tag}/blk{b}" in g:
+            ref = g[f"{tag}/blk{b}"]
+        else:
+            continue
+        val = _leaf_dense(C.data[b])
+        nref = np.linalg.norm(ref)
+        limit = 10 * tol if hasattr(C.data[b], "left") else 1e-12
+        assert np.linalg.norm(val - ref) <= limit * max(nref, 1e-300), b
+    # global error against the exact product of the assembled operands
+    exact = oa.to_dense() @ ob.to_dense()
+    err = np.linalg.norm(hx.to_dense(C) - exact) / np.linalg.norm(exact)
+    assert err <= tol, err
+    rep = C.report
+    assert rep.far_leaves == int(np.sum(ranks_ref >= 0))
+    assert rep.near_leaves == int(np.sum(ranks_ref < 0))
+    assert rep.launches > 0
+
+
+def test_fixed_rank_policy(golden):
+    import paper_1805_08998_b200 as hx
+
+    g = golden("small2d.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "small2d.npz")
+    C = hx.hmult_new(A, B, hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"),
+                                             policy=hx.FixedRank(3)))
+    ref = O.hmult_new_o(oa, ob, O.Fixed(3), "dense-svd")
+    for b, p in ref.data.items():
+        q = C.data[b]
+        if isinstance(p, O.LR):
+            assert q.rank == p.rank
+            d = np.linalg.norm(q.to_dense() - p.dense())
+            # top-3 subspace of the exact block: the sketch is exact for these small blocks
+            assert d <= 1e-8 * max(np.linalg.norm(p.dense()), 1e-300)
+        else:
+            assert np.linalg.norm(q - p) <= 1e-12 * np.linalg.norm(p)
+
+
+def test_ragged_tree_reports_unsupported(golden):
+    import paper_1805_08998_b200 as hx
+
+    g = golden("ragged3d.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "ragged3d.npz")
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    try:
+        C = hx.hmult_new(A, B, cfg)
+    except NotImplementedError:
+        return
+    exact = oa.to_dense() @ ob.to_dense()
+    err = np.linalg.norm(hx.to_dense(C) - exact) / np.linalg.norm(exact)
+    assert err <= tol
