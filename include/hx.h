@@ -141,15 +141,19 @@ int hx_result_download(hx_ctx* ctx, double* host, int64_t n_elems);
 
 /* ---- GPU operand assembly (assemble_hmatrix, hmatrix.py:97-118) ----------------------
  * points: [n x dim] row-major in TREE order (points[perm]); kernel: 0 exp(-r),
- * 1 exp(-r/0.5), 2 exp(-r^2/0.1), 3 1/(r+h).  Far leaves by ACA at eps (with the
- * eps/2 SVD recompression of compressors.py:245-246), near leaves dense.  The packed
- * pool stays on the device as operand `which`; offsets/ranks/flags are returned. */
-int hx_assemble(hx_ctx* ctx, int which, const hx_tree* tree, const double* points,
-                int dim, int kernel, double h, double eps, int8_t* payload,
-                int32_t* rank, int64_t* u_off, int64_t* v_off, int64_t* d_off,
+ * 1 exp(-r/0.5), 2 exp(-r^2/0.1), 3 1/(r+h).  Far leaves by partially pivoted ACA at eps
+ * (compressors.py:162-247, with its eps/2 SVD recompression :245-246; a block whose ACA
+ * cannot certify convergence falls back to dense storage and is flagged), near leaves
+ * dense.  The packed pool (hx_operand layout) is allocated on the device and returned in
+ * *pool_dev; per-node payload/rank/offsets/degraded flags are written to host arrays of
+ * length tree->n_nodes.  Free the pool with hx_pool_free. */
+int hx_assemble(hx_ctx* ctx, const hx_tree* tree, const double* points, int dim, int kernel,
+                double h, double eps, int8_t* payload, int32_t* rank, int64_t* u_off,
+                int64_t* v_off, int64_t* d_off, int8_t* degraded, double** pool_dev,
                 int64_t* pool_elems);
-/* Copy `n_elems` of operand `which`'s device pool to host memory. */
-int hx_operand_download(hx_ctx* ctx, int which, double* host, int64_t n_elems);
+/* Copy n_elems doubles of a library-allocated device pool to host memory. */
+int hx_pool_download(hx_ctx* ctx, const double* pool_dev, double* host, int64_t n_elems);
+int hx_pool_free(hx_ctx* ctx, double* pool_dev);
 
 int hx_ctx_synchronize(hx_ctx* ctx);
 void hx_ctx_free(hx_ctx* ctx);

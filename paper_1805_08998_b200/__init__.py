@@ -14,5 +14,6 @@ from .compressors import CompressorKind
 from .hmatrix import HMatrix, frobenius_norm, to_dense
 from .lowrank import EpsRank, FixedRank, LowRank, select_rank, zero_lowrank
 from .multiply import MultiplyConfig, MultReport, hmult_new
+from .assembly import KERNELS, assemble_hmatrix
 
 __version__ = "0.1.0"

@@ -78,9 +78,10 @@ SIGNATURES = {
                    C.POINTER(HxProductStats)],
     "hx_result_layout": [C.c_void_p, i32p, i8p, i64p],
     "hx_result_download": [C.c_void_p, f64p, C.c_int64],
-    "hx_assemble": [C.c_void_p, C.c_int, C.POINTER(HxTree), f64p, C.c_int, C.c_int,
-                    C.c_double, C.c_double, i8p, i32p, i64p, i64p, i64p, i64p],
-    "hx_operand_download": [C.c_void_p, C.c_int, f64p, C.c_int64],
+    "hx_assemble": [C.c_void_p, C.POINTER(HxTree), f64p, C.c_int, C.c_int, C.c_double,
+                    C.c_double, i8p, i32p, i64p, i64p, i64p, i8p, C.POINTER(C.c_void_p), i64p],
+    "hx_pool_download": [C.c_void_p, C.c_void_p, f64p, C.c_int64],
+    "hx_pool_free": [C.c_void_p, C.c_void_p],
     "hx_ctx_synchronize": [C.c_void_p],
     "hx_ctx_free": [C.c_void_p],
     "hx_last_error": [C.c_char_p, C.c_size_t],

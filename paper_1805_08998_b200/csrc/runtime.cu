@@ -119,6 +119,7 @@ struct hx_ctx {
   DArr<SmallJob> small_jobs;
   DArr<int> rank_d, retry_d;
   std::vector<DArr<double>> work;  // one workspace per sketch round
+  std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
   int64_t omega_rows = 0;
   int omega_cols = 0;
   uint64_t omega_seed = ~0ULL;
@@ -632,18 +633,6 @@ extern "C" int hx_result_download(hx_ctx* c, double* host, int64_t n) {
   });
 }
 
-extern "C" int hx_operand_download(hx_ctx* c, int which, double* host, int64_t n) {
-  return guarded([&]() -> int {
-    if (!c || !host || which < 0 || which > 1) return fail(HX_EINVAL, "bad arguments");
-    if (n > c->opnd_elems[which]) return fail(HX_EINVAL, "more elements than the pool holds");
-    CK(cudaSetDevice(c->device));
-    CK(cudaMemcpyAsync(host, c->buf(which), size_t(n) * sizeof(double), cudaMemcpyDeviceToHost,
-                       c->s));
-    CK(cudaStreamSynchronize(c->s));
-    return HX_OK;
-  });
-}
-
 extern "C" int hx_ctx_synchronize(hx_ctx* c) {
   return guarded([&]() -> int {
     if (!c) return fail(HX_EINVAL, "null ctx");
@@ -661,6 +650,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
     b.release();
   }
   for (auto& w : c->work) w.release();
+  for (double* p : c->pools) cudaFree(p);
   for (int i = 0; i < 3; ++i) {
     c->terms[i].release();
     c->tiles[i].release();
@@ -683,3 +673,5 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   cudaStreamDestroy(c->s);
   delete c;
 }
+
+#include "assemble.cuh"

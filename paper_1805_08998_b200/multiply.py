@@ -124,8 +124,21 @@ def plan_tile(bct):
     return 32 if nmin <= 32 else 64
 
 
-def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0):
-    """Run the product on one GPU; returns (HMatrix, MultReport)."""
+def _host_directory(h):
+    pool, d = operand_directory(h)
+    if pool is None:  # assembled on the device: one download of the packed pool
+        pool = h._hx_pool.download()
+        h._hx_packed = (pool, d)
+    return pool, d
+
+
+def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
+                    device_operands=True):
+    """Run the product on one GPU and return the product ``HMatrix``.
+
+    ``device_operands``: attach operand pools already resident on this device (GPU
+    assembly) instead of uploading the host copy.  ``leaf_mask`` restricts the product to
+    the owned output leaves (multi-GPU partition)."""
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     policy = cfg.policy
@@ -138,24 +151,32 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         for w in wl:
             warnings.warn(w.message)
     t_start = time.perf_counter()
-    pool_a, dir_a = operand_directory(h)
     same = k is h
-    pool_b, dir_b = (pool_a, dir_a) if same else operand_directory(k)
+
+    def resident(x):
+        d = getattr(x, "_hx_device", None)
+        return d if (device_operands and d is not None and d[0] == device) else None
+
+    pool_a, dir_a = operand_directory(h) if resident(h) else _host_directory(h)
+    if same:
+        pool_b, dir_b = pool_a, dir_a
+    else:
+        pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
     t0 = time.perf_counter()
     plan = _lib.Plan(tree_arrays(h.bct), dir_a, dir_a if same else dir_b, leaf_mask,
                      plan_tile(h.bct))
     plan_ms = (time.perf_counter() - t0) * 1e3
-    dev_a = getattr(h, "_hx_device", None)
-    if dev_a is not None and dev_a[0] == device:
+    dev_a = resident(h)
+    if dev_a is not None:
         dev.set_operand(0, dev_ptr=dev_a[1], n=dev_a[2])
     else:
         dev.set_operand(0, pool=pool_a)
     if same:
         dev.alias_b()
     else:
-        dev_b = getattr(k, "_hx_device", None)
-        if dev_b is not None and dev_b[0] == device:
+        dev_b = resident(k)
+        if dev_b is not None:
             dev.set_operand(1, dev_ptr=dev_b[1], n=dev_b[2])
         else:
             dev.set_operand(1, pool=pool_b)
