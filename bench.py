@@ -1,0 +1,452 @@
+"""Benchmark of the tolerance-controlled H x H product (BASELINE.json metric).
+
+One step = one full product C = A*B on the bench workload (default: BASELINE config 2,
+n=32768 on S^2, Gaussian kernel, leaf 64, eta 0.8, ACA 1e-8 operands, tol 1e-6), operands
+resident in HBM: host-side term-list planning + all device phases, bracketed by CUDA
+events on the product stream (barrier + synchronize on both sides; max over ranks).
+
+value  = canonical FP64 work of the product (SURVEY 8(d) min-route model) / step time,
+         in GFLOP/s, whole job.
+e2e    = the same through the public API with host operands: pack/H2D of the operand pool,
+         the product, D2H of every output block and construction of the HMatrix.
+Multi-GPU (torchrun): output leaves are LPT-partitioned over ranks by estimated cost,
+operand pools replicated from rank 0 by an NCCL broadcast; no reduction (strong scaling).
+
+--impl reference: the reference algorithm (the NumPy restatement in oracle/, the
+reference is pure Python and cannot travel to the GPU box) on the host cores, one bounded
+sample of the same workload per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_DMMA_PEAK_TFLOPS = 37.1   # profiles/r01_fp64_peak.txt (measured, this pool's B200)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ clocks sampling
+class Clocks:
+    def __init__(self, device):
+        self.proc = None
+        self.path = None
+        self.device = device
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.device}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:  # pragma: no cover
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(max(smax)) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ canonical work
+def canonical_work(info, leaves, ranks):
+    """F and B of the product given plan info/leaves and far ranks."""
+    F = info.flops_form + info.flops_near
+    B = info.bytes_form + info.bytes_near
+    far = leaves["kind"] == 1
+    m = leaves["m"][far].astype(float)
+    n = leaves["n"][far].astype(float)
+    K = leaves["K"][far].astype(float)
+    fdd = leaves["fdd"][far]
+    edd = leaves["edd"][far]
+    r = ranks[far].astype(float)
+    mu = np.minimum(m, n)
+    ell = np.minimum(r + 8, mu)
+    f_dense = fdd + 2 * m * n * K + 14 * m * n * mu + 8 * mu ** 3 + 2 * (m + n) * mu * r
+    b_dense = 8 * (K * (m + n) + edd + 2 * m * n + (m + n) * r)
+    f_fact = np.where((fdd == 0) & (K < mu),
+                      2 * m * K ** 2 + 2 * n * K ** 2 - (4 / 3) * K ** 3 + 2 * K ** 3 + 22 * K ** 3
+                      + 2 * (m + n) * K * r, np.inf)
+    b_fact = 8 * (2 * K * (m + n) + (m + n) * r)
+    f_sk = (2 * ell * (2 * K * (m + n) + 2 * edd) + 2 * m * ell ** 2 + 14 * n * ell ** 2
+            + 8 * ell ** 3 + 2 * (m + n) * ell * r)
+    b_sk = 8 * (2 * (K * (m + n) + edd) + 2 * ell * (m + n))
+    fs = np.stack([f_dense, f_fact, f_sk])
+    bs = np.stack([b_dense, b_fact, b_sk])
+    pick = np.argmin(fs, axis=0)
+    cols = np.arange(len(m))
+    F += float(fs[pick, cols].sum())
+    B += float(bs[pick, cols].sum())
+    return F, B
+
+
+# ------------------------------------------------------------------ partition
+def lpt_partition(cost, world):
+    """Longest-processing-time greedy: leaf index -> rank."""
+    order = np.argsort(-cost, kind="stable")
+    load = np.zeros(world)
+    owner = np.zeros(len(cost), dtype=np.int64)
+    for i in order:
+        r = int(np.argmin(load))
+        owner[i] = r
+        load[r] += cost[i]
+    return owner, load
+
+
+def leaf_costs(leaves):
+    m = leaves["m"].astype(float)
+    n = leaves["n"].astype(float)
+    K = leaves["K"].astype(float)
+    return 2 * m * n * K + leaves["fdd"] + np.where(leaves["kind"] == 1, 60 * m * n, 0.0)
+
+
+# ------------------------------------------------------------------ CPU reference sample
+def cpu_sample(cfg_id, c, A, budget_s, tag="aca"):
+    """Reference algorithm (oracle port) on the first output leaves in DFS order until the
+    time budget is spent; returns (gflop, seconds, leaves, threads)."""
+    from oracle import hmat_oracle as O
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import _lib, configs, hmatrix, multiply
+
+    pts = configs.make_points(c)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, c["n_min"]), c["eta"])
+    _, d = multiply._host_directory(A)
+    data = {}
+    for b, p in A.data.items():
+        data[b] = O.LR(np.ascontiguousarray(p.left), np.ascontiguousarray(p.right)) \
+            if hasattr(p, "left") else np.ascontiguousarray(p)
+    oa = O.HMatO(obt, data)
+    leaves = [b for b in range(obt.n_nodes) if obt.kind[b] != O.INNER]
+    # grow the sample geometrically until one run takes a good part of the budget
+    count = 64
+    t = 0.0
+    while True:
+        only = set(leaves[:count])
+        t0 = time.perf_counter()
+        Cr = O.hmult_new_o(oa, oa, O.Eps(c["tol"]), tag, only=only)
+        t = time.perf_counter() - t0
+        if t > 0.3 * budget_s or count >= len(leaves):
+            break
+        count = min(len(leaves), int(count * max(2.0, 0.5 * budget_s / max(t, 1e-3))))
+    mask = np.zeros(obt.n_nodes, np.uint8)
+    mask[list(only)] = 1
+    plan = _lib.Plan(hmatrix.tree_arrays(A.bct), d, d, mask, multiply.plan_tile(A.bct))
+    lv = plan.leaves()
+    ranks = np.array([Cr.data[int(b)].rank if lv["kind"][i] == 1 else -1
+                      for i, b in enumerate(lv["ids"])])
+    F, _ = canonical_work(plan.info, lv, ranks)
+    threads = int(os.environ.get("OPENBLAS_NUM_THREADS", os.cpu_count() or 1))
+    return F / 1e9, t, len(only), threads
+
+
+# ------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--tag", default="dense-svd")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return bench_reference(args, rank, world)
+    return bench_ours(args, rank, world, local)
+
+
+def bench_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import configs
+
+    c = configs.CONFIGS[args.config]
+    # operands: the same GPU-assembled A (assembly is not part of the timed product)
+    bct, A, B = configs.build_operands(c)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        gf, t, nl, threads = cpu_sample(args.config, c, A, args.cpu_budget / 2, tag="aca")
+        if i >= args.warmup:
+            vals.append(gf / t)
+    v = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": "hxh_product_fp64_gflops", "value": v,
+        "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded BASELINE point cloud)",
+        "config": {"workload": configs.NAMES[args.config], "compressor": "aca"},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                         "sample": f"reference algorithm (oracle port, NumPy/OpenBLAS) on the "
+                                   f"first {nl} output leaves in DFS order per step"},
+        "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def bench_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import _lib, configs, hmatrix, multiply
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = configs.CONFIGS[args.config]
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(args.tag), policy=hx.EpsRank(c["tol"]))
+    pts = configs.make_points(c)
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, c["n_min"]), c["eta"])
+    h = c["n"] ** (-1.0 / 3.0)
+    keep = []
+
+    def operand(kern):
+        if world == 1:
+            return hx.assemble_hmatrix(kern, bct, hx.EpsRank(c["eps_a"]), pts, h=h, device=local)
+        # rank 0 assembles, NCCL broadcast of the packed pool + host directory
+        if rank == 0:
+            H = hx.assemble_hmatrix(kern, bct, hx.EpsRank(c["eps_a"]), pts, h=h, device=local)
+            n_el = H._hx_device[2]
+            meta = [n_el, H._hx_packed[1], sorted(H.degraded)]
+        else:
+            meta = [None, None, None]
+        dist.broadcast_object_list(meta, src=0)
+        n_el, d, deg = meta
+        buf = torch.empty(max(n_el, 1), dtype=torch.float64, device="cuda")
+        if rank == 0:
+            _copy_pool(H, buf, n_el)
+        dist.broadcast(buf, src=0)
+        keep.append(buf)
+        if rank != 0:
+            H = hx.HMatrix(bct, {}, set(deg))
+            from paper_1805_08998_b200.assembly import _LazyLeaves
+            H.data = _LazyLeaves(H)
+            H._hx_packed = (None, d)
+            H._hx_device = (local, buf.data_ptr(), n_el)
+
+            class _P:  # host download path for the lazy dict / e2e leg
+                def download(self_inner):
+                    return buf[:n_el].cpu().numpy()
+            H._hx_pool = _P()
+        return H
+
+    t_setup = time.time()
+    A = operand(c["ka"])
+    B = A if c["kb"] is None else operand(c["kb"])
+    # partition of the output leaves (full plan once for the costs)
+    _, dA = multiply.operand_directory(A)
+    _, dB = multiply.operand_directory(B)
+    mask = None
+    if world > 1:
+        full = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, None,
+                         multiply.plan_tile(bct))
+        lv = full.leaves()
+        owner, load = lpt_partition(leaf_costs(lv), world)
+        mask = np.zeros(bct.n_nodes, np.uint8)
+        mask[lv["ids"][owner == rank]] = 1
+        full.close()
+    setup_s = time.time() - t_setup
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        return multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask)
+
+    for _ in range(args.warmup):
+        C = step()
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    launches = 0
+    dom_ms = 0.0
+    form_ms = mat_ms = rec_ms = plan_ms = 0.0
+    for _ in range(args.steps):
+        C = step()
+        r = C.report
+        launches += r.launches
+        dom_ms += r.form_ms
+        form_ms += r.form_ms
+        mat_ms += r.materialize_ms
+        rec_ms += r.recompress_ms
+        plan_ms += r.plan_ms
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ck = clocks.stop()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    # canonical work of the whole product (all ranks' leaves)
+    lv = C.plan_leaves
+    F_local, B_local = canonical_work(C.plan_info, lv, C.leaf_rank)
+    ranks_all = None
+    if world > 1:
+        full = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, None,
+                         multiply.plan_tile(bct))
+        lv_all = full.leaves()
+        # far ranks of every leaf: gather owned ranks
+        mine = dict(zip(lv["ids"].tolist(), C.leaf_rank.tolist()))
+        gathered = [None] * world
+        dist.all_gather_object(gathered, mine)
+        allr = {}
+        for g in gathered:
+            allr.update(g)
+        ranks_all = np.array([allr[int(b)] for b in lv_all["ids"]])
+        F_tot, B_tot = canonical_work(full.info, lv_all, ranks_all)
+    else:
+        F_tot, B_tot = F_local, B_local
+    value = F_tot / (ms_max * 1e-3) / 1e9
+
+    # e2e through the public API with host operands
+    e2e = None
+    if not args.no_e2e:
+        pa, _ = multiply._host_directory(A)
+        pb = pa if B is A else multiply._host_directory(B)[0]
+        h2d = 8 * (pa.size + (0 if B is A else pb.size))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        for _ in range(max(1, args.steps // 2)):
+            Ce = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
+                                          device_operands=False)
+            d2h = 8 * sum((p.left.size + p.right.size) if hasattr(p, "left") else p.size
+                          for p in Ce.data.values())
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / max(1, args.steps // 2)
+        tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": F_tot / float(tt.item()) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(tt.item()) * 1e3}
+
+    # roofline of the dominant kernel: term formation (HBM-bound in the canonical model)
+    peaks = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6552.3))
+    info = C.plan_info
+    form_s = form_ms / args.steps * 1e-3
+    achieved = info.bytes_form / form_s / 1e9 if form_s > 0 else 0.0
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "traffic": None,
+                "kernel": "grouped_gemm_kernel (term formation: cores + pushed-through factors)",
+                "note": "achieved = canonical term-formation bytes (SURVEY 8(d)) / measured "
+                        "phase time; FP64 DMMA peak measured 37.1 TFLOP/s "
+                        "(profiles/r01_fp64_peak.txt)",
+                "fp64_tflops_whole_product": value / 1e3,
+                "fp64_frac_whole_product": value / 1e3 / FP64_DMMA_PEAK_TFLOPS}
+    # roofline time of the whole product (phase-wise max(F/P, B/BW))
+    cpu = None
+    if rank == 0 and world == 1:
+        try:
+            gf, tcpu, nl, threads = cpu_sample(args.config, c, A, args.cpu_budget, tag="aca")
+            cpu = {"value": gf / tcpu, "unit": "GFLOP/s", "cores": threads, "kind": "port",
+                   "sample": f"reference algorithm (oracle NumPy port, aca compressor) on the "
+                             f"first {nl} output leaves in DFS order, {tcpu:.1f}s"}
+        except Exception as exc:  # pragma: no cover - reported, never fatal
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "port",
+                   "sample": f"failed: {exc!r}"}
+    if rank == 0:
+        rep = C.report
+        line = {
+            "metric": "hxh_product_fp64_gflops", "value": value, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded BASELINE point cloud, GPU ACA-assembled operands)",
+            "config": {"workload": configs.NAMES[args.config], "compressor": args.tag,
+                       "l2": "inputs larger than L2 (operand pools "
+                             f"{8 * A._hx_device[2] / 1e9:.2f} GB)",
+                       "parallelism": f"output-leaf partition x{world}"},
+            "canonical_gflop": F_tot / 1e9, "canonical_gbytes": B_tot / 1e9,
+            "phases_ms": {"plan_host": plan_ms / args.steps, "form": form_ms / args.steps,
+                          "materialize": mat_ms / args.steps,
+                          "recompress": rec_ms / args.steps},
+            "max_far_rank": rep.max_far_rank, "setup_s": setup_s,
+            "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
+            "e2e": e2e, "clocks": ck,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def _copy_pool(H, buf, n_el):
+    """Device-to-device copy of a library-owned pool into a torch tensor (NCCL source)."""
+    import ctypes as C
+
+    from paper_1805_08998_b200 import _lib
+
+    _lib.check(_lib.lib().hx_pool_download(H._hx_pool.dev.h, C.c_void_p(H._hx_pool.ptr),
+                                           C.cast(C.c_void_p(buf.data_ptr()), _lib.f64p),
+                                           n_el), "hx_pool_download")
+
+
+if __name__ == "__main__":
+    sys.exit(main())

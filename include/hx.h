@@ -151,7 +151,8 @@ int hx_assemble(hx_ctx* ctx, const hx_tree* tree, const double* points, int dim,
                 double h, double eps, int8_t* payload, int32_t* rank, int64_t* u_off,
                 int64_t* v_off, int64_t* d_off, int8_t* degraded, double** pool_dev,
                 int64_t* pool_elems);
-/* Copy n_elems doubles of a library-allocated device pool to host memory. */
+/* Copy n_elems doubles of a library-allocated device pool to host memory (or to another
+ * device buffer: the copy direction is inferred from the pointers). */
 int hx_pool_download(hx_ctx* ctx, const double* pool_dev, double* host, int64_t n_elems);
 int hx_pool_free(hx_ctx* ctx, double* pool_dev);
 

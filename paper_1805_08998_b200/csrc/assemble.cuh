@@ -474,7 +474,8 @@ extern "C" int hx_pool_download(hx_ctx* c, const double* pool, double* host, int
   return guarded([&]() -> int {
     if (!c || !pool || !host || n < 0) return fail(HX_EINVAL, "bad arguments");
     CK(cudaSetDevice(c->device));
-    CK(cudaMemcpyAsync(host, pool, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost, c->s));
+    // cudaMemcpyDefault: the destination may be host memory or another device buffer
+    CK(cudaMemcpyAsync(host, pool, size_t(n) * sizeof(double), cudaMemcpyDefault, c->s));
     CK(cudaStreamSynchronize(c->s));
     return HX_OK;
   });
