@@ -402,7 +402,7 @@ def bench_ours(args, rank, world, local):
                 "fp64_frac_whole_product": value / 1e3 / FP64_DMMA_PEAK_TFLOPS}
     # roofline time of the whole product (phase-wise max(F/P, B/BW))
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and args.cpu_budget > 0:
         try:
             gf, tcpu, nl, threads = cpu_sample(args.config, c, A, args.cpu_budget, tag="aca")
             cpu = {"value": gf / tcpu, "unit": "GFLOP/s", "cores": threads, "kind": "port",
