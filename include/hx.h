@@ -77,6 +77,8 @@ typedef struct hx_plan_info {
   int64_t fac_terms, fac_tiles;
   int64_t core_elems, term_elems, tile_elems;
   int64_t max_out_dim;      /* largest output block side                           */
+  int64_t n_xgroups;        /* terms batched by their shared H-block X             */
+  int64_t gather_elems, gather_jobs;
   double flops_form, bytes_form;   /* canonical model term formation   */
   double flops_near, bytes_near;   /* canonical model near leaves                    */
 } hx_plan_info;

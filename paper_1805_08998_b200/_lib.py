@@ -38,7 +38,8 @@ class HxPlanInfo(C.Structure):
         "n_out", "n_far", "n_near", "n_terms_real", "n_terms_expand", "n_dxd")] + [
         ("created", C.c_int64 * 3)] + [(name, C.c_int64) for name in (
             "mat_terms", "mat_tiles", "mat_groups", "core_terms", "core_tiles", "fac_terms",
-            "fac_tiles", "core_elems", "term_elems", "tile_elems", "max_out_dim")] + [
+            "fac_tiles", "core_elems", "term_elems", "tile_elems", "max_out_dim",
+            "n_xgroups", "gather_elems", "gather_jobs")] + [
         (name, C.c_double) for name in ("flops_form", "bytes_form", "flops_near",
                                         "bytes_near")]
 

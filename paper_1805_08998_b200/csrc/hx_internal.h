@@ -63,7 +63,16 @@ struct hx_plan {
   std::vector<hx::Group> core_groups, fac_groups, mat_groups;
   std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
   std::vector<hx::OutLeaf> leaves;
-  int64_t core_elems = 0, term_elems = 0, tile_elems = 0;
+  int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
+  std::vector<hx::CopyRec> gather;
+  // X-groups are processed in batches whose gathered factors and cores fit a bounded
+  // workspace (BUF_GATHER / BUF_CORE offsets restart at 0 in every batch)
+  struct Batch {
+    int64_t gather_begin, gather_end;
+    int64_t core_begin, core_end;   // core tiles
+    int64_t fac_begin, fac_end;     // fac tiles
+  };
+  std::vector<Batch> batches;
   int64_t near_ws_begin = 0;  // near-leaf blocks sit after all far blocks in BUF_TILE
   int32_t n_sumsq = 0;
   std::vector<int32_t> log_block, log_a, log_b, log_rank;

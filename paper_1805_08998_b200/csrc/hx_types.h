@@ -30,7 +30,15 @@ enum Buf : uint8_t {
   BUF_OMEGA = 5,   // Gaussian test matrix for the sketch
   BUF_WORK = 6,    // recompression workspace (Y/Q, Bt/Q2, small matrices)
   BUF_OUT = 7,     // output factors (left m x r, right n x r per far leaf)
-  NUM_BUFS = 8
+  BUF_GATHER = 8,  // thin factors of each X-group gathered side by side (G)
+  NUM_BUFS = 9
+};
+
+// Contiguous copy of n doubles from (src_buf, src_off) to BUF_GATHER + dst_off.
+struct CopyRec {
+  int64_t src_off, dst_off, n;
+  int32_t src_buf;
+  int32_t pad;
 };
 
 enum TileMode : uint8_t {

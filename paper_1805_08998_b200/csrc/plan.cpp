@@ -14,9 +14,17 @@
 //   pairs at far leaves are expanded into the same kinds of terms on sub-blocks (exact,
 //   SURVEY Appendix D), pending near x near pairs become dense x dense products.
 //
-// Output: three batches of tiles for the grouped-GEMM kernel (hx_types.h):
-//   core  : k x k cores  V_A^T U_B  (and V_l^T U_B / U_l^T V_A for the far leaves l of X)
-//   fac   : computed term factors   V_B core^T, U_A core, X U_B, X^T V_A
+// Every created term has one computed factor, and it is always "an H-block times a thin
+// matrix":  left_t = X U  (X = the A-side block, U = U_B)  or  right_t = X^T V  (X = the
+// B-side block, V = V_A) -- far x far pushes the smaller rank, which is the same formula
+// with X a single low-rank leaf.  Terms sharing the same X (on average ~35 on config 2)
+// are batched: their thin factors are gathered side by side into G and X is applied once
+// to G, so X's leaves are read once per group instead of once per term.
+//
+// Output: batches for the device
+//   gather: thin factors copied into each group's G
+//   core  : V_l^T G (A side) / U_l^T G (B side) for the low-rank leaves l of X
+//   fac   : row bands of X G / X^T G  (dense leaves D_l G, low-rank leaves U_l core_l)
 //   mat   : every output leaf materialized tile by tile from the terms of its root path
 #include <algorithm>
 #include <cstring>
@@ -37,6 +45,14 @@ constexpr int INNER = 0, FAR = 1, NEAR = 2;
 
 inline int64_t align16(int64_t x) { return (x + 15) & ~int64_t(15); }
 
+// One created low-rank term (before batching).
+struct TRec {
+  int32_t pc, qc;    // A-side and B-side blocks of the sub-pair
+  int32_t k;         // rank of the term
+  int32_t mat;       // index of its materialization term (patched with the factor offset)
+  int8_t side;       // 0: left_t = X U_B (X = pc), 1: right_t = X^T V_A (X = qc)
+};
+
 struct Builder {
   const hx_tree& t;
   const hx_operand& A;
@@ -45,12 +61,13 @@ struct Builder {
   int T;
   hx_plan& P;
   std::vector<uint8_t> owned_sub;
+  std::vector<TRec> recs;
 
   // materialization groups of the current root path (real blocks)
   std::vector<int32_t> path_groups;
 
   struct VGroup {
-    int32_t g;           // index into group table (term range)
+    int32_t g;  // index into group table (term range)
     int64_t r0, r1, c0, c1;
   };
 
@@ -67,10 +84,9 @@ struct Builder {
   }
   int child_of(int b, int i, int j) const { return t.child[4 * b + 2 * i + j]; }
 
-  // ------------------------------------------------------------------ work emission
-  Term make_term(uint8_t abuf, int64_t aoff, int32_t ald, uint8_t akc, uint8_t bbuf,
-                 int64_t boff, int32_t bld, uint8_t bkc, int32_t k, int64_t rlo, int64_t clo,
-                 int64_t rows, int64_t cols) {
+  static Term make_term(uint8_t abuf, int64_t aoff, int32_t ald, uint8_t akc, uint8_t bbuf,
+                        int64_t boff, int32_t bld, uint8_t bkc, int32_t k, int64_t rlo,
+                        int64_t clo, int64_t rows, int64_t cols) {
     Term x;
     x.a_off = aoff;
     x.b_off = boff;
@@ -88,22 +104,18 @@ struct Builder {
     return x;
   }
 
-  // Tiles over an R x C output (column-major, ld = R) at out_off in out_buf, coordinate
-  // origin (row_base, 0).  Every tile gets the pieces that intersect its rows.
-  void emit_tiles(std::vector<Term>& terms, std::vector<Tile>& tiles,
-                  std::vector<Group>& groups, uint8_t out_buf, int64_t out_off, int64_t R,
-                  int64_t C, int64_t row_base, const std::vector<Term>& pieces) {
-    for (int64_t i = 0; i < R; i += T) {
+  // Tiles over an R x C output (column-major, ld = R) at out_off in out_buf; the tile grid
+  // starts at coordinate (row_base, 0).  `band_pieces[i]` are the terms of row band i.
+  void emit_band_tiles(std::vector<Term>& terms, std::vector<Tile>& tiles,
+                       std::vector<Group>& groups, uint8_t out_buf, int64_t out_off, int64_t R,
+                       int64_t C, int64_t row_base,
+                       const std::vector<std::vector<Term>>& band_pieces) {
+    for (int64_t i = 0, band = 0; i < R; i += T, ++band) {
       const int64_t r1 = std::min<int64_t>(R, i + T);
       const int32_t gb = int32_t(terms.size());
-      for (const Term& p : pieces) {
-        const int64_t pr0 = p.r_lo, pr1 = int64_t(p.r_lo) + p.rows;
-        if (pr1 <= row_base + i || pr0 >= row_base + r1) continue;
-        terms.push_back(p);
-      }
-      const int32_t ge = int32_t(terms.size());
+      for (const Term& p : band_pieces[band]) terms.push_back(p);
       const int32_t gidx = int32_t(groups.size());
-      groups.push_back(Group{gb, ge});
+      groups.push_back(Group{gb, int32_t(terms.size())});
       for (int64_t j = 0; j < C; j += T) {
         Tile tl;
         std::memset(&tl, 0, sizeof(tl));
@@ -123,22 +135,8 @@ struct Builder {
     }
   }
 
-  int64_t new_core(int k1, int k2, const Term& piece) {
-    const int64_t off = P.core_elems;
-    P.core_elems = align16(P.core_elems + int64_t(k1) * k2);
-    std::vector<Term> one{piece};
-    emit_tiles(P.core_terms, P.core_tiles, P.core_groups, hx::BUF_CORE, off, k1, k2, 0, one);
-    return off;
-  }
-
-  int64_t new_factor(int64_t rows, int64_t cols) {
-    const int64_t off = P.term_elems;
-    P.term_elems = align16(P.term_elems + rows * cols);
-    return off;
-  }
-
-  // Leaves of the subtree of operand node x (DFS order), with the multiply/byte counts of
-  // one thin product through it (hmatrix.py:177-202).
+  // Leaves of the subtree of node x (DFS order), with the multiply/byte counts of one
+  // thin product through it (hmatrix.py:177-202).
   void subtree_leaves(const hx_operand& op, int x, std::vector<int>& out, double& mv,
                       double& bytes) {
     if (kind(x) == INNER) {
@@ -162,108 +160,51 @@ struct Builder {
 
   // --------------------------------------------------------------- term creation
   // One sub-pair (pc, qc) on the (real or virtual) block tc x sc with a factored side:
-  // _thin_product (sumexpr.py:93-117).  Returns the rank of the new term (0 = dropped).
+  // _thin_product (sumexpr.py:93-117).  Records the term; its computed factor is produced
+  // by the group pass.  Returns the rank of the new term (0 = dropped).
   int create_lr(int tc, int sc, int pc, int qc, int log_block) {
-    const int rho = t.sigma[pc];
-    const int64_t m = sz(tc), n = sz(sc), kr = sz(rho);
+    const int64_t m = sz(tc), n = sz(sc);
     const bool aF = isF(A, pc), bF = isF(B, qc);
-    hx_plan_info& I = P.info;
+    int k, kind_log;
+    int8_t side;
     if (aF && bF) {
       const int kA = A.rank[pc], kB = B.rank[qc];
       if (kA == 0 || kB == 0) return 0;
-      const Term cp = make_term(hx::BUF_A, A.v_off[pc], int32_t(kr), 1, hx::BUF_B, B.u_off[qc],
-                                int32_t(kr), 1, int32_t(kr), 0, 0, kA, kB);
-      const int64_t core = new_core(kA, kB, cp);
-      I.flops_form += 2.0 * kr * kA * kB + 2.0 * kA * kB * double(kA <= kB ? n : m);
-      I.bytes_form += 8.0 * (kr * kA + kr * kB) +
-                      8.0 * (kA <= kB ? double(n) * (kA + kB) : double(m) * (kA + kB));
+      kind_log = 0;
       if (kA <= kB) {
-        const int64_t f = new_factor(n, kA);
-        std::vector<Term> pc1{make_term(hx::BUF_B, B.v_off[qc], int32_t(n), 0, hx::BUF_CORE,
-                                        core, kA, 0, kB, 0, 0, n, kA)};
-        emit_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, f, n, kA, 0, pc1);
-        P.mat_terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, f,
-                                        int32_t(n), 0, kA, lo(tc), lo(sc), m, n));
+        side = 1;  // (U_A, V_B core^T): right = B_qc^T V_A
+        k = kA;
       } else {
-        const int64_t f = new_factor(m, kB);
-        std::vector<Term> pc1{make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_CORE,
-                                        core, kA, 1, kA, 0, 0, m, kB)};
-        emit_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, f, m, kB, 0, pc1);
-        P.mat_terms.push_back(make_term(hx::BUF_TERM, f, int32_t(m), 0, hx::BUF_B, B.v_off[qc],
-                                        int32_t(n), 0, kB, lo(tc), lo(sc), m, n));
+        side = 0;  // (U_A core, V_B): left = A_pc U_B
+        k = kB;
       }
-      const int r = std::min(kA, kB);
-      if (log_block >= 0) log(log_block, 0, pc, qc, r);
-      return r;
+    } else if (aF) {
+      k = A.rank[pc];
+      if (k == 0) return 0;
+      side = 1;
+      kind_log = 1;
+    } else {
+      k = B.rank[qc];
+      if (k == 0) return 0;
+      side = 0;
+      kind_log = 2;
     }
-    if (aF) {
-      // (U_A, X^T V_A) with X = B node qc
-      const int kA = A.rank[pc];
-      if (kA == 0) return 0;
-      std::vector<int> leaves;
-      double mv = 0, bytes = 0;
-      subtree_leaves(B, qc, leaves, mv, bytes);
-      I.flops_form += double(kA) * mv;
-      I.bytes_form += bytes + 8.0 * kA * double(kr + n);
-      std::vector<Term> pieces;
-      for (int l : leaves) {
-        const int rl = t.tau[l], sl = t.sigma[l];
-        const int64_t roff = lo(rl) - lo(rho);
-        if (isF(B, l)) {
-          const int kl = B.rank[l];
-          if (kl == 0) continue;
-          const Term cp = make_term(hx::BUF_B, B.u_off[l], int32_t(sz(rl)), 1, hx::BUF_A,
-                                    A.v_off[pc] + roff, int32_t(kr), 1, int32_t(sz(rl)), 0, 0,
-                                    kl, kA);
-          const int64_t core = new_core(kl, kA, cp);
-          pieces.push_back(make_term(hx::BUF_B, B.v_off[l], int32_t(sz(sl)), 0, hx::BUF_CORE,
-                                     core, kl, 1, kl, lo(sl), 0, sz(sl), kA));
-        } else {
-          pieces.push_back(make_term(hx::BUF_B, B.d_off[l], int32_t(sz(rl)), 1, hx::BUF_A,
-                                     A.v_off[pc] + roff, int32_t(kr), 1, int32_t(sz(rl)),
-                                     lo(sl), 0, sz(sl), kA));
-        }
-      }
-      const int64_t f = new_factor(n, kA);
-      emit_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, f, n, kA, lo(sc), pieces);
-      P.mat_terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, f,
-                                      int32_t(n), 0, kA, lo(tc), lo(sc), m, n));
-      if (log_block >= 0) log(log_block, 1, pc, qc, kA);
-      return kA;
-    }
-    // (X U_B, V_B) with X = A node pc
-    const int kB = B.rank[qc];
-    if (kB == 0) return 0;
-    std::vector<int> leaves;
-    double mv = 0, bytes = 0;
-    subtree_leaves(A, pc, leaves, mv, bytes);
-    I.flops_form += double(kB) * mv;
-    I.bytes_form += bytes + 8.0 * kB * double(kr + m);
-    std::vector<Term> pieces;
-    for (int l : leaves) {
-      const int tl = t.tau[l], rl = t.sigma[l];
-      const int64_t roff = lo(rl) - lo(rho);
-      if (isF(A, l)) {
-        const int kl = A.rank[l];
-        if (kl == 0) continue;
-        const Term cp = make_term(hx::BUF_A, A.v_off[l], int32_t(sz(rl)), 1, hx::BUF_B,
-                                  B.u_off[qc] + roff, int32_t(kr), 1, int32_t(sz(rl)), 0, 0,
-                                  kl, kB);
-        const int64_t core = new_core(kl, kB, cp);
-        pieces.push_back(make_term(hx::BUF_A, A.u_off[l], int32_t(sz(tl)), 0, hx::BUF_CORE,
-                                   core, kl, 1, kl, lo(tl), 0, sz(tl), kB));
-      } else {
-        pieces.push_back(make_term(hx::BUF_A, A.d_off[l], int32_t(sz(tl)), 0, hx::BUF_B,
-                                   B.u_off[qc] + roff, int32_t(kr), 1, int32_t(sz(rl)),
-                                   lo(tl), 0, sz(tl), kB));
-      }
-    }
-    const int64_t f = new_factor(m, kB);
-    emit_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, f, m, kB, lo(tc), pieces);
-    P.mat_terms.push_back(make_term(hx::BUF_TERM, f, int32_t(m), 0, hx::BUF_B, B.v_off[qc],
-                                    int32_t(n), 0, kB, lo(tc), lo(sc), m, n));
-    if (log_block >= 0) log(log_block, 2, pc, qc, kB);
-    return kB;
+    TRec r;
+    r.pc = pc;
+    r.qc = qc;
+    r.k = k;
+    r.side = side;
+    r.mat = int32_t(P.mat_terms.size());
+    recs.push_back(r);
+    // the fixed factor is a pool factor; the computed one is patched by build_groups()
+    if (side == 0)
+      P.mat_terms.push_back(make_term(hx::BUF_TERM, -1, int32_t(m), 0, hx::BUF_B, B.v_off[qc],
+                                      int32_t(n), 0, k, lo(tc), lo(sc), m, n));
+    else
+      P.mat_terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, -1,
+                                      int32_t(n), 0, k, lo(tc), lo(sc), m, n));
+    if (log_block >= 0) log(log_block, kind_log, pc, qc, k);
+    return k;
   }
 
   void create_dxd(int tc, int sc, int pc, int qc) {
@@ -288,6 +229,136 @@ struct Builder {
     P.info.created[k]++;
   }
 
+  // --------------------------------------------------------------- grouped term factors
+  // workspace bound (doubles) for one batch of gathered factors, and for its cores
+  static constexpr int64_t budget = int64_t(1) << 28;
+
+  void build_groups() {
+    const int nn = t.n_nodes;
+    const size_t nr = recs.size();
+    // counting sort of the terms by (side, X)
+    std::vector<int32_t> cnt(2 * size_t(nn) + 1, 0);
+    auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
+    for (const TRec& r : recs) cnt[key(r) + 1]++;
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    std::vector<int32_t> order(nr);
+    {
+      std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+      for (size_t i = 0; i < nr; ++i) order[pos[key(recs[i])]++] = int32_t(i);
+    }
+    std::vector<int> leaves;
+    std::vector<std::vector<Term>> bands;
+    int64_t gat_cur = 0, core_cur = 0;
+    auto close_batch = [&]() {
+      hx_plan::Batch& bt = P.batches.back();
+      bt.gather_end = int64_t(P.gather.size());
+      bt.core_end = int64_t(P.core_tiles.size());
+      bt.fac_end = int64_t(P.fac_tiles.size());
+    };
+    auto open_batch = [&]() {
+      P.batches.push_back(hx_plan::Batch{int64_t(P.gather.size()), 0,
+                                         int64_t(P.core_tiles.size()), 0,
+                                         int64_t(P.fac_tiles.size()), 0});
+      gat_cur = 0;
+      core_cur = 0;
+    };
+    open_batch();
+    for (int g = 0; g < 2 * nn; ++g) {
+      const int32_t b0 = cnt[g], b1 = cnt[g + 1];
+      if (b0 == b1) continue;
+      const int side = g >= nn ? 1 : 0;
+      const int X = g - side * nn;
+      const hx_operand& opX = side == 0 ? A : B;
+      // rows of the computed factor and of the middle cluster rho'
+      const int rows_cl = side == 0 ? t.tau[X] : t.sigma[X];
+      const int rho = side == 0 ? t.sigma[X] : t.tau[X];
+      const int64_t R = sz(rows_cl), kr = sz(rho);
+      int64_t ktot = 0;
+      for (int32_t i = b0; i < b1; ++i) ktot += recs[order[i]].k;
+      leaves.clear();
+      double mv = 0, bytes = 0;
+      subtree_leaves(opX, X, leaves, mv, bytes);
+      int64_t core_need = 0;
+      for (int l : leaves)
+        if (isF(opX, l)) core_need += align16(int64_t(opX.rank[l]) * ktot);
+      const int64_t gat_need = align16(kr * ktot);
+      if ((gat_cur + gat_need > budget || core_cur + core_need > budget) &&
+          (gat_cur > 0 || core_cur > 0)) {
+        close_batch();
+        open_batch();
+      }
+      const int64_t out = P.term_elems;
+      P.term_elems = align16(P.term_elems + R * ktot);
+      const int64_t gat = gat_cur;
+      gat_cur += gat_need;
+      P.gather_elems = std::max(P.gather_elems, gat_cur);
+      // gather the thin factors side by side, patch the materialization terms
+      int64_t col = 0;
+      for (int32_t i = b0; i < b1; ++i) {
+        const TRec& r = recs[order[i]];
+        hx::CopyRec cp;
+        cp.src_buf = side == 0 ? hx::BUF_B : hx::BUF_A;
+        cp.src_off = side == 0 ? B.u_off[r.qc] : A.v_off[r.pc];
+        cp.dst_off = gat + col * kr;
+        cp.n = kr * r.k;
+        P.gather.push_back(cp);
+        Term& mt = P.mat_terms[r.mat];
+        if (side == 0) {
+          mt.a_off = out + col * R;
+          mt.a_ld = int32_t(R);
+        } else {
+          mt.b_off = out + col * R;
+          mt.b_ld = int32_t(R);
+        }
+        col += r.k;
+      }
+      // X applied to G: leaves of X
+      P.info.flops_form += double(ktot) * mv;
+      P.info.bytes_form += double(b1 - b0) * bytes + 8.0 * double(ktot) * double(kr + R);
+      P.info.n_xgroups++;
+      const int64_t nb = (R + T - 1) / T;
+      bands.assign(size_t(nb), {});
+      for (int l : leaves) {
+        // A side: leaf l = (tau_l, rho_l) rows tau_l;  B side: l = (rho_l, sigma_l) rows sigma_l
+        const int rl = side == 0 ? t.sigma[l] : t.tau[l];   // middle-cluster part
+        const int ol = side == 0 ? t.tau[l] : t.sigma[l];   // output rows
+        const int64_t roff = lo(rl) - lo(rho);
+        Term piece;
+        if (isF(opX, l)) {
+          const int kl = opX.rank[l];
+          if (kl == 0) continue;
+          // core_l = V_l^T G[rho_l] (A side) or U_l^T G[rho_l] (B side): kl x ktot
+          const int64_t core = core_cur;
+          core_cur = align16(core_cur + int64_t(kl) * ktot);
+          P.core_elems = std::max(P.core_elems, core_cur);
+          const int64_t mid_f = side == 0 ? opX.v_off[l] : opX.u_off[l];
+          std::vector<std::vector<Term>> one(size_t((kl + T - 1) / T));
+          const Term cp = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, mid_f, int32_t(sz(rl)), 1,
+                                    hx::BUF_GATHER, gat + roff, int32_t(kr), 1, int32_t(sz(rl)),
+                                    0, 0, kl, ktot);
+          for (auto& v : one) v.push_back(cp);
+          emit_band_tiles(P.core_terms, P.core_tiles, P.core_groups, hx::BUF_CORE, core, kl, ktot,
+                          0, one);
+          const int64_t out_f = side == 0 ? opX.u_off[l] : opX.v_off[l];
+          piece = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, out_f, int32_t(sz(ol)), 0,
+                            hx::BUF_CORE, core, kl, 1, kl, lo(ol), 0, sz(ol), ktot);
+        } else {
+          // dense: D_l G[rho_l] (A side) or D_l^T G[rho_l] (B side)
+          piece = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, opX.d_off[l], int32_t(sz(t.tau[l])),
+                            uint8_t(side == 0 ? 0 : 1), hx::BUF_GATHER, gat + roff, int32_t(kr), 1,
+                            int32_t(sz(rl)), lo(ol), 0, sz(ol), ktot);
+        }
+        const int64_t a = (lo(ol) - lo(rows_cl)) / T;
+        const int64_t e = (lo(ol) + sz(ol) - lo(rows_cl) - 1) / T;
+        for (int64_t bnd = std::max<int64_t>(a, 0); bnd <= std::min<int64_t>(e, nb - 1); ++bnd)
+          bands[size_t(bnd)].push_back(piece);
+      }
+      emit_band_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, out, R, ktot,
+                      lo(rows_cl), bands);
+    }
+    close_batch();
+  }
+
   // --------------------------------------------------------------- the descent
   // Pending pairs of (virtual) block tc x sc split onto child (ti, si):
   // sumexpr.py:146-153.  Created terms are appended to P.mat_terms (current group).
@@ -310,15 +381,13 @@ struct Builder {
     }
   }
 
-  // Expansion of the pending inner x inner pairs of far leaf `leaf` over virtual
-  // sub-blocks (exact).
+  // Expansion of the pending inner x inner pairs of a far leaf over virtual sub-blocks
+  // (exact).
   void expand(int tc, int sc, const std::vector<std::pair<int, int>>& pend,
               std::vector<VGroup>& vg, int64_t& K, double& fdd, double& edd) {
     if (pend.empty()) return;
-    if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0) {
-      // leaf level: pending pairs are dense x dense (already placed by caller)
+    if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0)
       throw std::runtime_error("expand reached leaf clusters");
-    }
     for (int ti = 0; ti < 2; ++ti)
       for (int si = 0; si < 2; ++si) {
         const int tcc = t.c_child[2 * tc + ti], scc = t.c_child[2 * sc + si];
@@ -410,67 +479,64 @@ struct Builder {
     P.leaves.push_back(L);
   }
 
-  void visit(int b, const std::vector<std::pair<int, int>>& pend) {
-    const int kb = kind(b);
-    const int tc = t.tau[b], sc = t.sigma[b];
-    if (kb == INNER) {
-      for (int ci = 0; ci < 4; ++ci) {
-        const int c = t.child[4 * b + ci];
-        if (c < 0 || !owned_sub[c]) continue;
-        const int32_t gb = int32_t(P.mat_terms.size());
-        std::vector<std::pair<int, int>> sub;
-        int64_t Kc = 0;
-        split_pairs(tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
-        P.info.n_terms_real += int64_t(P.mat_terms.size()) - gb;
-        // DxD pairs of a leaf at the leaf level join the leaf's own group
-        const bool leaf_level = kind(c) != INNER &&
-                                (t.c_child[2 * t.tau[c]] < 0 || t.c_child[2 * t.sigma[c]] < 0);
-        double fdd = 0, edd = 0;
-        std::vector<std::pair<int, int>> rest;
-        if (leaf_level) {
-          for (const auto& pq : sub) {
-            create_dxd(t.tau[c], t.sigma[c], pq.first, pq.second);
-            const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c])),
-                         kk = double(sz(t.sigma[pq.first]));
-            fdd += 2.0 * mm * kk * nn;
-            edd += mm * kk + kk * nn;
-          }
-        } else {
-          rest.swap(sub);
-        }
-        const int32_t ge = int32_t(P.mat_terms.size());
-        const bool has = ge > gb;
-        if (has) {
-          P.mat_groups_all.push_back(Group{gb, ge});
-          path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
-        }
-        const int64_t save_K = path_K;
-        path_K += Kc;
-        if (kind(c) == INNER) {
-          visit(c, rest);
-        } else {
-          std::vector<VGroup> vg;
-          int64_t K = path_K;
-          if (kind(c) == FAR) expand(t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
-          else if (!rest.empty()) throw hx::Unsupported("near leaf above the leaf level");
-          const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
-          if (kind(c) == NEAR) {
-            P.info.flops_near += fdd + 2.0 * mm * nn * double(K);
-            P.info.bytes_near += 8.0 * (double(K) * (mm + nn) + edd + mm * nn);
-            P.info.n_near++;
-          } else {
-            P.info.n_far++;
-          }
-          emit_leaf_tiles(c, kind(c) == FAR, vg, K, fdd, edd);
-        }
-        path_K = save_K;
-        if (has) path_groups.pop_back();
-      }
-    }
-  }
-
   int64_t path_K = 0;
   int64_t ws_far = 0, ws_near = 0;
+
+  void visit(int b, const std::vector<std::pair<int, int>>& pend) {
+    const int tc = t.tau[b], sc = t.sigma[b];
+    for (int ci = 0; ci < 4; ++ci) {
+      const int c = t.child[4 * b + ci];
+      if (c < 0 || !owned_sub[c]) continue;
+      const int32_t gb = int32_t(P.mat_terms.size());
+      std::vector<std::pair<int, int>> sub;
+      int64_t Kc = 0;
+      split_pairs(tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
+      P.info.n_terms_real += int64_t(P.mat_terms.size()) - gb;
+      // DxD pairs of a leaf at the leaf level join the leaf's own group
+      const bool leaf_level = kind(c) != INNER &&
+                              (t.c_child[2 * t.tau[c]] < 0 || t.c_child[2 * t.sigma[c]] < 0);
+      double fdd = 0, edd = 0;
+      std::vector<std::pair<int, int>> rest;
+      if (leaf_level) {
+        for (const auto& pq : sub) {
+          create_dxd(t.tau[c], t.sigma[c], pq.first, pq.second);
+          const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c])),
+                       kk = double(sz(t.sigma[pq.first]));
+          fdd += 2.0 * mm * kk * nn;
+          edd += mm * kk + kk * nn;
+        }
+      } else {
+        rest.swap(sub);
+      }
+      const int32_t ge = int32_t(P.mat_terms.size());
+      const bool has = ge > gb;
+      if (has) {
+        P.mat_groups_all.push_back(Group{gb, ge});
+        path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
+      }
+      const int64_t save_K = path_K;
+      path_K += Kc;
+      if (kind(c) == INNER) {
+        visit(c, rest);
+      } else {
+        std::vector<VGroup> vg;
+        int64_t K = path_K;
+        if (kind(c) == FAR) expand(t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
+        else if (!rest.empty()) throw hx::Unsupported("near leaf above the leaf level");
+        const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
+        if (kind(c) == NEAR) {
+          P.info.flops_near += fdd + 2.0 * mm * nn * double(K);
+          P.info.bytes_near += 8.0 * (double(K) * (mm + nn) + edd + mm * nn);
+          P.info.n_near++;
+        } else {
+          P.info.n_far++;
+        }
+        emit_leaf_tiles(c, kind(c) == FAR, vg, K, fdd, edd);
+      }
+      path_K = save_K;
+      if (has) path_groups.pop_back();
+    }
+  }
 
   // near blocks go after the far ones so the result download is two contiguous copies
   void place_near() {
@@ -484,11 +550,6 @@ struct Builder {
   }
 
   void run() {
-    run_dfs();
-    place_near();
-  }
-
-  void run_dfs() {
     const int nn = t.n_nodes;
     owned_sub.assign(nn, 0);
     // bottom-up ownership: children have larger pre-order ids than their parent
@@ -506,24 +567,27 @@ struct Builder {
     }
     if (t.kind[0] != INNER) {
       // the root itself is a leaf: S(root) = {(A_root, B_root)} evaluated directly
-      if (!owned_sub[0]) return;
-      const int tc = t.tau[0], sc = t.sigma[0];
-      if (t.kind[0] == FAR) throw hx::Unsupported("admissible root block");
-      const int32_t gb = int32_t(P.mat_terms.size());
-      create_dxd(tc, sc, 0, 0);
-      P.mat_groups_all.push_back(Group{gb, int32_t(P.mat_terms.size())});
-      path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
-      const double m = double(sz(tc));
-      const double fdd = 2.0 * m * m * m, edd = 2.0 * m * m;
-      P.info.flops_near += fdd;
-      P.info.bytes_near += 8.0 * (edd + m * m);
-      P.info.n_near++;
-      std::vector<VGroup> vg;
-      emit_leaf_tiles(0, false, vg, 0, fdd, edd);
-      return;
+      if (owned_sub[0]) {
+        const int tc = t.tau[0], sc = t.sigma[0];
+        if (t.kind[0] == FAR) throw hx::Unsupported("admissible root block");
+        const int32_t gb = int32_t(P.mat_terms.size());
+        create_dxd(tc, sc, 0, 0);
+        P.mat_groups_all.push_back(Group{gb, int32_t(P.mat_terms.size())});
+        path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
+        const double m = double(sz(tc));
+        const double fdd = 2.0 * m * m * m, edd = 2.0 * m * m;
+        P.info.flops_near += fdd;
+        P.info.bytes_near += 8.0 * (edd + m * m);
+        P.info.n_near++;
+        std::vector<VGroup> vg;
+        emit_leaf_tiles(0, false, vg, 0, fdd, edd);
+      }
+    } else {
+      std::vector<std::pair<int, int>> root{{0, 0}};
+      visit(0, root);
     }
-    std::vector<std::pair<int, int>> root{{0, 0}};
-    visit(0, root);
+    build_groups();
+    place_near();
   }
 };
 
@@ -557,6 +621,8 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
     I.core_elems = plan->core_elems;
     I.term_elems = plan->term_elems;
     I.tile_elems = plan->tile_elems;
+    I.gather_elems = plan->gather_elems;
+    I.gather_jobs = int64_t(plan->gather.size());
     *out = plan;
     return HX_OK;
   });
@@ -587,13 +653,11 @@ extern "C" int hx_plan_leaves(const hx_plan* plan, int32_t* ids, int8_t* kind, i
 extern "C" int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kind,
                                 int32_t* a_node, int32_t* b_node, int32_t* rank) {
   if (!plan) return hx::fail(HX_EINVAL, "null plan");
-  const size_t n = plan->log_block.size();
   if (block) std::copy(plan->log_block.begin(), plan->log_block.end(), block);
   if (kind) std::copy(plan->log_kind.begin(), plan->log_kind.end(), kind);
   if (a_node) std::copy(plan->log_a.begin(), plan->log_a.end(), a_node);
   if (b_node) std::copy(plan->log_b.begin(), plan->log_b.end(), b_node);
   if (rank) std::copy(plan->log_rank.begin(), plan->log_rank.end(), rank);
-  (void)n;
   return HX_OK;
 }
 

@@ -82,6 +82,14 @@ __global__ void omega_kernel(double* om, int64_t n, uint64_t seed) {
   om[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
+// Thin factors of each X-group copied side by side into G (BUF_GATHER).
+__global__ void gather_kernel(const CopyRec* __restrict__ recs, BufPtrs bufs) {
+  const CopyRec r = recs[blockIdx.x];
+  const double* __restrict__ src = bufs.p[r.src_buf] + r.src_off;
+  double* __restrict__ dst = bufs.p[BUF_GATHER] + r.dst_off;
+  for (int64_t e = threadIdx.x; e < r.n; e += blockDim.x) dst[e] = src[e];
+}
+
 }  // namespace
 
 struct FarBlock {
@@ -110,6 +118,7 @@ struct hx_ctx {
   DArr<Group> groups[3];
   DArr<double> sumsq, fro2;
   DArr<int> seg_b, seg_e;
+  DArr<CopyRec> gather_recs;
   DArr<Term> rterms;
   DArr<Tile> rtiles;
   DArr<Group> rgroups;
@@ -336,14 +345,24 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
     c->own[BUF_CORE].ensure(size_t(P->core_elems));
     c->own[BUF_TERM].ensure(size_t(P->term_elems));
     c->own[BUF_TILE].ensure(size_t(P->tile_elems));
+    c->own[BUF_GATHER].ensure(size_t(P->gather_elems));
     c->sumsq.ensure(size_t(P->n_sumsq));
+    c->gather_recs.upload(P->gather, s);
     BufPtrs bp = c->ptrs();
 
-    // ---- 1. term formation
-    launch_gemm(c, P->tile, c->tiles[0].p, c->groups[0].p, c->terms[0].p,
-                int(P->core_tiles.size()), bp, nullptr);
-    launch_gemm(c, P->tile, c->tiles[1].p, c->groups[1].p, c->terms[1].p,
-                int(P->fac_tiles.size()), bp, nullptr);
+    // ---- 1. term formation: gather thin factors per X-group, cores, X G products
+    for (const hx_plan::Batch& bt : P->batches) {
+      const int ng = int(bt.gather_end - bt.gather_begin);
+      if (ng > 0) {
+        gather_kernel<<<ng, 256, 0, s>>>(c->gather_recs.p + bt.gather_begin, bp);
+        CK(cudaGetLastError());
+        c->launches++;
+      }
+      launch_gemm(c, P->tile, c->tiles[0].p + bt.core_begin, c->groups[0].p, c->terms[0].p,
+                  int(bt.core_end - bt.core_begin), bp, nullptr);
+      launch_gemm(c, P->tile, c->tiles[1].p + bt.fac_begin, c->groups[1].p, c->terms[1].p,
+                  int(bt.fac_end - bt.fac_begin), bp, nullptr);
+    }
     CK(cudaEventRecord(c->ev[1], s));
     // ---- 2. materialization
     launch_gemm(c, P->tile, c->tiles[2].p, c->groups[2].p, c->terms[2].p,
@@ -660,6 +679,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   c->fro2.release();
   c->seg_b.release();
   c->seg_e.release();
+  c->gather_recs.release();
   c->rterms.release();
   c->rtiles.release();
   c->rgroups.release();
