@@ -72,6 +72,7 @@ SIGNATURES = {
     "hx_plan_leaves": [C.c_void_p, i32p, i8p, i32p, i32p, i64p, f64p, f64p],
     "hx_plan_term_log": [C.c_void_p, i32p, i8p, i32p, i32p, i32p],
     "hx_plan_free": [C.c_void_p],
+    "hx_plan_mma_flops": [C.c_void_p, f64p],
     "hx_ctx_create": [C.c_int, C.POINTER(C.c_void_p)],
     "hx_ctx_operand": [C.c_void_p, C.c_int, f64p, C.c_void_p, C.c_int64],
     "hx_ctx_operand_alias": [C.c_void_p],

@@ -16,8 +16,8 @@ HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "dense_la.cuh", "assemble.
 OUT = os.path.join(HERE, "libhx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC,-O2,-fopenmp", "-shared", "--expt-relaxed-constexpr",
+         "-Xptxas", "-v", "-lgomp"]
 
 
 def _stale():

@@ -12,6 +12,27 @@
 
 namespace hx {
 
+// std::vector whose resize() leaves POD elements uninitialized (the plan arrays are
+// filled right after sizing; zeroing hundreds of MB first would double the memory traffic)
+template <class T>
+struct DefaultInitAlloc : std::allocator<T> {
+  template <class U>
+  struct rebind {
+    using other = DefaultInitAlloc<U>;
+  };
+  using std::allocator<T>::allocator;
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+};
+template <class T>
+using pvec = std::vector<T, DefaultInitAlloc<T>>;
+
 struct Unsupported : std::runtime_error {
   explicit Unsupported(const std::string& s) : std::runtime_error(s) {}
 };
@@ -58,13 +79,13 @@ int guarded(F&& f) {
 
 struct hx_plan {
   int tile = 64;
-  std::vector<hx::Term> core_terms, fac_terms, mat_terms;
-  std::vector<hx::Tile> core_tiles, fac_tiles, mat_tiles;
-  std::vector<hx::Group> core_groups, fac_groups, mat_groups;
+  hx::pvec<hx::Term> core_terms, fac_terms, mat_terms;
+  hx::pvec<hx::Tile> core_tiles, fac_tiles, mat_tiles;
+  hx::pvec<hx::Group> core_groups, fac_groups, mat_groups;
   std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
-  std::vector<hx::OutLeaf> leaves;
+  hx::pvec<hx::OutLeaf> leaves;
   int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
-  std::vector<hx::CopyRec> gather;
+  hx::pvec<hx::CopyRec> gather;
   // X-groups are processed in batches whose gathered factors and cores fit a bounded
   // workspace (BUF_GATHER / BUF_CORE offsets restart at 0 in every batch)
   struct Batch {

@@ -21,12 +21,21 @@
 // are batched: their thin factors are gathered side by side into G and X is applied once
 // to G, so X's leaves are read once per group instead of once per term.
 //
+// The descent runs sequentially down to a cut level, then the subtrees below the cut in
+// parallel (OpenMP), each into its own output that is merged in DFS order; the grouped
+// factor work is then counted and filled in parallel.
+//
 // Output: batches for the device
 //   gather: thin factors copied into each group's G
-//   core  : V_l^T G (A side) / U_l^T G (B side) for the low-rank leaves l of X
+//   core  : V_l^T G (A side) / U_l^T G (B side) for the low-rank leaves l of X (stacked)
 //   fac   : row bands of X G / X^T G  (dense leaves D_l G, low-rank leaves U_l core_l)
 //   mat   : every output leaf materialized tile by tile from the terms of its root path
+#include <omp.h>
+
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -53,6 +62,46 @@ struct TRec {
   int8_t side;       // 0: left_t = X U_B (X = pc), 1: right_t = X^T V_A (X = qc)
 };
 
+using PairList = std::vector<std::pair<int, int>>;
+using GRef = std::pair<int32_t, int32_t>;  // (output index, group id local to that output)
+
+// Output of one descent task (the top part or one subtree below the cut).
+struct Out {
+  hx::pvec<TRec> recs;
+  std::vector<Term> terms;        // materialization terms
+  std::vector<Group> groups;      // one per creation block (real or virtual), local indices
+  std::vector<GRef> tile_groups;  // per tile: the groups of its root path and sub-blocks
+  std::vector<Tile> tiles;        // g_begin/g_end index tile_groups; ws offsets local
+  std::vector<hx::OutLeaf> leaves;
+  std::vector<int32_t> log_block, log_a, log_b, log_rank;
+  std::vector<int8_t> log_kind;
+  int64_t n_terms_real = 0, n_terms_expand = 0, n_dxd = 0, created[3] = {0, 0, 0};
+  int64_t n_far = 0, n_near = 0, max_out_dim = 0;
+  double flops_near = 0, bytes_near = 0;
+  int64_t ws_far = 0, ws_near = 0;
+  int32_t n_sumsq = 0;
+};
+
+struct Walk {
+  Out& o;
+  int32_t self;
+  std::vector<GRef> path;  // groups of the current root path
+  int64_t path_K = 0;
+};
+
+struct Task {
+  int c;
+  PairList pend;
+  std::vector<GRef> path;
+  int64_t path_K;
+  int64_t log_pos;  // top-part log length when the subtree was deferred
+};
+
+struct VGroup {
+  GRef g;
+  int64_t r0, r1, c0, c1;
+};
+
 struct Builder {
   const hx_tree& t;
   const hx_operand& A;
@@ -61,15 +110,7 @@ struct Builder {
   int T;
   hx_plan& P;
   std::vector<uint8_t> owned_sub;
-  std::vector<TRec> recs;
-
-  // materialization groups of the current root path (real blocks)
-  std::vector<int32_t> path_groups;
-
-  struct VGroup {
-    int32_t g;  // index into group table (term range)
-    int64_t r0, r1, c0, c1;
-  };
+  hx::pvec<TRec> recs;
 
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
@@ -104,41 +145,10 @@ struct Builder {
     return x;
   }
 
-  // Tiles over an R x C output (column-major, ld = R) at out_off in out_buf; the tile grid
-  // starts at coordinate (row_base, 0).  `band_pieces[i]` are the terms of row band i.
-  void emit_band_tiles(std::vector<Term>& terms, std::vector<Tile>& tiles,
-                       std::vector<Group>& groups, uint8_t out_buf, int64_t out_off, int64_t R,
-                       int64_t C, int64_t row_base,
-                       const std::vector<std::vector<Term>>& band_pieces) {
-    for (int64_t i = 0, band = 0; i < R; i += T, ++band) {
-      const int64_t r1 = std::min<int64_t>(R, i + T);
-      const int32_t gb = int32_t(terms.size());
-      for (const Term& p : band_pieces[band]) terms.push_back(p);
-      const int32_t gidx = int32_t(groups.size());
-      groups.push_back(Group{gb, int32_t(terms.size())});
-      for (int64_t j = 0; j < C; j += T) {
-        Tile tl;
-        std::memset(&tl, 0, sizeof(tl));
-        tl.out_off = out_off + i + j * R;
-        tl.out_ld = int32_t(R);
-        tl.row0 = int32_t(row_base + i);
-        tl.col0 = int32_t(j);
-        tl.rows = int16_t(r1 - i);
-        tl.cols = int16_t(std::min<int64_t>(C, j + T) - j);
-        tl.g_begin = gidx;
-        tl.g_end = gidx + 1;
-        tl.aux = -1;
-        tl.out_buf = out_buf;
-        tl.mode = hx::MODE_STORE;
-        tiles.push_back(tl);
-      }
-    }
-  }
-
   // Leaves of the subtree of node x (DFS order), with the multiply/byte counts of one
   // thin product through it (hmatrix.py:177-202).
   void subtree_leaves(const hx_operand& op, int x, std::vector<int>& out, double& mv,
-                      double& bytes) {
+                      double& bytes) const {
     if (kind(x) == INNER) {
       for (int c = 0; c < 4; ++c) {
         const int ch = t.child[4 * x + c];
@@ -162,7 +172,8 @@ struct Builder {
   // One sub-pair (pc, qc) on the (real or virtual) block tc x sc with a factored side:
   // _thin_product (sumexpr.py:93-117).  Records the term; its computed factor is produced
   // by the group pass.  Returns the rank of the new term (0 = dropped).
-  int create_lr(int tc, int sc, int pc, int qc, int log_block) {
+  int create_lr(Walk& w, int tc, int sc, int pc, int qc, int log_block) const {
+    Out& o = w.o;
     const int64_t m = sz(tc), n = sz(sc);
     const bool aF = isF(A, pc), bF = isF(B, qc);
     int k, kind_log;
@@ -194,176 +205,43 @@ struct Builder {
     r.qc = qc;
     r.k = k;
     r.side = side;
-    r.mat = int32_t(P.mat_terms.size());
-    recs.push_back(r);
+    r.mat = int32_t(o.terms.size());
+    o.recs.push_back(r);
     // the fixed factor is a pool factor; the computed one is patched by build_groups()
     if (side == 0)
-      P.mat_terms.push_back(make_term(hx::BUF_TERM, -1, int32_t(m), 0, hx::BUF_B, B.v_off[qc],
-                                      int32_t(n), 0, k, lo(tc), lo(sc), m, n));
+      o.terms.push_back(make_term(hx::BUF_TERM, -1, int32_t(m), 0, hx::BUF_B, B.v_off[qc],
+                                  int32_t(n), 0, k, lo(tc), lo(sc), m, n));
     else
-      P.mat_terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, -1,
-                                      int32_t(n), 0, k, lo(tc), lo(sc), m, n));
-    if (log_block >= 0) log(log_block, kind_log, pc, qc, k);
+      o.terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, -1,
+                                  int32_t(n), 0, k, lo(tc), lo(sc), m, n));
+    if (log_block >= 0) {
+      o.log_block.push_back(log_block);
+      o.log_kind.push_back(int8_t(kind_log));
+      o.log_a.push_back(pc);
+      o.log_b.push_back(qc);
+      o.log_rank.push_back(k);
+      o.created[kind_log]++;
+    }
     return k;
   }
 
-  void create_dxd(int tc, int sc, int pc, int qc) {
+  void create_dxd(Walk& w, int tc, int sc, int pc, int qc) const {
     const int rho = t.sigma[pc];
     const int64_t m = sz(tc), n = sz(sc), kr = sz(rho);
     if (!isD(A, pc) || !isD(B, qc))
       throw hx::Unsupported("pending pair that is neither inner x inner nor dense x dense");
     if (t.tau[pc] != tc || t.sigma[qc] != sc)
       throw hx::Unsupported("dense sub-views (ragged cluster trees)");
-    P.mat_terms.push_back(make_term(hx::BUF_A, A.d_off[pc], int32_t(m), 0, hx::BUF_B,
-                                    B.d_off[qc], int32_t(kr), 1, int32_t(kr), lo(tc), lo(sc),
-                                    m, n));
-    P.info.n_dxd++;
-  }
-
-  void log(int block, int k, int a, int b, int r) {
-    P.log_block.push_back(block);
-    P.log_kind.push_back(int8_t(k));
-    P.log_a.push_back(a);
-    P.log_b.push_back(b);
-    P.log_rank.push_back(r);
-    P.info.created[k]++;
-  }
-
-  // --------------------------------------------------------------- grouped term factors
-  // workspace bound (doubles) for one batch of gathered factors, and for its cores
-  static constexpr int64_t budget = int64_t(1) << 28;
-
-  void build_groups() {
-    const int nn = t.n_nodes;
-    const size_t nr = recs.size();
-    // counting sort of the terms by (side, X)
-    std::vector<int32_t> cnt(2 * size_t(nn) + 1, 0);
-    auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
-    for (const TRec& r : recs) cnt[key(r) + 1]++;
-    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-    std::vector<int32_t> order(nr);
-    {
-      std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
-      for (size_t i = 0; i < nr; ++i) order[pos[key(recs[i])]++] = int32_t(i);
-    }
-    std::vector<int> leaves;
-    std::vector<std::vector<Term>> bands;
-    int64_t gat_cur = 0, core_cur = 0;
-    auto close_batch = [&]() {
-      hx_plan::Batch& bt = P.batches.back();
-      bt.gather_end = int64_t(P.gather.size());
-      bt.core_end = int64_t(P.core_tiles.size());
-      bt.fac_end = int64_t(P.fac_tiles.size());
-    };
-    auto open_batch = [&]() {
-      P.batches.push_back(hx_plan::Batch{int64_t(P.gather.size()), 0,
-                                         int64_t(P.core_tiles.size()), 0,
-                                         int64_t(P.fac_tiles.size()), 0});
-      gat_cur = 0;
-      core_cur = 0;
-    };
-    open_batch();
-    for (int g = 0; g < 2 * nn; ++g) {
-      const int32_t b0 = cnt[g], b1 = cnt[g + 1];
-      if (b0 == b1) continue;
-      const int side = g >= nn ? 1 : 0;
-      const int X = g - side * nn;
-      const hx_operand& opX = side == 0 ? A : B;
-      // rows of the computed factor and of the middle cluster rho'
-      const int rows_cl = side == 0 ? t.tau[X] : t.sigma[X];
-      const int rho = side == 0 ? t.sigma[X] : t.tau[X];
-      const int64_t R = sz(rows_cl), kr = sz(rho);
-      int64_t ktot = 0;
-      for (int32_t i = b0; i < b1; ++i) ktot += recs[order[i]].k;
-      leaves.clear();
-      double mv = 0, bytes = 0;
-      subtree_leaves(opX, X, leaves, mv, bytes);
-      int64_t core_need = 0;
-      for (int l : leaves)
-        if (isF(opX, l)) core_need += align16(int64_t(opX.rank[l]) * ktot);
-      const int64_t gat_need = align16(kr * ktot);
-      if ((gat_cur + gat_need > budget || core_cur + core_need > budget) &&
-          (gat_cur > 0 || core_cur > 0)) {
-        close_batch();
-        open_batch();
-      }
-      const int64_t out = P.term_elems;
-      P.term_elems = align16(P.term_elems + R * ktot);
-      const int64_t gat = gat_cur;
-      gat_cur += gat_need;
-      P.gather_elems = std::max(P.gather_elems, gat_cur);
-      // gather the thin factors side by side, patch the materialization terms
-      int64_t col = 0;
-      for (int32_t i = b0; i < b1; ++i) {
-        const TRec& r = recs[order[i]];
-        hx::CopyRec cp;
-        cp.src_buf = side == 0 ? hx::BUF_B : hx::BUF_A;
-        cp.src_off = side == 0 ? B.u_off[r.qc] : A.v_off[r.pc];
-        cp.dst_off = gat + col * kr;
-        cp.n = kr * r.k;
-        P.gather.push_back(cp);
-        Term& mt = P.mat_terms[r.mat];
-        if (side == 0) {
-          mt.a_off = out + col * R;
-          mt.a_ld = int32_t(R);
-        } else {
-          mt.b_off = out + col * R;
-          mt.b_ld = int32_t(R);
-        }
-        col += r.k;
-      }
-      // X applied to G: leaves of X
-      P.info.flops_form += double(ktot) * mv;
-      P.info.bytes_form += double(b1 - b0) * bytes + 8.0 * double(ktot) * double(kr + R);
-      P.info.n_xgroups++;
-      const int64_t nb = (R + T - 1) / T;
-      bands.assign(size_t(nb), {});
-      for (int l : leaves) {
-        // A side: leaf l = (tau_l, rho_l) rows tau_l;  B side: l = (rho_l, sigma_l) rows sigma_l
-        const int rl = side == 0 ? t.sigma[l] : t.tau[l];   // middle-cluster part
-        const int ol = side == 0 ? t.tau[l] : t.sigma[l];   // output rows
-        const int64_t roff = lo(rl) - lo(rho);
-        Term piece;
-        if (isF(opX, l)) {
-          const int kl = opX.rank[l];
-          if (kl == 0) continue;
-          // core_l = V_l^T G[rho_l] (A side) or U_l^T G[rho_l] (B side): kl x ktot
-          const int64_t core = core_cur;
-          core_cur = align16(core_cur + int64_t(kl) * ktot);
-          P.core_elems = std::max(P.core_elems, core_cur);
-          const int64_t mid_f = side == 0 ? opX.v_off[l] : opX.u_off[l];
-          std::vector<std::vector<Term>> one(size_t((kl + T - 1) / T));
-          const Term cp = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, mid_f, int32_t(sz(rl)), 1,
-                                    hx::BUF_GATHER, gat + roff, int32_t(kr), 1, int32_t(sz(rl)),
-                                    0, 0, kl, ktot);
-          for (auto& v : one) v.push_back(cp);
-          emit_band_tiles(P.core_terms, P.core_tiles, P.core_groups, hx::BUF_CORE, core, kl, ktot,
-                          0, one);
-          const int64_t out_f = side == 0 ? opX.u_off[l] : opX.v_off[l];
-          piece = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, out_f, int32_t(sz(ol)), 0,
-                            hx::BUF_CORE, core, kl, 1, kl, lo(ol), 0, sz(ol), ktot);
-        } else {
-          // dense: D_l G[rho_l] (A side) or D_l^T G[rho_l] (B side)
-          piece = make_term(side == 0 ? hx::BUF_A : hx::BUF_B, opX.d_off[l], int32_t(sz(t.tau[l])),
-                            uint8_t(side == 0 ? 0 : 1), hx::BUF_GATHER, gat + roff, int32_t(kr), 1,
-                            int32_t(sz(rl)), lo(ol), 0, sz(ol), ktot);
-        }
-        const int64_t a = (lo(ol) - lo(rows_cl)) / T;
-        const int64_t e = (lo(ol) + sz(ol) - lo(rows_cl) - 1) / T;
-        for (int64_t bnd = std::max<int64_t>(a, 0); bnd <= std::min<int64_t>(e, nb - 1); ++bnd)
-          bands[size_t(bnd)].push_back(piece);
-      }
-      emit_band_tiles(P.fac_terms, P.fac_tiles, P.fac_groups, hx::BUF_TERM, out, R, ktot,
-                      lo(rows_cl), bands);
-    }
-    close_batch();
+    w.o.terms.push_back(make_term(hx::BUF_A, A.d_off[pc], int32_t(m), 0, hx::BUF_B, B.d_off[qc],
+                                  int32_t(kr), 1, int32_t(kr), lo(tc), lo(sc), m, n));
+    w.o.n_dxd++;
   }
 
   // --------------------------------------------------------------- the descent
   // Pending pairs of (virtual) block tc x sc split onto child (ti, si):
-  // sumexpr.py:146-153.  Created terms are appended to P.mat_terms (current group).
-  void split_pairs(int tc, int sc, int ti, int si, const std::vector<std::pair<int, int>>& pend,
-                   std::vector<std::pair<int, int>>& sub, int log_block, int64_t& K) {
+  // sumexpr.py:146-153.  Created terms are appended to the current group.
+  void split_pairs(Walk& w, int tc, int sc, int ti, int si, const PairList& pend, PairList& sub,
+                   int log_block, int64_t& K) const {
     const int tcc = t.c_child[2 * tc + ti], scc = t.c_child[2 * sc + si];
     for (const auto& pq : pend) {
       const int p = pq.first, q = pq.second;
@@ -373,7 +251,7 @@ struct Builder {
         const int pc = child_of(p, ti, ri), qc = child_of(q, ri, si);
         if (pc < 0 || qc < 0) throw std::runtime_error("block tree is not level-conserving");
         if (isF(A, pc) || isF(B, qc)) {
-          K += create_lr(tcc, scc, pc, qc, log_block);
+          K += create_lr(w, tcc, scc, pc, qc, log_block);
         } else {
           sub.emplace_back(pc, qc);
         }
@@ -383,42 +261,44 @@ struct Builder {
 
   // Expansion of the pending inner x inner pairs of a far leaf over virtual sub-blocks
   // (exact).
-  void expand(int tc, int sc, const std::vector<std::pair<int, int>>& pend,
-              std::vector<VGroup>& vg, int64_t& K, double& fdd, double& edd) {
+  void expand(Walk& w, int tc, int sc, const PairList& pend, std::vector<VGroup>& vg,
+              int64_t& K, double& fdd, double& edd) const {
     if (pend.empty()) return;
     if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0)
       throw std::runtime_error("expand reached leaf clusters");
+    Out& o = w.o;
     for (int ti = 0; ti < 2; ++ti)
       for (int si = 0; si < 2; ++si) {
         const int tcc = t.c_child[2 * tc + ti], scc = t.c_child[2 * sc + si];
-        const int32_t gb = int32_t(P.mat_terms.size());
-        std::vector<std::pair<int, int>> sub;
+        const int32_t gb = int32_t(o.terms.size());
+        PairList sub;
         int64_t Kv = 0;
-        split_pairs(tc, sc, ti, si, pend, sub, -1, Kv);
+        split_pairs(w, tc, sc, ti, si, pend, sub, -1, Kv);
         K += Kv;
-        P.info.n_terms_expand += int64_t(P.mat_terms.size()) - gb;
+        o.n_terms_expand += int64_t(o.terms.size()) - gb;
         const bool leaf_level = t.c_child[2 * tcc] < 0 || t.c_child[2 * scc] < 0;
         if (leaf_level) {
           for (const auto& pq : sub) {
-            create_dxd(tcc, scc, pq.first, pq.second);
+            create_dxd(w, tcc, scc, pq.first, pq.second);
             const double mm = double(sz(tcc)), nn = double(sz(scc)),
                          kk = double(sz(t.sigma[pq.first]));
             fdd += 2.0 * mm * kk * nn;
             edd += mm * kk + kk * nn;
           }
         }
-        const int32_t ge = int32_t(P.mat_terms.size());
+        const int32_t ge = int32_t(o.terms.size());
         if (ge > gb) {
-          P.mat_groups_all.push_back(Group{gb, ge});
-          vg.push_back(VGroup{int32_t(P.mat_groups_all.size() - 1), lo(tcc), lo(tcc) + sz(tcc),
-                              lo(scc), lo(scc) + sz(scc)});
+          o.groups.push_back(Group{gb, ge});
+          vg.push_back(VGroup{GRef{w.self, int32_t(o.groups.size() - 1)}, lo(tcc),
+                              lo(tcc) + sz(tcc), lo(scc), lo(scc) + sz(scc)});
         }
-        if (!leaf_level) expand(tcc, scc, sub, vg, K, fdd, edd);
+        if (!leaf_level) expand(w, tcc, scc, sub, vg, K, fdd, edd);
       }
   }
 
-  void emit_leaf_tiles(int b, bool far, const std::vector<VGroup>& vg, int64_t K, double fdd,
-                       double edd) {
+  void emit_leaf_tiles(Walk& w, int b, bool far, const std::vector<VGroup>& vg, int64_t K,
+                       double fdd, double edd) const {
+    Out& o = w.o;
     const int tc = t.tau[b], sc = t.sigma[b];
     const int64_t m = sz(tc), n = sz(sc);
     hx::OutLeaf L;
@@ -428,21 +308,21 @@ struct Builder {
     L.n = int32_t(n);
     L.row0 = lo(tc);
     L.col0 = lo(sc);
-    int64_t& ws = far ? ws_far : ws_near;
+    int64_t& ws = far ? o.ws_far : o.ws_near;
     L.ws_off = ws;
     L.K = K;
     L.fdd = fdd;
     L.edd = edd;
     ws = align16(ws + m * n);
-    L.tile_begin = int32_t(P.mat_tiles.size());
-    L.sumsq_begin = P.n_sumsq;
+    L.tile_begin = int32_t(o.tiles.size());
+    L.sumsq_begin = o.n_sumsq;
     int32_t prev_gb = -1, prev_ge = -1;
-    std::vector<int32_t> cur, prev;
+    std::vector<GRef> cur, prev;
     for (int64_t j = 0; j < n; j += T) {
       for (int64_t i = 0; i < m; i += T) {
         const int64_t r0 = lo(tc) + i, r1 = lo(tc) + std::min<int64_t>(m, i + T);
         const int64_t c0 = lo(sc) + j, c1 = lo(sc) + std::min<int64_t>(n, j + T);
-        cur.assign(path_groups.begin(), path_groups.end());
+        cur.assign(w.path.begin(), w.path.end());
         for (const VGroup& v : vg)
           if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0) cur.push_back(v.g);
         int32_t gb, ge;
@@ -450,9 +330,9 @@ struct Builder {
           gb = prev_gb;
           ge = prev_ge;
         } else {
-          gb = int32_t(P.mat_groups.size());
-          for (int32_t g : cur) P.mat_groups.push_back(P.mat_groups_all[g]);
-          ge = int32_t(P.mat_groups.size());
+          gb = int32_t(o.tile_groups.size());
+          o.tile_groups.insert(o.tile_groups.end(), cur.begin(), cur.end());
+          ge = int32_t(o.tile_groups.size());
           prev = cur;
           prev_gb = gb;
           prev_ge = ge;
@@ -469,37 +349,38 @@ struct Builder {
         tl.g_end = ge;
         tl.out_buf = hx::BUF_TILE;
         tl.mode = hx::MODE_STORE_SUMSQ;
-        tl.aux = P.n_sumsq++;
-        P.mat_tiles.push_back(tl);
+        tl.aux = o.n_sumsq++;
+        o.tiles.push_back(tl);
       }
     }
-    L.tile_end = int32_t(P.mat_tiles.size());
-    L.sumsq_end = P.n_sumsq;
-    P.info.max_out_dim = std::max<int64_t>(P.info.max_out_dim, std::max(m, n));
-    P.leaves.push_back(L);
+    L.tile_end = int32_t(o.tiles.size());
+    L.sumsq_end = o.n_sumsq;
+    o.max_out_dim = std::max<int64_t>(o.max_out_dim, std::max(m, n));
+    o.leaves.push_back(L);
   }
 
-  int64_t path_K = 0;
-  int64_t ws_far = 0, ws_near = 0;
-
-  void visit(int b, const std::vector<std::pair<int, int>>& pend) {
+  // DFS below block b (whose own terms are already created).  With `tasks`, inner children
+  // at block level `cut` are deferred as parallel tasks instead of descended.
+  void visit(Walk& w, int b, int level, const PairList& pend, int cut,
+             std::vector<Task>* tasks) const {
+    Out& o = w.o;
     const int tc = t.tau[b], sc = t.sigma[b];
     for (int ci = 0; ci < 4; ++ci) {
       const int c = t.child[4 * b + ci];
       if (c < 0 || !owned_sub[c]) continue;
-      const int32_t gb = int32_t(P.mat_terms.size());
-      std::vector<std::pair<int, int>> sub;
+      const int32_t gb = int32_t(o.terms.size());
+      PairList sub;
       int64_t Kc = 0;
-      split_pairs(tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
-      P.info.n_terms_real += int64_t(P.mat_terms.size()) - gb;
+      split_pairs(w, tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
+      o.n_terms_real += int64_t(o.terms.size()) - gb;
       // DxD pairs of a leaf at the leaf level join the leaf's own group
       const bool leaf_level = kind(c) != INNER &&
                               (t.c_child[2 * t.tau[c]] < 0 || t.c_child[2 * t.sigma[c]] < 0);
       double fdd = 0, edd = 0;
-      std::vector<std::pair<int, int>> rest;
+      PairList rest;
       if (leaf_level) {
         for (const auto& pq : sub) {
-          create_dxd(t.tau[c], t.sigma[c], pq.first, pq.second);
+          create_dxd(w, t.tau[c], t.sigma[c], pq.first, pq.second);
           const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c])),
                        kk = double(sz(t.sigma[pq.first]));
           fdd += 2.0 * mm * kk * nn;
@@ -508,48 +389,430 @@ struct Builder {
       } else {
         rest.swap(sub);
       }
-      const int32_t ge = int32_t(P.mat_terms.size());
+      const int32_t ge = int32_t(o.terms.size());
       const bool has = ge > gb;
       if (has) {
-        P.mat_groups_all.push_back(Group{gb, ge});
-        path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
+        o.groups.push_back(Group{gb, ge});
+        w.path.push_back(GRef{w.self, int32_t(o.groups.size() - 1)});
       }
-      const int64_t save_K = path_K;
-      path_K += Kc;
+      const int64_t save_K = w.path_K;
+      w.path_K += Kc;
       if (kind(c) == INNER) {
-        visit(c, rest);
+        if (tasks && level + 1 >= cut) {
+          tasks->push_back(Task{c, std::move(rest), w.path, w.path_K,
+                                int64_t(o.log_block.size())});
+        } else {
+          visit(w, c, level + 1, rest, cut, tasks);
+        }
       } else {
         std::vector<VGroup> vg;
-        int64_t K = path_K;
-        if (kind(c) == FAR) expand(t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
+        int64_t K = w.path_K;
+        if (kind(c) == FAR) expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
         else if (!rest.empty()) throw hx::Unsupported("near leaf above the leaf level");
         const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
         if (kind(c) == NEAR) {
-          P.info.flops_near += fdd + 2.0 * mm * nn * double(K);
-          P.info.bytes_near += 8.0 * (double(K) * (mm + nn) + edd + mm * nn);
-          P.info.n_near++;
+          o.flops_near += fdd + 2.0 * mm * nn * double(K);
+          o.bytes_near += 8.0 * (double(K) * (mm + nn) + edd + mm * nn);
+          o.n_near++;
         } else {
-          P.info.n_far++;
+          o.n_far++;
         }
-        emit_leaf_tiles(c, kind(c) == FAR, vg, K, fdd, edd);
+        emit_leaf_tiles(w, c, kind(c) == FAR, vg, K, fdd, edd);
       }
-      path_K = save_K;
-      if (has) path_groups.pop_back();
+      w.path_K = save_K;
+      if (has) w.path.pop_back();
+    }
+  }
+
+  int choose_cut() const {
+    // first block level holding enough inner blocks to keep every thread busy
+    const int want = 8 * std::max(1, omp_get_max_threads());
+    std::vector<int> level_nodes{0}, next;
+    for (int level = 0; level < 64 && !level_nodes.empty(); ++level) {
+      int inner = 0;
+      next.clear();
+      for (int b : level_nodes)
+        if (kind(b) == INNER) {
+          ++inner;
+          for (int c = 0; c < 4; ++c)
+            if (t.child[4 * b + c] >= 0) next.push_back(t.child[4 * b + c]);
+        }
+      if (inner >= want) return level;
+      level_nodes.swap(next);
+    }
+    return 1 << 30;  // small tree: no parallel tasks
+  }
+
+  // --------------------------------------------------------------- merge of the outputs
+  void merge(std::vector<Out>& outs) {
+    const size_t no = outs.size();
+    std::vector<int64_t> b_terms(no + 1, 0), b_tg(no + 1, 0), b_tiles(no + 1, 0),
+        b_sumsq(no + 1, 0), b_far(no + 1, 0), b_near(no + 1, 0), b_recs(no + 1, 0),
+        b_leaves(no + 1, 0);
+    for (size_t i = 0; i < no; ++i) {
+      const Out& o = outs[i];
+      b_terms[i + 1] = b_terms[i] + int64_t(o.terms.size());
+      b_tg[i + 1] = b_tg[i] + int64_t(o.tile_groups.size());
+      b_tiles[i + 1] = b_tiles[i] + int64_t(o.tiles.size());
+      b_sumsq[i + 1] = b_sumsq[i] + o.n_sumsq;
+      b_far[i + 1] = b_far[i] + o.ws_far;
+      b_near[i + 1] = b_near[i] + o.ws_near;
+      b_recs[i + 1] = b_recs[i] + int64_t(o.recs.size());
+      b_leaves[i + 1] = b_leaves[i] + int64_t(o.leaves.size());
+    }
+    P.mat_terms.resize(size_t(b_terms[no]));
+    P.mat_groups.resize(size_t(b_tg[no]));
+    P.mat_tiles.resize(size_t(b_tiles[no]));
+    P.leaves.resize(size_t(b_leaves[no]));
+    recs.resize(size_t(b_recs[no]));
+    ws_far_total = b_far[no];
+    ws_near_total = b_near[no];
+    P.n_sumsq = int32_t(b_sumsq[no]);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < int64_t(no); ++i) {
+      const Out& o = outs[i];
+      std::copy(o.terms.begin(), o.terms.end(), P.mat_terms.begin() + b_terms[i]);
+      for (size_t r = 0; r < o.recs.size(); ++r) {
+        TRec x = o.recs[r];
+        x.mat += int32_t(b_terms[i]);
+        recs[size_t(b_recs[i]) + r] = x;
+      }
+      for (size_t g = 0; g < o.tile_groups.size(); ++g) {
+        const GRef ref = o.tile_groups[g];
+        Group gr = outs[ref.first].groups[ref.second];
+        gr.t_begin += int32_t(b_terms[ref.first]);
+        gr.t_end += int32_t(b_terms[ref.first]);
+        P.mat_groups[size_t(b_tg[i]) + g] = gr;
+      }
+      for (size_t l = 0; l < o.leaves.size(); ++l) {
+        hx::OutLeaf L = o.leaves[l];
+        const int64_t wb = L.kind == 1 ? b_far[i] : b_near[i];
+        L.ws_off += wb;
+        for (int32_t k = L.tile_begin; k < L.tile_end; ++k) {
+          Tile tl = o.tiles[k];
+          tl.out_off += wb;
+          tl.g_begin += int32_t(b_tg[i]);
+          tl.g_end += int32_t(b_tg[i]);
+          tl.aux += int32_t(b_sumsq[i]);
+          P.mat_tiles[size_t(b_tiles[i]) + k] = tl;
+        }
+        L.tile_begin += int32_t(b_tiles[i]);
+        L.tile_end += int32_t(b_tiles[i]);
+        L.sumsq_begin += int32_t(b_sumsq[i]);
+        L.sumsq_end += int32_t(b_sumsq[i]);
+        P.leaves[size_t(b_leaves[i]) + l] = L;
+      }
+    }
+    // restrict log in the reference's visiting order: each subtree's log goes right after
+    // the top-part entries logged before the subtree was deferred
+    {
+      const Out& top = outs[0];
+      size_t pos = 0;
+      auto append = [&](const Out& o, size_t a, size_t e) {
+        P.log_block.insert(P.log_block.end(), o.log_block.begin() + a, o.log_block.begin() + e);
+        P.log_kind.insert(P.log_kind.end(), o.log_kind.begin() + a, o.log_kind.begin() + e);
+        P.log_a.insert(P.log_a.end(), o.log_a.begin() + a, o.log_a.begin() + e);
+        P.log_b.insert(P.log_b.end(), o.log_b.begin() + a, o.log_b.begin() + e);
+        P.log_rank.insert(P.log_rank.end(), o.log_rank.begin() + a, o.log_rank.begin() + e);
+      };
+      for (size_t i = 1; i < no; ++i) {
+        const size_t at = size_t(task_log_pos[i - 1]);
+        append(top, pos, at);
+        pos = at;
+        append(outs[i], 0, outs[i].log_block.size());
+      }
+      append(top, pos, top.log_block.size());
+    }
+    hx_plan_info& I = P.info;
+    for (const Out& o : outs) {
+      I.n_terms_real += o.n_terms_real;
+      I.n_terms_expand += o.n_terms_expand;
+      I.n_dxd += o.n_dxd;
+      for (int k = 0; k < 3; ++k) I.created[k] += o.created[k];
+      I.n_far += o.n_far;
+      I.n_near += o.n_near;
+      I.max_out_dim = std::max(I.max_out_dim, o.max_out_dim);
+      I.flops_near += o.flops_near;
+      I.bytes_near += o.bytes_near;
+    }
+  }
+
+  int64_t ws_far_total = 0, ws_near_total = 0;
+  std::vector<int64_t> task_log_pos;
+
+  // --------------------------------------------------------------- grouped term factors
+  // workspace bound (doubles) for one batch of gathered factors, and for its cores
+  static constexpr int64_t budget = int64_t(1) << 28;
+
+  struct GInfo {
+    int32_t b0, b1;   // term range in `order`
+    int32_t X, rows_cl, rho;
+    int8_t side;
+    int64_t R, kr, ktot;
+    std::vector<int> leaves;  // leaves of X (DFS order)
+    int64_t srows;            // rows of the stacked cores (sum of the leaf ranks)
+    int64_t n_core_tiles, n_core_groups, n_core_terms;
+    int64_t n_fac_tiles, n_fac_groups, n_fac_terms;
+    double mv, bytes;
+    // offsets (second pass)
+    int64_t out, gat, core;
+    int64_t o_gather, o_ct, o_cg, o_cm, o_ft, o_fg, o_fm;
+  };
+
+  static int64_t nbands(int64_t rows, int T) { return (rows + T - 1) / T; }
+  static int64_t bands_hit(int64_t a, int64_t len, int64_t nb, int T) {
+    const int64_t b0 = std::max<int64_t>(a / T, 0);
+    const int64_t b1 = std::min<int64_t>((a + len - 1) / T, nb - 1);
+    return b1 >= b0 ? b1 - b0 + 1 : 0;
+  }
+
+  // Tiles of an R x C output (ld R) whose row band i uses group gbase + i.
+  void write_band_tiles(Tile* tiles, uint8_t out_buf, int64_t out_off, int64_t R, int64_t C,
+                        int64_t row_base, int32_t gbase) const {
+    int64_t w = 0;
+    for (int64_t i = 0, band = 0; i < R; i += T, ++band) {
+      const int64_t r1 = std::min<int64_t>(R, i + T);
+      for (int64_t j = 0; j < C; j += T) {
+        Tile& tl = tiles[w++];
+        std::memset(&tl, 0, sizeof(tl));
+        tl.out_off = out_off + i + j * R;
+        tl.out_ld = int32_t(R);
+        tl.row0 = int32_t(row_base + i);
+        tl.col0 = int32_t(j);
+        tl.rows = int16_t(r1 - i);
+        tl.cols = int16_t(std::min<int64_t>(C, j + T) - j);
+        tl.g_begin = gbase + int32_t(band);
+        tl.g_end = gbase + int32_t(band) + 1;
+        tl.aux = -1;
+        tl.out_buf = out_buf;
+        tl.mode = hx::MODE_STORE;
+      }
+    }
+  }
+
+  void build_groups() {
+    const int nn = t.n_nodes;
+    const size_t nr = recs.size();
+    // counting sort of the terms by (side, X)
+    std::vector<int32_t> cnt(2 * size_t(nn) + 1, 0);
+    auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
+    for (const TRec& r : recs) cnt[key(r) + 1]++;
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    std::vector<int32_t> order(nr);
+    {
+      std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
+      for (size_t i = 0; i < nr; ++i) order[pos[key(recs[i])]++] = int32_t(i);
+    }
+    std::vector<GInfo> G;
+    for (int g = 0; g < 2 * nn; ++g) {
+      if (cnt[g] == cnt[g + 1]) continue;
+      GInfo gi{};
+      gi.b0 = cnt[g];
+      gi.b1 = cnt[g + 1];
+      gi.side = int8_t(g >= nn ? 1 : 0);
+      gi.X = g - gi.side * nn;
+      G.push_back(std::move(gi));
+    }
+    const int64_t ng = int64_t(G.size());
+    // pass 1 (parallel): leaves of X and work counts
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
+      GInfo& g = G[gi_];
+      const hx_operand& opX = g.side == 0 ? A : B;
+      g.rows_cl = g.side == 0 ? t.tau[g.X] : t.sigma[g.X];
+      g.rho = g.side == 0 ? t.sigma[g.X] : t.tau[g.X];
+      g.R = sz(g.rows_cl);
+      g.kr = sz(g.rho);
+      g.ktot = 0;
+      for (int32_t i = g.b0; i < g.b1; ++i) g.ktot += recs[order[i]].k;
+      g.mv = 0;
+      g.bytes = 0;
+      subtree_leaves(opX, g.X, g.leaves, g.mv, g.bytes);
+      const int64_t ct = nbands(g.ktot, T);
+      const int64_t nb = nbands(g.R, T);
+      g.srows = 0;
+      g.n_fac_terms = 0;
+      for (int l : g.leaves) {
+        const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];
+        if (isF(opX, l)) {
+          if (opX.rank[l] == 0) continue;
+          g.srows += opX.rank[l];
+        }
+        g.n_fac_terms += bands_hit(lo(ol) - lo(g.rows_cl), sz(ol), nb, T);
+      }
+      const int64_t nbs = nbands(g.srows, T);
+      int64_t r = 0, terms = 0;
+      for (int l : g.leaves)
+        if (isF(opX, l) && opX.rank[l] > 0) {
+          terms += bands_hit(r, opX.rank[l], nbs, T);
+          r += opX.rank[l];
+        }
+      g.n_core_terms = terms;
+      g.n_core_groups = nbs;
+      g.n_core_tiles = nbs * ct;
+      g.n_fac_groups = nb;
+      g.n_fac_tiles = nb * ct;
+    }
+    // pass 2 (sequential): batches and offsets
+    int64_t gat_cur = 0, core_cur = 0;
+    int64_t o_gather = 0, o_ct = 0, o_cg = 0, o_cm = 0, o_ft = 0, o_fg = 0, o_fm = 0;
+    P.batches.push_back(hx_plan::Batch{0, 0, 0, 0, 0, 0});
+    for (GInfo& g : G) {
+      const int64_t gat_need = align16(g.kr * g.ktot);
+      const int64_t core_need = align16(g.srows * g.ktot);
+      if ((gat_cur + gat_need > budget || core_cur + core_need > budget) &&
+          (gat_cur > 0 || core_cur > 0)) {
+        hx_plan::Batch& b = P.batches.back();
+        b.gather_end = o_gather;
+        b.core_end = o_ct;
+        b.fac_end = o_ft;
+        P.batches.push_back(hx_plan::Batch{o_gather, 0, o_ct, 0, o_ft, 0});
+        gat_cur = core_cur = 0;
+      }
+      g.out = P.term_elems;
+      P.term_elems = align16(P.term_elems + g.R * g.ktot);
+      g.gat = gat_cur;
+      gat_cur += gat_need;
+      g.core = core_cur;
+      core_cur += core_need;
+      P.gather_elems = std::max(P.gather_elems, gat_cur);
+      P.core_elems = std::max(P.core_elems, core_cur);
+      g.o_gather = o_gather;
+      o_gather += g.b1 - g.b0;
+      g.o_ct = o_ct;
+      o_ct += g.n_core_tiles;
+      g.o_cg = o_cg;
+      o_cg += g.n_core_groups;
+      g.o_cm = o_cm;
+      o_cm += g.n_core_terms;
+      g.o_ft = o_ft;
+      o_ft += g.n_fac_tiles;
+      g.o_fg = o_fg;
+      o_fg += g.n_fac_groups;
+      g.o_fm = o_fm;
+      o_fm += g.n_fac_terms;
+      P.info.flops_form += double(g.ktot) * g.mv;
+      P.info.bytes_form += double(g.b1 - g.b0) * g.bytes + 8.0 * double(g.ktot) * double(g.kr + g.R);
+      P.info.n_xgroups++;
+    }
+    {
+      hx_plan::Batch& b = P.batches.back();
+      b.gather_end = o_gather;
+      b.core_end = o_ct;
+      b.fac_end = o_ft;
+    }
+    P.gather.resize(size_t(o_gather));
+    P.core_tiles.resize(size_t(o_ct));
+    P.core_groups.resize(size_t(o_cg));
+    P.core_terms.resize(size_t(o_cm));
+    P.fac_tiles.resize(size_t(o_ft));
+    P.fac_groups.resize(size_t(o_fg));
+    P.fac_terms.resize(size_t(o_fm));
+    // pass 3 (parallel): fill
+#pragma omp parallel for schedule(dynamic, 64)
+    for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
+      const GInfo& g = G[gi_];
+      const hx_operand& opX = g.side == 0 ? A : B;
+      const uint8_t xbuf = g.side == 0 ? hx::BUF_A : hx::BUF_B;
+      // gather the thin factors side by side, patch the materialization terms
+      int64_t col = 0;
+      for (int32_t i = g.b0; i < g.b1; ++i) {
+        const TRec& r = recs[order[i]];
+        hx::CopyRec& cp = P.gather[size_t(g.o_gather + (i - g.b0))];
+        cp.src_buf = g.side == 0 ? hx::BUF_B : hx::BUF_A;
+        cp.src_off = g.side == 0 ? B.u_off[r.qc] : A.v_off[r.pc];
+        cp.dst_off = g.gat + col * g.kr;
+        cp.n = g.kr * r.k;
+        cp.pad = 0;
+        Term& mt = P.mat_terms[r.mat];
+        if (g.side == 0) {
+          mt.a_off = g.out + col * g.R;
+          mt.a_ld = int32_t(g.R);
+        } else {
+          mt.b_off = g.out + col * g.R;
+          mt.b_ld = int32_t(g.R);
+        }
+        col += r.k;
+      }
+      // stacked cores S (srows x ktot, ld srows): rows [off_l, off_l + k_l) = V_l^T G[rho_l]
+      // (A side) or U_l^T G[rho_l] (B side)
+      const int64_t nbs = nbands(g.srows, T);
+      const int64_t nb = nbands(g.R, T);
+      {
+        int64_t w = g.o_cm;
+        for (int64_t band = 0; band < nbs; ++band) {
+          const int64_t ba = band * T, be = std::min<int64_t>(g.srows, ba + T);
+          const int32_t tb = int32_t(w);
+          int64_t off = 0;
+          for (int l : g.leaves) {
+            if (!isF(opX, l) || opX.rank[l] == 0) continue;
+            const int kl = opX.rank[l];
+            if (off < be && off + kl > ba) {
+              const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];
+              const int64_t roff = lo(rl) - lo(g.rho);
+              const int64_t mid_f = g.side == 0 ? opX.v_off[l] : opX.u_off[l];
+              P.core_terms[size_t(w++)] =
+                  make_term(xbuf, mid_f, int32_t(sz(rl)), 1, hx::BUF_GATHER, g.gat + roff,
+                            int32_t(g.kr), 1, int32_t(sz(rl)), off, 0, kl, g.ktot);
+            }
+            off += kl;
+          }
+          P.core_groups[size_t(g.o_cg + band)] = Group{tb, int32_t(w)};
+        }
+        write_band_tiles(&P.core_tiles[size_t(g.o_ct)], hx::BUF_CORE, g.core, g.srows, g.ktot, 0,
+                         int32_t(g.o_cg));
+      }
+      // row bands of X G (A side) / X^T G (B side)
+      {
+        int64_t w = g.o_fm;
+        for (int64_t band = 0; band < nb; ++band) {
+          const int64_t ba = lo(g.rows_cl) + band * T;
+          const int64_t be = std::min<int64_t>(lo(g.rows_cl) + g.R, ba + T);
+          const int32_t tb = int32_t(w);
+          int64_t off = 0;
+          for (int l : g.leaves) {
+            const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];  // middle-cluster part
+            const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];  // output rows
+            const bool lr = isF(opX, l);
+            const int kl = lr ? opX.rank[l] : 0;
+            if (lr && kl == 0) continue;
+            if (lo(ol) < be && lo(ol) + sz(ol) > ba) {
+              const int64_t roff = lo(rl) - lo(g.rho);
+              if (lr) {
+                const int64_t out_f = g.side == 0 ? opX.u_off[l] : opX.v_off[l];
+                P.fac_terms[size_t(w++)] =
+                    make_term(xbuf, out_f, int32_t(sz(ol)), 0, hx::BUF_CORE, g.core + off,
+                              int32_t(g.srows), 1, kl, lo(ol), 0, sz(ol), g.ktot);
+              } else {
+                P.fac_terms[size_t(w++)] =
+                    make_term(xbuf, opX.d_off[l], int32_t(sz(t.tau[l])),
+                              uint8_t(g.side == 0 ? 0 : 1), hx::BUF_GATHER, g.gat + roff,
+                              int32_t(g.kr), 1, int32_t(sz(rl)), lo(ol), 0, sz(ol), g.ktot);
+              }
+            }
+            off += kl;
+          }
+          P.fac_groups[size_t(g.o_fg + band)] = Group{tb, int32_t(w)};
+        }
+        write_band_tiles(&P.fac_tiles[size_t(g.o_ft)], hx::BUF_TERM, g.out, g.R, g.ktot,
+                         lo(g.rows_cl), int32_t(g.o_fg));
+      }
     }
   }
 
   // near blocks go after the far ones so the result download is two contiguous copies
   void place_near() {
-    P.near_ws_begin = ws_far;
-    P.tile_elems = ws_far + ws_near;
+    P.near_ws_begin = ws_far_total;
+    P.tile_elems = ws_far_total + ws_near_total;
     for (hx::OutLeaf& L : P.leaves) {
       if (L.kind != 2) continue;
-      L.ws_off += ws_far;
-      for (int32_t i = L.tile_begin; i < L.tile_end; ++i) P.mat_tiles[i].out_off += ws_far;
+      L.ws_off += ws_far_total;
+      for (int32_t i = L.tile_begin; i < L.tile_end; ++i) P.mat_tiles[i].out_off += ws_far_total;
     }
   }
 
   void run() {
+    const auto t0 = std::chrono::steady_clock::now();
     const int nn = t.n_nodes;
     owned_sub.assign(nn, 0);
     // bottom-up ownership: children have larger pre-order ids than their parent
@@ -565,29 +828,62 @@ struct Builder {
         owned_sub[b] = o;
       }
     }
+    std::vector<Out> outs(1);
     if (t.kind[0] != INNER) {
       // the root itself is a leaf: S(root) = {(A_root, B_root)} evaluated directly
       if (owned_sub[0]) {
+        Walk w{outs[0], 0, {}, 0};
         const int tc = t.tau[0], sc = t.sigma[0];
         if (t.kind[0] == FAR) throw hx::Unsupported("admissible root block");
-        const int32_t gb = int32_t(P.mat_terms.size());
-        create_dxd(tc, sc, 0, 0);
-        P.mat_groups_all.push_back(Group{gb, int32_t(P.mat_terms.size())});
-        path_groups.push_back(int32_t(P.mat_groups_all.size() - 1));
+        create_dxd(w, tc, sc, 0, 0);
+        outs[0].groups.push_back(Group{0, int32_t(outs[0].terms.size())});
+        w.path.push_back(GRef{0, 0});
         const double m = double(sz(tc));
         const double fdd = 2.0 * m * m * m, edd = 2.0 * m * m;
-        P.info.flops_near += fdd;
-        P.info.bytes_near += 8.0 * (edd + m * m);
-        P.info.n_near++;
+        outs[0].flops_near += fdd;
+        outs[0].bytes_near += 8.0 * (edd + m * m);
+        outs[0].n_near++;
         std::vector<VGroup> vg;
-        emit_leaf_tiles(0, false, vg, 0, fdd, edd);
+        emit_leaf_tiles(w, 0, false, vg, 0, fdd, edd);
       }
     } else {
-      std::vector<std::pair<int, int>> root{{0, 0}};
-      visit(0, root);
+      std::vector<Task> tasks;
+      {
+        Walk w{outs[0], 0, {}, 0};
+        const PairList root{{0, 0}};
+        visit(w, 0, 0, root, choose_cut(), &tasks);
+      }
+      outs.resize(1 + tasks.size());
+      for (const Task& tk : tasks) task_log_pos.push_back(tk.log_pos);
+      std::vector<std::string> errors(tasks.size());
+#pragma omp parallel for schedule(dynamic, 1)
+      for (int64_t i = 0; i < int64_t(tasks.size()); ++i) {
+        try {
+          Walk w{outs[size_t(i) + 1], int32_t(i + 1), tasks[size_t(i)].path,
+                 tasks[size_t(i)].path_K};
+          int lvl = 0;
+          visit(w, tasks[size_t(i)].c, lvl, tasks[size_t(i)].pend, 1 << 30, nullptr);
+        } catch (const std::exception& e) {
+          errors[size_t(i)] = e.what();
+        }
+      }
+      for (const std::string& e : errors)
+        if (!e.empty()) throw hx::Unsupported(e);
+      if (std::getenv("HX_PLAN_VERBOSE"))
+        std::fprintf(stderr, "[hx plan] %zu descent tasks, %.1f ms\n", tasks.size(),
+                     std::chrono::duration<double, std::milli>(
+                         std::chrono::steady_clock::now() - t0).count());
     }
+    merge(outs);
+    outs.clear();
+    const auto t1 = std::chrono::steady_clock::now();
     build_groups();
+    const auto t2 = std::chrono::steady_clock::now();
     place_near();
+    if (std::getenv("HX_PLAN_VERBOSE"))
+      std::fprintf(stderr, "[hx plan] descent %.1f ms, groups %.1f ms, %zu terms\n",
+                   std::chrono::duration<double, std::milli>(t1 - t0).count(),
+                   std::chrono::duration<double, std::milli>(t2 - t1).count(), recs.size());
   }
 };
 
@@ -662,3 +958,23 @@ extern "C" int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kin
 }
 
 extern "C" void hx_plan_free(hx_plan* plan) { delete plan; }
+
+extern "C" int hx_plan_mma_flops(const hx_plan* plan, double* flops) {
+  if (!plan || !flops) return hx::fail(HX_EINVAL, "null argument");
+  const hx::pvec<Tile>* tiles[3] = {&plan->core_tiles, &plan->fac_tiles, &plan->mat_tiles};
+  const hx::pvec<Group>* groups[3] = {&plan->core_groups, &plan->fac_groups,
+                                         &plan->mat_groups};
+  const hx::pvec<Term>* terms[3] = {&plan->core_terms, &plan->fac_terms, &plan->mat_terms};
+  const double tt = double(plan->tile) * plan->tile;
+  for (int b = 0; b < 3; ++b) {
+    double f = 0;
+    for (const Tile& tl : *tiles[b])
+      for (int32_t g = tl.g_begin; g < tl.g_end; ++g) {
+        const Group gr = (*groups[b])[g];
+        for (int32_t i = gr.t_begin; i < gr.t_end; ++i)
+          f += 2.0 * tt * double(((*terms[b])[i].k + 3) & ~3);
+      }
+    flops[b] = f;
+  }
+  return HX_OK;
+}

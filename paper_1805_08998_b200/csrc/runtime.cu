@@ -54,7 +54,10 @@ struct DArr {
     ensure(n);
     if (n) CK(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, s));
   }
-  void upload(const std::vector<T>& v, cudaStream_t s) { upload(v.data(), v.size(), s); }
+  template <class Alloc>
+  void upload(const std::vector<T, Alloc>& v, cudaStream_t s) {
+    upload(v.data(), v.size(), s);
+  }
   void release() {
     if (p) cudaFree(p);
     p = nullptr;
@@ -334,9 +337,9 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
     CK(cudaEventRecord(c->ev[0], s));
 
     // ---- plan upload and buffers
-    const std::vector<Term>* T3[3] = {&P->core_terms, &P->fac_terms, &P->mat_terms};
-    const std::vector<Tile>* L3[3] = {&P->core_tiles, &P->fac_tiles, &P->mat_tiles};
-    const std::vector<Group>* G3[3] = {&P->core_groups, &P->fac_groups, &P->mat_groups};
+    const pvec<Term>* T3[3] = {&P->core_terms, &P->fac_terms, &P->mat_terms};
+    const pvec<Tile>* L3[3] = {&P->core_tiles, &P->fac_tiles, &P->mat_tiles};
+    const pvec<Group>* G3[3] = {&P->core_groups, &P->fac_groups, &P->mat_groups};
     for (int i = 0; i < 3; ++i) {
       c->terms[i].upload(*T3[i], s);
       c->tiles[i].upload(*L3[i], s);
