@@ -134,6 +134,7 @@ typedef struct hx_product_stats {
   int64_t out_elems;     /* doubles in the packed result                            */
   double fro2_total;     /* sum of squared Frobenius norms of all output blocks     */
   double dom_kernel_ms;  /* summed device time of the materialization launches      */
+  double ms_upload;      /* H2D of the plan's work lists (inside ms_total)          */
 } hx_product_stats;
 
 int hx_product(hx_ctx* ctx, const hx_plan* plan, const hx_product_cfg* cfg,

@@ -56,7 +56,7 @@ class HxProductStats(C.Structure):
         (name, C.c_int64) for name in ("far_leaves", "near_leaves", "degraded_blocks",
                                        "max_far_rank", "matvec_count", "sketch_rounds",
                                        "launches", "out_elems")] + [
-        ("fro2_total", C.c_double), ("dom_kernel_ms", C.c_double)]
+        ("fro2_total", C.c_double), ("dom_kernel_ms", C.c_double), ("ms_upload", C.c_double)]
 
 
 class HxError(RuntimeError):

@@ -137,7 +137,8 @@ template <int TM>
 __global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restrict__ tiles,
                                                            const Group* __restrict__ groups,
                                                            const Term* __restrict__ terms,
-                                                           BufPtrs bufs, double* __restrict__ sumsq,
+                                                           const __grid_constant__ BufPtrs bufs,
+                                                           double* __restrict__ sumsq,
                                                            int n_tiles) {
   using C = GemmCfg<TM>;
   __shared__ __align__(16) double smem[2 * C::STAGE];
@@ -167,6 +168,20 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restric
   cp_async_commit();
   while (have) {
     const int kcur = min(C::KC, tld.k - ld.k0);
+    // 8x8 fragments of this warp that the current term touches (terms created on a
+    // sub-block, or stacked cores, cover only part of the tile): skip the others
+    unsigned amask = 0, bmask = 0;
+    {
+      const int ra = tld.r_lo - tl.row0, rb = ra + tld.rows;
+      const int ca = tld.c_lo - tl.col0, cb = ca + tld.cols;
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a) {
+        const int f0 = wm * C::WT + a * 8;
+        if (f0 < rb && f0 + 8 > ra) amask |= 1u << a;
+        const int g0 = wn * C::WT + a * 8;
+        if (g0 < cb && g0 + 8 > ca) bmask |= 1u << a;
+      }
+    }
     // prefetch the following chunk into the other stage
     ld.k0 += C::KC;
     bool more = next_chunk(ld, groups, terms, C::KC, tld);
@@ -181,17 +196,31 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restric
     const double* sP = smem + stage * C::STAGE;
     const double* sQ = sP + C::KC * C::LDS;
     const int ksteps = (kcur + 3) >> 2;
-    for (int ks = 0; ks < ksteps; ++ks) {
-      const int kk = ks * 4 + (lane & 3);
-      double af[C::FR], bf[C::FR];
+    if (amask && bmask) {
+      const bool full = amask == (1u << C::FR) - 1 && bmask == (1u << C::FR) - 1;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double af[C::FR], bf[C::FR];
 #pragma unroll
-      for (int a = 0; a < C::FR; ++a) af[a] = sP[kk * C::LDS + wm * C::WT + a * 8 + (lane >> 2)];
+        for (int a = 0; a < C::FR; ++a)
+          af[a] = sP[kk * C::LDS + wm * C::WT + a * 8 + (lane >> 2)];
 #pragma unroll
-      for (int b = 0; b < C::FR; ++b) bf[b] = sQ[kk * C::LDS + wn * C::WT + b * 8 + (lane >> 2)];
+        for (int b = 0; b < C::FR; ++b)
+          bf[b] = sQ[kk * C::LDS + wn * C::WT + b * 8 + (lane >> 2)];
+        if (full) {
 #pragma unroll
-      for (int a = 0; a < C::FR; ++a)
+          for (int a = 0; a < C::FR; ++a)
 #pragma unroll
-        for (int b = 0; b < C::FR; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+            for (int b = 0; b < C::FR; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < C::FR; ++a)
+#pragma unroll
+            for (int b = 0; b < C::FR; ++b)
+              if ((amask >> a) & (bmask >> b) & 1u)
+                dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+        }
+      }
     }
     __syncthreads();
     stage ^= 1;

@@ -352,6 +352,7 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
     c->sumsq.ensure(size_t(P->n_sumsq));
     c->gather_recs.upload(P->gather, s);
     BufPtrs bp = c->ptrs();
+    CK(cudaEventRecord(c->ev[5], s));
 
     // ---- 1. term formation: gather thin factors per X-group, cores, X G products
     for (const hx_plan::Batch& bt : P->batches) {
@@ -603,8 +604,10 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
       float ms = 0;
       CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[4]));
       st->ms_total = ms;
-      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[1]));
+      CK(cudaEventElapsedTime(&ms, c->ev[5], c->ev[1]));
       st->ms_form = ms;
+      CK(cudaEventElapsedTime(&ms, c->ev[0], c->ev[5]));
+      st->ms_upload = ms;
       CK(cudaEventElapsedTime(&ms, c->ev[1], c->ev[2]));
       st->ms_mat = ms;
       st->dom_kernel_ms = ms;

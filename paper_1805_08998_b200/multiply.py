@@ -59,6 +59,8 @@ class MultReport:
     form_ms: float = 0.0
     materialize_ms: float = 0.0
     recompress_ms: float = 0.0
+    upload_ms: float = 0.0
+    out_elems: int = 0
     sketch_rounds: int = 0
     launches: int = 0
     fro2: float = 0.0
@@ -133,12 +135,14 @@ def _host_directory(h):
 
 
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
-                    device_operands=True):
+                    device_operands=True, fetch=True):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
     assembly) instead of uploading the host copy.  ``leaf_mask`` restricts the product to
-    the owned output leaves (multi-GPU partition)."""
+    the owned output leaves (multi-GPU partition).  ``fetch=False`` leaves the output
+    blocks in device memory (only ranks and the report come back): the device-resident
+    measurement of bench.py."""
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     policy = cfg.policy
@@ -193,15 +197,16 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     _lib.check(_lib.lib().hx_result_layout(dev.h, _lib.ptr(rank, _lib.i32p),
                                            _lib.ptr(deg, _lib.i8p), _lib.ptr(off, _lib.i64p)),
                "hx_result_layout")
-    res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
-    _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p), res.size),
-               "hx_result_download")
     data = {}
     degraded = set()
     ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
     kinds = leaves["kind"].tolist()
     rl, ol = rank.tolist(), off.tolist()
-    for i in range(nl):
+    if fetch:
+        res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
+        _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p), res.size),
+                   "hx_result_download")
+    for i in range(nl if fetch else 0):
         m, n, o = ms[i], ns[i], ol[i]
         if kinds[i] == 1:
             r = rl[i]
@@ -224,6 +229,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     rep.form_ms = st.ms_form
     rep.materialize_ms = st.ms_mat
     rep.recompress_ms = st.ms_recompress
+    rep.upload_ms = st.ms_upload
+    rep.out_elems = int(st.out_elems)
     rep.sketch_rounds = int(st.sketch_rounds)
     rep.launches = int(st.launches)
     rep.fro2 = float(st.fro2_total)
