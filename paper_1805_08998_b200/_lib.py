@@ -85,6 +85,8 @@ SIGNATURES = {
     "hx_pool_download": [C.c_void_p, C.c_void_p, f64p, C.c_int64],
     "hx_pool_free": [C.c_void_p, C.c_void_p],
     "hx_ctx_synchronize": [C.c_void_p],
+    "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
+                      C.c_int64, C.POINTER(f64p), i64p, f64p, C.c_int64],
     "hx_ctx_free": [C.c_void_p],
     "hx_last_error": [C.c_char_p, C.c_size_t],
     "hx_version": [],

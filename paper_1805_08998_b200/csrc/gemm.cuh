@@ -3,17 +3,21 @@
 // One CTA computes one Tile: out[rows x cols] (=|+=) sum over the tile's groups, over each
 // group's terms, of P_t(tile rows, :) * Q_t(:, tile cols)  (layouts in hx_types.h).
 // This single kernel runs every contraction of the product:
-//   * k x k cores            V_A^T U_B                        (_thin_product, sumexpr.py:99-107)
-//   * pushed-through factors V_B core^T, U_A core, X U_B, X^T V_A (sumexpr.py:103-117,
+//   * stacked k x k cores    V_l^T G, U_l^T G                 (_thin_product, sumexpr.py:99-107)
+//   * pushed-through factors X G, X^T G                       (sumexpr.py:103-117,
 //                            hmatrix.py:177-202)
 //   * block materialization  sum_j U_j V_j^T + sum_p D_A D_B  (SumExpression.apply_mat,
 //                            sumexpr.py:59-66; evaluate_dense, sumexpr.py:165-170)
 //   * sketch products        T Omega, T^T Q                   (recompression)
 //
-// TM x TM tile, 4 warps in a 2 x 2 grid; a warp owns (TM/2) x (TM/2) as (TM/16)^2 DMMA
-// 8x8 accumulators.  K is streamed in chunks of KC through double-buffered shared memory
-// filled with cp.async (8-byte, zero-filled outside the term's extent), so the next
-// chunk -- possibly of the next term -- loads while the current one multiplies.
+// TM x TM tile, 4 warps (2 x 2); a warp owns (TM/2)^2 as 8x8 DMMA accumulators.
+// Terms of the product have small k (ranks ~10-50), so K is streamed in chunks of KC = 32
+// "slots" that pack consecutive terms: a chunk is a list of segments (term, k offset,
+// slot count) with one staging layout.  Each operand is staged in the layout it has in HBM
+// so that copies are 16-byte cp.async where aligned: tile-contiguous operands as
+// [slot][tile index], k-contiguous ones as [tile index][slot].  Rows outside a term's
+// extent are zero-filled by the copies (src-size 0); unused pad slots are zeroed.  The
+// double-buffered chunk ring overlaps the next chunk's copies with the current DMMAs.
 #pragma once
 #include <cstdint>
 
@@ -31,10 +35,13 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                : "d"(a), "d"(b));
 }
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+__device__ __forceinline__ void cp_async16(unsigned saddr, const void* gmem, int valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(valid));
+}
+__device__ __forceinline__ void cp_async8(unsigned saddr, const void* gmem, int valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(saddr), "l"(gmem),
+               "r"(valid));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
 template <int N>
@@ -42,107 +49,253 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int TM>
+template <int TM_>
 struct GemmCfg {
-  static constexpr int KC = 16;            // k chunk
-  static constexpr int LDS = TM + 4;       // padded smem row (doubles): 2-way max on DMMA reads
-  static constexpr int WT = TM / 2;        // warp tile side
-  static constexpr int FR = WT / 8;        // 8x8 fragments per warp side
+  static constexpr int TM = TM_;
+  static constexpr int KC = 32;                // slots per chunk
+  static constexpr int LDI = TM + 4;           // [slot][i] row (doubles), 16B aligned
+  static constexpr int LDK = KC + 4;           // [i][slot] row (doubles), 16B aligned
+  static constexpr int OPSZ = (KC * LDI > TM * LDK) ? KC * LDI : TM * LDK;
+  static constexpr int WT = TM / 2;            // warp tile side
+  static constexpr int FR = WT / 8;            // 8x8 fragments per warp side
   static constexpr int THREADS = 128;
-  static constexpr int STAGE = 2 * KC * LDS;  // P + Q chunk (doubles)
+  static constexpr int STAGE = 2 * OPSZ;       // P + Q (doubles)
+  static constexpr int SMEM = 2 * STAGE * 8;
+  static constexpr int MAXSEG = 8;
 };
 
-// Cursor over the (group, term, k-chunk) sequence of one tile.
-struct ChunkCursor {
+using Gemm64 = GemmCfg<64>;
+using Gemm32 = GemmCfg<32>;
+
+// Cursor over (group, term, k offset) of one tile.
+struct Cursor {
   int g, g_end, t, t_end, k0;
+  Term tm;
 };
 
-template <int TM>
-__device__ __forceinline__ void load_chunk(double* __restrict__ sP, double* __restrict__ sQ,
-                                           const BufPtrs& bufs, const Term& tm, int k0,
-                                           int row0, int col0, int tile_rows, int tile_cols) {
-  using C = GemmCfg<TM>;
-  const int tid = threadIdx.x;
-  const double* A = bufs.p[tm.a_buf] + tm.a_off;
-  const double* B = bufs.p[tm.b_buf] + tm.b_off;
-  const int i0 = row0 - tm.r_lo;   // first term row of this tile
-  const int j0 = col0 - tm.c_lo;
-  const int kr = tm.k - k0;         // remaining k
-  // P chunk: TM rows x KC
-  if (tm.a_kc == 0) {
-#pragma unroll
-    for (int e = tid; e < TM * C::KC; e += C::THREADS) {
-      const int i = e % TM, kk = e / TM;
-      const int gi = i0 + i;
-      const bool v = (i < tile_rows) && (gi >= 0) && (gi < tm.rows) && (kk < kr);
-      const double* src = v ? A + gi + int64_t(k0 + kk) * tm.a_ld : A;
-      cp_async8(sP + kk * C::LDS + i, src, v);
-    }
-  } else {
-#pragma unroll
-    for (int e = tid; e < TM * C::KC; e += C::THREADS) {
-      const int kk = e % C::KC, i = e / C::KC;
-      const int gi = i0 + i;
-      const bool v = (i < tile_rows) && (gi >= 0) && (gi < tm.rows) && (kk < kr);
-      const double* src = v ? A + (k0 + kk) + int64_t(gi) * tm.a_ld : A;
-      cp_async8(sP + kk * C::LDS + i, src, v);
-    }
-  }
-  // Q chunk: KC x TM cols
-  if (tm.b_kc == 0) {
-#pragma unroll
-    for (int e = tid; e < TM * C::KC; e += C::THREADS) {
-      const int j = e % TM, kk = e / TM;
-      const int gj = j0 + j;
-      const bool v = (j < tile_cols) && (gj >= 0) && (gj < tm.cols) && (kk < kr);
-      const double* src = v ? B + gj + int64_t(k0 + kk) * tm.b_ld : B;
-      cp_async8(sQ + kk * C::LDS + j, src, v);
-    }
-  } else {
-#pragma unroll
-    for (int e = tid; e < TM * C::KC; e += C::THREADS) {
-      const int kk = e % C::KC, j = e / C::KC;
-      const int gj = j0 + j;
-      const bool v = (j < tile_cols) && (gj >= 0) && (gj < tm.cols) && (kk < kr);
-      const double* src = v ? B + (k0 + kk) + int64_t(gj) * tm.b_ld : B;
-      cp_async8(sQ + kk * C::LDS + j, src, v);
-    }
-  }
-}
+struct Chunk {
+  int used;              // slots filled (0 = no chunk)
+  int akc, bkc;          // staged layouts of P and Q
+  unsigned amask, bmask; // 8x8 fragments of this warp touched by any segment
+};
 
-// Advance the cursor to the next non-empty chunk; returns false at the end.
-__device__ __forceinline__ bool next_chunk(ChunkCursor& c, const Group* __restrict__ groups,
-                                           const Term* __restrict__ terms, int KC, Term& tm) {
+// Advance to the next term with k > 0 (c.k0 reset); false at the end of the tile.
+__device__ __forceinline__ bool next_term(Cursor& c, const Group* __restrict__ groups,
+                                          const Term* __restrict__ terms) {
   while (true) {
+    ++c.t;
     if (c.t < c.t_end) {
-      if (c.k0 < tm.k) return true;
-      ++c.t;
+      c.tm = terms[c.t];
       c.k0 = 0;
-      if (c.t < c.t_end) {
-        tm = terms[c.t];
-        continue;
-      }
+      if (c.tm.k > 0) return true;
+      continue;
     }
     ++c.g;
     if (c.g >= c.g_end) return false;
     const Group gr = groups[c.g];
-    c.t = gr.t_begin;
+    c.t = gr.t_begin - 1;
     c.t_end = gr.t_end;
-    c.k0 = 0;
-    if (c.t < c.t_end) tm = terms[c.t];
   }
 }
 
-template <int TM>
-__global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restrict__ tiles,
-                                                           const Group* __restrict__ groups,
-                                                           const Term* __restrict__ terms,
-                                                           const __grid_constant__ BufPtrs bufs,
-                                                           double* __restrict__ sumsq,
-                                                           int n_tiles) {
-  using C = GemmCfg<TM>;
-  __shared__ __align__(16) double smem[2 * C::STAGE];
-  __shared__ double red[4];
+// Stage n slots of one operand of one segment.
+//   kc == 0: X(idx, kk) = base[idx + kk*ld] -> smem [slot][idx] (LDI)
+//   kc == 1: X(idx, kk) = base[kk + idx*ld] -> smem [idx][slot] (LDK)
+// base points at tile index 0, k offset of the segment.  idx valid in [lo, hi).
+template <class C>
+__device__ __forceinline__ void stage_seg(unsigned sbase, const double* base,
+                                          const double* safe, int ld, int kc,
+                                          int lo, int hi, int slot0, int n) {
+  constexpr int TM = C::TM;
+  const int tid = threadIdx.x;
+  if (kc == 0) {
+    const bool al = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((ld & 1) == 0) &&
+                    (((lo | hi) & 1) == 0);
+    if (al) {
+      // thread -> row pair p, slot lane c; TM/2 pairs per slot column
+      constexpr int PR = TM / 2, CL = C::THREADS / PR;
+      const int p = tid % PR, c = tid / PR;
+      const int i = 2 * p;
+      const int v = (i >= lo && i < hi) ? 16 : 0;
+      const double* src = base + i + int64_t(c) * ld;
+      unsigned dst = sbase + 8u * unsigned((slot0 + c) * C::LDI + i);
+      const int64_t step = int64_t(CL) * ld;
+      for (int s = c; s < n; s += CL) {
+        cp_async16(dst, v ? src : safe, v);
+        src += step;
+        dst += 8u * CL * C::LDI;
+      }
+    } else {
+      const int i = tid % TM, c = tid / TM;
+      constexpr int CL = C::THREADS / TM;
+      const int v = (i >= lo && i < hi) ? 8 : 0;
+      const double* src = base + i + int64_t(c) * ld;
+      unsigned dst = sbase + 8u * unsigned((slot0 + c) * C::LDI + i);
+      for (int s = c; s < n; s += CL) {
+        cp_async8(dst, v ? src : safe, v);
+        src += int64_t(CL) * ld;
+        dst += 8u * CL * C::LDI;
+      }
+    }
+  } else {
+    const bool al = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((ld & 1) == 0) &&
+                    ((slot0 & 1) == 0);
+    if (al) {
+      // thread -> slot pair q, row lane r: pairs along k
+      constexpr int PK = C::KC / 2, RL = C::THREADS / PK;
+      const int q = tid % PK, r = tid / PK;
+      const int kk = 2 * q;
+      if (kk < n) {
+        // an odd segment end is copied alone: a zero-filled pair half would clobber the
+        // first slot of the next segment
+        const bool pair = kk + 1 < n;
+        const double* src = base + kk + int64_t(r) * ld;
+        unsigned dst = sbase + 8u * unsigned(r * C::LDK + slot0 + kk);
+        for (int i = r; i < TM; i += RL) {
+          const bool v = i >= lo && i < hi;
+          if (pair) cp_async16(dst, v ? src : safe, v ? 16 : 0);
+          else cp_async8(dst, v ? src : safe, v ? 8 : 0);
+          src += int64_t(RL) * ld;
+          dst += 8u * RL * C::LDK;
+        }
+      }
+    } else {
+      constexpr int RL = C::THREADS / C::KC;
+      const int kk = tid % C::KC, r = tid / C::KC;
+      if (kk < n) {
+        const double* src = base + kk + int64_t(r) * ld;
+        unsigned dst = sbase + 8u * unsigned(r * C::LDK + slot0 + kk);
+        for (int i = r; i < TM; i += RL) {
+          const bool v = i >= lo && i < hi;
+          cp_async8(dst, v ? src : safe, v ? 8 : 0);
+          src += int64_t(RL) * ld;
+          dst += 8u * RL * C::LDK;
+        }
+      }
+    }
+  }
+}
+
+// Zero slots [a, b) of an operand in either layout (pad up to a multiple of 4).
+template <class C>
+__device__ __forceinline__ void zero_slots(double* s, int kc, int a, int b) {
+  const int n = b - a;
+  if (n <= 0) return;
+  for (int e = threadIdx.x; e < n * C::TM; e += C::THREADS) {
+    const int kk = a + e / C::TM, i = e % C::TM;
+    s[kc ? i * C::LDK + kk : kk * C::LDI + i] = 0.0;
+  }
+}
+
+// Fill one chunk from the cursor.  Returns the chunk descriptor (used = 0: nothing left).
+template <class C>
+__device__ __forceinline__ Chunk build_chunk(double* sP, double* sQ, Cursor& cur, bool& have,
+                                             const Group* __restrict__ groups,
+                                             const Term* __restrict__ terms,
+                                             const BufPtrs& bufs, const Tile& tl, int wm, int wn) {
+  Chunk ch;
+  ch.used = 0;
+  ch.amask = ch.bmask = 0;
+  ch.akc = cur.tm.a_kc;
+  ch.bkc = cur.tm.b_kc;
+  const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(sP));
+  const unsigned sq = static_cast<unsigned>(__cvta_generic_to_shared(sQ));
+  int nseg = 0;
+  while (have && ch.used < C::KC && nseg < C::MAXSEG) {
+    const Term& tm = cur.tm;
+    if (tm.a_kc != ch.akc || tm.b_kc != ch.bkc) break;  // one staging layout per chunk
+    const int n = min(C::KC - ch.used, tm.k - cur.k0);
+    const int i0 = tl.row0 - tm.r_lo, j0 = tl.col0 - tm.c_lo;
+    const int rlo = max(0, -i0), rhi = min(int(tl.rows), tm.rows - i0);
+    const int clo = max(0, -j0), chi = min(int(tl.cols), tm.cols - j0);
+    const double* A = bufs.p[tm.a_buf] + tm.a_off;
+    const double* B = bufs.p[tm.b_buf] + tm.b_off;
+    const double* pa =
+        tm.a_kc ? A + cur.k0 + int64_t(i0) * tm.a_ld : A + i0 + int64_t(cur.k0) * tm.a_ld;
+    const double* pb =
+        tm.b_kc ? B + cur.k0 + int64_t(j0) * tm.b_ld : B + j0 + int64_t(cur.k0) * tm.b_ld;
+    // masked copies read nothing, but get an in-bounds address (the term's first element)
+    stage_seg<C>(sp, pa, A, tm.a_ld, tm.a_kc, rlo, rhi, ch.used, n);
+    stage_seg<C>(sq, pb, B, tm.b_ld, tm.b_kc, clo, chi, ch.used, n);
+#pragma unroll
+    for (int a = 0; a < C::FR; ++a) {
+      const int f0 = wm * C::WT + a * 8;
+      if (f0 < rhi && f0 + 8 > rlo) ch.amask |= 1u << a;
+      const int g0 = wn * C::WT + a * 8;
+      if (g0 < chi && g0 + 8 > clo) ch.bmask |= 1u << a;
+    }
+    ch.used += n;
+    ++nseg;
+    cur.k0 += n;
+    if (cur.k0 >= tm.k) have = next_term(cur, groups, terms);
+  }
+  const int padded = (ch.used + 3) & ~3;
+  zero_slots<C>(sP, ch.akc, ch.used, padded);
+  zero_slots<C>(sQ, ch.bkc, ch.used, padded);
+  return ch;
+}
+
+// DMMA over one staged chunk; AK/BK: compile-time staging layouts.
+template <class C, int AK, int BK>
+__device__ __forceinline__ void mma_chunk_t(double (&acc)[C::FR][C::FR][2], const double* sP,
+                                            const double* sQ, const Chunk& ch, int wm, int wn,
+                                            int lane) {
+  constexpr int SA_I = AK ? C::LDK : 1, SA_K = AK ? 1 : C::LDI;
+  constexpr int SB_I = BK ? C::LDK : 1, SB_K = BK ? 1 : C::LDI;
+  const int ksteps = (ch.used + 3) >> 2;
+  const int r = lane >> 2, q = lane & 3;
+  const double* pa = sP + (wm * C::WT + r) * SA_I + q * SA_K;
+  const double* pb = sQ + (wn * C::WT + r) * SB_I + q * SB_K;
+  const bool full = ch.amask == (1u << C::FR) - 1 && ch.bmask == (1u << C::FR) - 1;
+  if (full) {
+    for (int ks = 0; ks < ksteps; ++ks) {
+      double af[C::FR], bf[C::FR];
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a) af[a] = pa[a * 8 * SA_I + ks * 4 * SA_K];
+#pragma unroll
+      for (int b = 0; b < C::FR; ++b) bf[b] = pb[b * 8 * SB_I + ks * 4 * SB_K];
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a)
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  } else {
+    for (int ks = 0; ks < ksteps; ++ks) {
+      double af[C::FR], bf[C::FR];
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a) af[a] = pa[a * 8 * SA_I + ks * 4 * SA_K];
+#pragma unroll
+      for (int b = 0; b < C::FR; ++b) bf[b] = pb[b * 8 * SB_I + ks * 4 * SB_K];
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a)
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b)
+          if ((ch.amask >> a) & (ch.bmask >> b) & 1u)
+            dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+    }
+  }
+}
+
+template <class C>
+__device__ __forceinline__ void mma_chunk(double (&acc)[C::FR][C::FR][2], const double* sP,
+                                          const double* sQ, const Chunk& ch, int wm, int wn,
+                                          int lane) {
+  if (!(ch.amask && ch.bmask)) return;
+  switch (ch.akc * 2 + ch.bkc) {
+    case 0: mma_chunk_t<C, 0, 0>(acc, sP, sQ, ch, wm, wn, lane); break;
+    case 1: mma_chunk_t<C, 0, 1>(acc, sP, sQ, ch, wm, wn, lane); break;
+    case 2: mma_chunk_t<C, 1, 0>(acc, sP, sQ, ch, wm, wn, lane); break;
+    default: mma_chunk_t<C, 1, 1>(acc, sP, sQ, ch, wm, wn, lane); break;
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS) grouped_gemm_kernel(
+    const Tile* __restrict__ tiles, const Group* __restrict__ groups,
+    const Term* __restrict__ terms, const __grid_constant__ BufPtrs bufs,
+    double* __restrict__ sumsq, int n_tiles) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red[C::THREADS / 32];
   const int tile_idx = blockIdx.x;
   if (tile_idx >= n_tiles) return;
   const Tile tl = tiles[tile_idx];
@@ -155,76 +308,26 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restric
 #pragma unroll
     for (int b = 0; b < C::FR; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  // two cursors: `ld` runs one chunk ahead of `cm` (the chunk being multiplied)
-  ChunkCursor ld{tl.g_begin - 1, tl.g_end, 0, 0, 0};
-  Term tld;
-  tld.k = 0;
-  bool have = next_chunk(ld, groups, terms, C::KC, tld);
+  Cursor cur;
+  cur.g = tl.g_begin - 1;
+  cur.g_end = tl.g_end;
+  cur.t = cur.t_end = 0;
+  cur.k0 = 0;
+  bool have = next_term(cur, groups, terms);
   int stage = 0;
-  if (have) {
-    load_chunk<TM>(smem, smem + C::KC * C::LDS, bufs, tld, ld.k0, tl.row0, tl.col0, tl.rows,
-                   tl.cols);
-  }
+  Chunk now = build_chunk<C>(smem, smem + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn);
   cp_async_commit();
-  while (have) {
-    const int kcur = min(C::KC, tld.k - ld.k0);
-    // 8x8 fragments of this warp that the current term touches (terms created on a
-    // sub-block, or stacked cores, cover only part of the tile): skip the others
-    unsigned amask = 0, bmask = 0;
-    {
-      const int ra = tld.r_lo - tl.row0, rb = ra + tld.rows;
-      const int ca = tld.c_lo - tl.col0, cb = ca + tld.cols;
-#pragma unroll
-      for (int a = 0; a < C::FR; ++a) {
-        const int f0 = wm * C::WT + a * 8;
-        if (f0 < rb && f0 + 8 > ra) amask |= 1u << a;
-        const int g0 = wn * C::WT + a * 8;
-        if (g0 < cb && g0 + 8 > ca) bmask |= 1u << a;
-      }
-    }
-    // prefetch the following chunk into the other stage
-    ld.k0 += C::KC;
-    bool more = next_chunk(ld, groups, terms, C::KC, tld);
-    if (more) {
-      double* s = smem + (stage ^ 1) * C::STAGE;
-      load_chunk<TM>(s, s + C::KC * C::LDS, bufs, tld, ld.k0, tl.row0, tl.col0, tl.rows,
-                     tl.cols);
-    }
+  while (now.used > 0) {
+    double* ns = smem + (stage ^ 1) * C::STAGE;
+    Chunk nxt = build_chunk<C>(ns, ns + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();
     const double* sP = smem + stage * C::STAGE;
-    const double* sQ = sP + C::KC * C::LDS;
-    const int ksteps = (kcur + 3) >> 2;
-    if (amask && bmask) {
-      const bool full = amask == (1u << C::FR) - 1 && bmask == (1u << C::FR) - 1;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const int kk = ks * 4 + (lane & 3);
-        double af[C::FR], bf[C::FR];
-#pragma unroll
-        for (int a = 0; a < C::FR; ++a)
-          af[a] = sP[kk * C::LDS + wm * C::WT + a * 8 + (lane >> 2)];
-#pragma unroll
-        for (int b = 0; b < C::FR; ++b)
-          bf[b] = sQ[kk * C::LDS + wn * C::WT + b * 8 + (lane >> 2)];
-        if (full) {
-#pragma unroll
-          for (int a = 0; a < C::FR; ++a)
-#pragma unroll
-            for (int b = 0; b < C::FR; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-        } else {
-#pragma unroll
-          for (int a = 0; a < C::FR; ++a)
-#pragma unroll
-            for (int b = 0; b < C::FR; ++b)
-              if ((amask >> a) & (bmask >> b) & 1u)
-                dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
-        }
-      }
-    }
+    mma_chunk<C>(acc, sP, sP + C::OPSZ, now, wm, wn, lane);
     __syncthreads();
     stage ^= 1;
-    have = more;
+    now = nxt;
   }
   cp_async_wait<0>();
 
@@ -254,7 +357,11 @@ __global__ void __launch_bounds__(128) grouped_gemm_kernel(const Tile* __restric
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) red[warp] = ss;
     __syncthreads();
-    if (threadIdx.x == 0) sumsq[tl.aux] = (red[0] + red[1]) + (red[2] + red[3]);
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < C::THREADS / 32; ++w) t += red[w];
+      sumsq[tl.aux] = t;
+    }
   }
 }
 

@@ -163,10 +163,20 @@ namespace {
 void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, const Term* terms,
                  int n_tiles, const BufPtrs& bp, double* sumsq) {
   if (n_tiles <= 0) return;
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(grouped_gemm_kernel<Gemm64>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm64::SMEM));
+    CK(cudaFuncSetAttribute(grouped_gemm_kernel<Gemm32>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm32::SMEM));
+    attr = true;
+  }
   if (tile == 32)
-    grouped_gemm_kernel<32><<<n_tiles, 128, 0, c->s>>>(tiles, groups, terms, bp, sumsq, n_tiles);
+    grouped_gemm_kernel<Gemm32><<<n_tiles, Gemm32::THREADS, Gemm32::SMEM, c->s>>>(
+        tiles, groups, terms, bp, sumsq, n_tiles);
   else
-    grouped_gemm_kernel<64><<<n_tiles, 128, 0, c->s>>>(tiles, groups, terms, bp, sumsq, n_tiles);
+    grouped_gemm_kernel<Gemm64><<<n_tiles, Gemm64::THREADS, Gemm64::SMEM, c->s>>>(
+        tiles, groups, terms, bp, sumsq, n_tiles);
   CK(cudaGetLastError());
   c->launches++;
 }
@@ -654,6 +664,50 @@ extern "C" int hx_result_download(hx_ctx* c, double* host, int64_t n) {
       CK(cudaMemcpyAsync(host + c->out_far, c->own[BUF_TILE].p + c->near_begin,
                          size_t(c->near_elems) * sizeof(double), cudaMemcpyDeviceToHost, c->s));
     CK(cudaStreamSynchronize(c->s));
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tiles,
+                             int64_t n_tiles, const void* groups, int64_t n_groups,
+                             double* const* host_bufs, const int64_t* buf_elems, double* sumsq,
+                             int64_t n_sumsq) {
+  return guarded([&]() -> int {
+    if ((tile != 32 && tile != 64) || !terms || !tiles || !groups || !host_bufs || !buf_elems)
+      return fail(HX_EINVAL, "bad arguments");
+    cudaStream_t s = nullptr;
+    hx_ctx tmp;
+    tmp.s = s;
+    DArr<Term> dt;
+    DArr<Tile> dl;
+    DArr<Group> dg;
+    DArr<double> ds;
+    dt.upload(static_cast<const Term*>(terms), size_t(n_terms), s);
+    dl.upload(static_cast<const Tile*>(tiles), size_t(n_tiles), s);
+    dg.upload(static_cast<const Group*>(groups), size_t(n_groups), s);
+    ds.ensure(size_t(std::max<int64_t>(n_sumsq, 1)));
+    std::vector<DArr<double>> db(NUM_BUFS);
+    BufPtrs bp;
+    for (int i = 0; i < NUM_BUFS; ++i) {
+      bp.p[i] = nullptr;
+      if (host_bufs[i] && buf_elems[i] > 0) {
+        db[i].upload(host_bufs[i], size_t(buf_elems[i]), s);
+        bp.p[i] = db[i].p;
+      }
+    }
+    launch_gemm(&tmp, tile, dl.p, dg.p, dt.p, int(n_tiles), bp, ds.p);
+    CK(cudaDeviceSynchronize());
+    for (int i = 0; i < NUM_BUFS; ++i)
+      if (bp.p[i])
+        CK(cudaMemcpy(host_bufs[i], db[i].p, size_t(buf_elems[i]) * 8, cudaMemcpyDeviceToHost));
+    if (sumsq && n_sumsq > 0)
+      CK(cudaMemcpy(sumsq, ds.p, size_t(n_sumsq) * 8, cudaMemcpyDeviceToHost));
+    for (auto& d : db) d.release();
+    dt.release();
+    dl.release();
+    dg.release();
+    ds.release();
+    tmp.s = nullptr;
     return HX_OK;
   });
 }
