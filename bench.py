@@ -302,6 +302,12 @@ def bench_ours(args, rank, world, local):
         mask[lv["ids"][owner == rank]] = 1
         full.close()
     setup_s = time.time() - t_setup
+    # tensor-core work of this rank's plan (outside the timed region)
+    mma = np.zeros(6)
+    wp = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, mask,
+                   multiply.plan_tile(bct))
+    _lib.check(_lib.lib().hx_plan_mma_flops(wp.h, _lib.ptr(mma, _lib.f64p)), "mma flops")
+    wp.close()
 
     stream = torch.cuda.current_stream()
 
@@ -388,18 +394,37 @@ def bench_ours(args, rank, world, local):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": float(tt.item()) * 1e3}
 
-    # roofline of the dominant kernel: term formation (HBM-bound in the canonical model)
+    # roofline of the dominant kernel: the materialization launch of grouped_gemm_kernel
+    # (one launch per step, FP64 DMMA-bound); algorithmic flops = exact useful products
+    # sum over tiles and terms of 2 * rows * cols * k (no padding), from the plan
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6552.3))
     info = C.plan_info
+    mat_s = mat_ms / args.steps * 1e-3
+    mat_tflops = mma[5] / mat_s / 1e12 if mat_s > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "mat_kernel_traffic.json")) as f:
+            tj = json.load(f)
+        if tj.get("config") == args.config:
+            traffic = tj["dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        pass
     form_s = form_ms / args.steps * 1e-3
-    achieved = info.bytes_form / form_s / 1e9 if form_s > 0 else 0.0
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": achieved / hbm, "traffic": None,
-                "kernel": "grouped_gemm_kernel (term formation: cores + pushed-through factors)",
-                "note": "achieved = canonical term-formation bytes (SURVEY 8(d)) / measured "
-                        "phase time; FP64 DMMA peak measured 37.1 TFLOP/s "
-                        "(profiles/r01_fp64_peak.txt)",
+    form_gbs = info.bytes_form / form_s / 1e9 if form_s > 0 else 0.0
+    roofline = {"bound": "tensor", "achieved": mat_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": mat_tflops / FP64_DMMA_PEAK_TFLOPS,
+                "traffic": traffic,
+                "kernel": "grouped_gemm_kernel<Gemm64> materialization launch",
+                "algorithmic_flops_per_launch": mma[5],
+                "issued_flops_per_launch": mma[2],
+                "peak_source": "FP64 DMMA measured on this pool's B200 (tools/fp64_peak.cu, "
+                               "profiles/r01_fp64_peak.txt); MEASURED_PEAKS.json has no FP64 "
+                               "entry",
+                "formation_phase": {"bound": "hbm", "achieved_gbs": form_gbs, "peak_gbs": hbm,
+                                    "frac": form_gbs / hbm,
+                                    "note": "canonical term-formation bytes (SURVEY 8(d)) / "
+                                            "formation phase time"},
                 "fp64_tflops_whole_product": value / 1e3,
                 "fp64_frac_whole_product": value / 1e3 / FP64_DMMA_PEAK_TFLOPS}
     # roofline time of the whole product (phase-wise max(F/P, B/BW))

@@ -101,8 +101,8 @@ int hx_plan_leaves(const hx_plan* plan, int32_t* ids, int8_t* kind, int32_t* m,
 int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kind, int32_t* a_node,
                      int32_t* b_node, int32_t* rank);
 void hx_plan_free(hx_plan* plan);
-/* Tensor-core work the plan issues (FP64 flops incl. tile padding) for the core, factor
- * and materialization batches: flops[0..2]. */
+/* Tensor-core work of the core, factor and materialization batches: flops[0..2] as issued
+ * (full tiles, k padded to 4), flops[3..5] useful (term extents, exact k). */
 int hx_plan_mma_flops(const hx_plan* plan, double* flops);
 
 /* ---- device context ----------------------------------------------------------------- */

@@ -967,14 +967,22 @@ extern "C" int hx_plan_mma_flops(const hx_plan* plan, double* flops) {
   const hx::pvec<Term>* terms[3] = {&plan->core_terms, &plan->fac_terms, &plan->mat_terms};
   const double tt = double(plan->tile) * plan->tile;
   for (int b = 0; b < 3; ++b) {
-    double f = 0;
+    double f = 0, u = 0;
     for (const Tile& tl : *tiles[b])
       for (int32_t g = tl.g_begin; g < tl.g_end; ++g) {
         const Group gr = (*groups[b])[g];
-        for (int32_t i = gr.t_begin; i < gr.t_end; ++i)
-          f += 2.0 * tt * double(((*terms[b])[i].k + 3) & ~3);
+        for (int32_t i = gr.t_begin; i < gr.t_end; ++i) {
+          const Term& tm = (*terms[b])[i];
+          f += 2.0 * tt * double((tm.k + 3) & ~3);
+          const int r0 = std::max(tl.row0, tm.r_lo), r1 = std::min(tl.row0 + tl.rows,
+                                                                   tm.r_lo + tm.rows);
+          const int c0 = std::max(tl.col0, tm.c_lo), c1 = std::min(tl.col0 + tl.cols,
+                                                                   tm.c_lo + tm.cols);
+          if (r1 > r0 && c1 > c0) u += 2.0 * double(r1 - r0) * double(c1 - c0) * tm.k;
+        }
       }
     flops[b] = f;
+    flops[3 + b] = u;
   }
   return HX_OK;
 }
