@@ -86,9 +86,13 @@ typedef struct hx_plan_info {
 /* ---- planning (CPU only; no GPU needed) ---------------------------------------------
  * leaf_mask (nullable, [n_nodes]): nonzero for output leaves this process owns; terms
  * are only built for blocks on the root path of an owned leaf (multi-GPU partition).
- * tile: CTA tile side (32 or 64). */
+ * tile: CTA tile side (32 or 64).
+ * flags: HX_PLAN_DEFER leaves the per-batch core / X G work lists to hx_product, which
+ * fills them batch by batch while the device runs the previous batches; the caller's
+ * tree / operand arrays must then stay alive until hx_product returns. */
+#define HX_PLAN_DEFER 1
 int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
-                   const uint8_t* leaf_mask, int tile, hx_plan** out);
+                   const uint8_t* leaf_mask, int tile, int flags, hx_plan** out);
 int hx_plan_info_get(const hx_plan* plan, hx_plan_info* info);
 /* Per output leaf (plan order): block id, kind (1 far / 2 near), m, n, stacked rank K,
  * dense-pair flops F_DD and elements E_DD (canonical model inputs). Any pointer may be
@@ -103,7 +107,7 @@ int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kind, int32_t*
 void hx_plan_free(hx_plan* plan);
 /* Tensor-core work of the core, factor and materialization batches: flops[0..2] as issued
  * (full tiles, k padded to 4), flops[3..5] useful (term extents, exact k). */
-int hx_plan_mma_flops(const hx_plan* plan, double* flops);
+int hx_plan_mma_flops(hx_plan* plan, double* flops);
 
 /* ---- device context ----------------------------------------------------------------- */
 int hx_ctx_create(int device, hx_ctx** out);
@@ -137,7 +141,7 @@ typedef struct hx_product_stats {
   double ms_upload;      /* H2D of the plan's work lists (inside ms_total)          */
 } hx_product_stats;
 
-int hx_product(hx_ctx* ctx, const hx_plan* plan, const hx_product_cfg* cfg,
+int hx_product(hx_ctx* ctx, hx_plan* plan, const hx_product_cfg* cfg,
                hx_product_stats* stats);
 /* Per output leaf (plan order): rank (-1 near), degraded flag, element offset of the
  * leaf's payload in the packed result (left m x r then right n x r, or dense m x n,

@@ -67,7 +67,7 @@ _lib = None
 
 SIGNATURES = {
     "hx_plan_create": [C.POINTER(HxTree), C.POINTER(HxOperand), C.POINTER(HxOperand), u8p,
-                       C.c_int, C.POINTER(C.c_void_p)],
+                       C.c_int, C.c_int, C.POINTER(C.c_void_p)],
     "hx_plan_info_get": [C.c_void_p, C.POINTER(HxPlanInfo)],
     "hx_plan_leaves": [C.c_void_p, i32p, i8p, i32p, i32p, i64p, f64p, f64p],
     "hx_plan_term_log": [C.c_void_p, i32p, i8p, i32p, i32p, i32p],
@@ -154,14 +154,16 @@ class OperandBuf:
 class Plan:
     """Owning wrapper of an ``hx_plan``."""
 
-    def __init__(self, tree_arrays, opa, opb, leaf_mask=None, tile=64):
+    DEFER = 1  # HX_PLAN_DEFER: factor work lists filled by hx_product, batch by batch
+
+    def __init__(self, tree_arrays, opa, opb, leaf_mask=None, tile=64, flags=0):
         self.tree = TreeBuf(tree_arrays)
         self.opa = OperandBuf(opa)
         self.opb = self.opa if opb is opa else OperandBuf(opb)
         self.mask = None if leaf_mask is None else np.ascontiguousarray(leaf_mask, np.uint8)
         h = C.c_void_p()
         check(lib().hx_plan_create(C.byref(self.tree.st), C.byref(self.opa.st),
-                                   C.byref(self.opb.st), ptr(self.mask, u8p), tile,
+                                   C.byref(self.opb.st), ptr(self.mask, u8p), tile, flags,
                                    C.byref(h)), "hx_plan_create")
         self.h = h
         self.info = HxPlanInfo()

@@ -1,0 +1,198 @@
+// Warp-level dense linear algebra for the many small far blocks (sketch width <= 32).
+//
+// The CTA kernels of dense_la.cuh spend most of their time in __syncthreads between the
+// q column steps of a QR and the q-1 rounds of every Jacobi sweep.  For small blocks one
+// warp owns one block and synchronises only with __syncwarp:
+//   warp_qr_kernel      Householder QR (dgeqr2 + dorg2r semantics, same as the CTA
+//                       kernel) of a p x q panel staged in shared memory (p <= 256, q <= 32)
+//   warp_jacobi_kernel  one-sided Jacobi SVD of a q x q factor, one column per lane held in
+//                       registers, partner columns exchanged with shuffles (q <= QM)
+#pragma once
+#include <cstdint>
+
+#include "dense_la.cuh"
+
+namespace hx {
+
+// Apply H = I - tau v v^T (v = (1, M[j+1:p, j])) to columns j+1..q-1 of M (ld), one
+// column per lane.
+__device__ __forceinline__ void warp_apply_reflector(double* M, int ld, int p, int q, int j,
+                                                     double tau, int lane) {
+  const double* v = M + j * ld;
+  for (int c = j + 1 + lane; c < q; c += 32) {
+    double* col = M + c * ld;
+    double w = col[j];
+    for (int i = j + 1; i < p; ++i) w += v[i] * col[i];
+    w *= tau;
+    col[j] -= w;
+    for (int i = j + 1; i < p; ++i) col[i] -= w * v[i];
+  }
+}
+
+// In-place Householder QR of M (p x q, column-major, ld) by one warp: R (q x q, ld q) is
+// written to Rout, M is overwritten by the explicit Q.
+__device__ void warp_householder_qr(double* M, int ld, int p, int q, double* Rout,
+                                    double* tau_s, int lane) {
+  for (int j = 0; j < q; ++j) {
+    double* x = M + j * ld;
+    double part = 0.0;
+    for (int i = j + 1 + lane; i < p; i += 32) part += x[i] * x[i];
+    const double xn2 = warp_sum(part);
+    const double alpha = x[j];
+    double tau, beta;
+    if (xn2 == 0.0) {
+      tau = 0.0;
+      beta = alpha;
+    } else {
+      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
+      tau = (beta - alpha) / beta;
+      const double scal = 1.0 / (alpha - beta);
+      for (int i = j + 1 + lane; i < p; i += 32) x[i] *= scal;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      x[j] = beta;
+      tau_s[j] = tau;
+    }
+    __syncwarp();
+    if (tau != 0.0) warp_apply_reflector(M, ld, p, q, j, tau, lane);
+    __syncwarp();
+  }
+  for (int e = lane; e < q * q; e += 32) {
+    const int i = e % q, c = e / q;
+    Rout[e] = (i <= c) ? M[i + c * ld] : 0.0;
+  }
+  __syncwarp();
+  for (int j = q - 1; j >= 0; --j) {
+    const double tau = tau_s[j];
+    if (j < q - 1) {
+      if (lane == 0) M[j + j * ld] = 1.0;
+      __syncwarp();
+      if (tau != 0.0) warp_apply_reflector(M, ld, p, q, j, tau, lane);
+      __syncwarp();
+    }
+    double* x = M + j * ld;
+    for (int i = j + 1 + lane; i < p; i += 32) x[i] *= -tau;
+    for (int i = lane; i < j; i += 32) x[i] = 0.0;
+    if (lane == 0) x[j] = 1.0 - tau;
+    __syncwarp();
+  }
+}
+
+// One warp per job; each warp stages its panel in its own slice of dynamic shared memory
+// (ld = p + 1: lanes walking different columns hit different banks).
+__global__ void warp_qr_kernel(const QrJob* __restrict__ jobs, int n_jobs, int slice) {
+  extern __shared__ __align__(16) double dsm[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jid = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (jid >= n_jobs) return;
+  const QrJob jb = jobs[jid];
+  const int p = jb.p, q = jb.q, ld = p + 1;
+  double* M = dsm + warp * slice;
+  double* tau_s = M + ld * q;
+  for (int c = 0; c < q; ++c)
+    for (int i = lane; i < p; i += 32) M[i + c * ld] = jb.X[i + int64_t(c) * p];
+  __syncwarp();
+  warp_householder_qr(M, ld, p, q, jb.R, tau_s, lane);
+  for (int c = 0; c < q; ++c)
+    for (int i = lane; i < p; i += 32) jb.X[i + int64_t(c) * p] = M[i + c * ld];
+}
+
+// One-sided Jacobi SVD of R (q x q, column-major) with lane c holding column c of R and of
+// V in registers.  Pairs follow the same round-robin (circle) ordering as the CTA kernel.
+template <int QM>
+__global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restrict__ jobs,
+                                                          int n_jobs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jid = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (jid >= n_jobs) return;
+  const JacJob jb = jobs[jid];
+  const int q = jb.q;
+  double col[QM], vc[QM];
+#pragma unroll
+  for (int x = 0; x < QM; ++x) {
+    col[x] = (lane < q && x < q) ? jb.R[x + lane * q] : 0.0;
+    vc[x] = (x == lane && lane < q) ? 1.0 : 0.0;
+  }
+  const int qe = (q + 1) & ~1;
+  const double tol = 1e-15;
+  for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+    int rotated = 0;
+    for (int r = 0; r < qe - 1; ++r) {
+      // partner of this lane in round r (circle method; position 0 is fixed)
+      int partner = -1;
+      if (lane < qe) {
+        // lane's position on the circle
+        int pos;
+        if (lane == 0) {
+          pos = 0;
+        } else {
+          pos = ((lane - 1 - r) % (qe - 1) + (qe - 1)) % (qe - 1) + 1;
+        }
+        int ppos;
+        if (pos == 0) ppos = 1;
+        else if (pos == 1) ppos = 0;
+        else ppos = qe + 1 - pos;
+        partner = (ppos == 0) ? 0 : ((ppos - 1 + r) % (qe - 1)) + 1;
+      }
+      const int src = (partner >= 0 && partner < 32) ? partner : lane;
+      double pc[QM];
+#pragma unroll
+      for (int x = 0; x < QM; ++x) pc[x] = __shfl_sync(0xffffffffu, col[x], src);
+      const bool low = lane < partner;
+      bool doit = false;
+      double c = 1.0, s = 0.0;
+      if (lane < q && partner >= 0 && partner < q) {
+        double a = 0.0, b = 0.0, g = 0.0;
+#pragma unroll
+        for (int x = 0; x < QM; ++x) {
+          const double u = low ? col[x] : pc[x];
+          const double w = low ? pc[x] : col[x];
+          a += u * u;
+          b += w * w;
+          g += u * w;
+        }
+        if (fabs(g) > tol * sqrt(a * b) && g != 0.0) {
+          const double zeta = (b - a) / (2.0 * g);
+          const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          c = 1.0 / sqrt(1.0 + t * t);
+          s = c * t;
+          doit = true;
+          rotated = 1;
+        }
+      }
+      // low column i: c*mi - s*mj ; high column j: s*mi + c*mj  (same for V)
+#pragma unroll
+      for (int x = 0; x < QM; ++x) {
+        const double pvx = __shfl_sync(0xffffffffu, vc[x], src);
+        if (doit) {
+          col[x] = low ? c * col[x] - s * pc[x] : s * pc[x] + c * col[x];
+          vc[x] = low ? c * vc[x] - s * pvx : s * pvx + c * vc[x];
+        }
+      }
+    }
+    if (!__any_sync(0xffffffffu, rotated)) break;
+  }
+  // singular values = column norms; descending order (stable) via ranking by all lanes
+  double nrm = 0.0;
+#pragma unroll
+  for (int x = 0; x < QM; ++x) nrm += col[x] * col[x];
+  nrm = (lane < q) ? sqrt(nrm) : -1.0;
+  int pos = 0;
+  for (int d = 0; d < q; ++d) {
+    const double od = __shfl_sync(0xffffffffu, nrm, d);
+    if (od > nrm || (od == nrm && d < lane)) ++pos;
+  }
+  if (lane < q) {
+    jb.sig[pos] = nrm;
+    const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+#pragma unroll
+    for (int x = 0; x < QM; ++x)
+      if (x < q) {
+        jb.W[x + pos * q] = nrm > 0.0 ? col[x] * inv : 0.0;
+        jb.V[x + pos * q] = vc[x];
+      }
+  }
+}
+
+}  // namespace hx

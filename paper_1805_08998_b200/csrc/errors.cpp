@@ -1,5 +1,7 @@
 // Thread-local last-error string behind hx_last_error().
+#include <cstdlib>
 #include <cstring>
+#include <new>
 #include <string>
 
 #include "hx_internal.h"
@@ -25,3 +27,14 @@ extern "C" int hx_last_error(char* buf, size_t len) {
 }
 
 extern "C" int hx_version(void) { return 1; }
+
+// Planner-only builds (no CUDA runtime linked): plain heap memory.  libhx.so overrides these
+// with the page-locked cache of runtime.cu.
+namespace hx {
+__attribute__((weak)) void* pinned_alloc(size_t bytes) {
+  void* p = std::malloc(bytes ? bytes : 1);
+  if (!p) throw std::bad_alloc();
+  return p;
+}
+__attribute__((weak)) void pinned_free(void* p, size_t) { std::free(p); }
+}  // namespace hx

@@ -2,6 +2,8 @@
 #pragma once
 #include <cstdint>
 #include <cstdio>
+#include <functional>
+#include <memory>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -33,6 +35,40 @@ struct DefaultInitAlloc : std::allocator<T> {
 template <class T>
 using pvec = std::vector<T, DefaultInitAlloc<T>>;
 
+// Page-locked host memory with a reuse cache (runtime.cu; errors.cpp carries a plain
+// malloc fallback for planner-only builds).  The plan's device work lists live here so
+// their uploads are true async DMA that overlaps planning of the next batch.
+void* pinned_alloc(size_t bytes);
+void pinned_free(void* p, size_t bytes);
+
+template <class T>
+struct PinnedAlloc {
+  using value_type = T;
+  PinnedAlloc() = default;
+  template <class U>
+  PinnedAlloc(const PinnedAlloc<U>&) {}
+  T* allocate(size_t n) { return static_cast<T*>(pinned_alloc(n * sizeof(T))); }
+  void deallocate(T* p, size_t n) { pinned_free(p, n * sizeof(T)); }
+  template <class U>
+  void construct(U* p) noexcept {
+    ::new (static_cast<void*>(p)) U;
+  }
+  template <class U, class... Args>
+  void construct(U* p, Args&&... args) {
+    ::new (static_cast<void*>(p)) U(std::forward<Args>(args)...);
+  }
+  template <class U>
+  bool operator==(const PinnedAlloc<U>&) const {
+    return true;
+  }
+  template <class U>
+  bool operator!=(const PinnedAlloc<U>&) const {
+    return false;
+  }
+};
+template <class T>
+using hvec = std::vector<T, PinnedAlloc<T>>;
+
 struct Unsupported : std::runtime_error {
   explicit Unsupported(const std::string& s) : std::runtime_error(s) {}
 };
@@ -57,6 +93,7 @@ struct OutLeaf {
 
 void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
+void plan_fill_all(hx_plan* plan);
 
 template <class F>
 int guarded(F&& f) {
@@ -79,21 +116,31 @@ int guarded(F&& f) {
 
 struct hx_plan {
   int tile = 64;
-  hx::pvec<hx::Term> core_terms, fac_terms, mat_terms;
-  hx::pvec<hx::Tile> core_tiles, fac_tiles, mat_tiles;
-  hx::pvec<hx::Group> core_groups, fac_groups, mat_groups;
+  hx::hvec<hx::Term> core_terms, fac_terms, mat_terms;
+  hx::hvec<hx::Tile> core_tiles, fac_tiles, mat_tiles;
+  hx::hvec<hx::Group> core_groups, fac_groups, mat_groups;
   std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
   hx::pvec<hx::OutLeaf> leaves;
   int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
-  hx::pvec<hx::CopyRec> gather;
+  hx::hvec<hx::CopyRec> gather;
   // X-groups are processed in batches whose gathered factors and cores fit a bounded
   // workspace (BUF_GATHER / BUF_CORE offsets restart at 0 in every batch)
   struct Batch {
     int64_t gather_begin, gather_end;
     int64_t core_begin, core_end;   // core tiles
     int64_t fac_begin, fac_end;     // fac tiles
+    int64_t cg_begin, cg_end, cm_begin, cm_end;  // core groups / terms
+    int64_t fg_begin, fg_end, fm_begin, fm_end;  // fac groups / terms
+    int64_t g_begin, g_end;         // X-groups of the batch
   };
   std::vector<Batch> batches;
+  // deferred plans (hx_plan_create with HX_PLAN_DEFER): the per-batch core / X G work
+  // lists are filled by hx_product while the device runs earlier batches
+  std::function<void(int64_t)> fill_batch;
+  std::vector<uint8_t> batch_ready;
+  std::shared_ptr<void> builder;
+  hx_tree tree;           // copies of the caller's descriptors (arrays stay caller-owned)
+  hx_operand opa, opb;
   int64_t near_ws_begin = 0;  // near-leaf blocks sit after all far blocks in BUF_TILE
   int32_t n_sumsq = 0;
   std::vector<int32_t> log_block, log_a, log_b, log_rank;

@@ -539,6 +539,7 @@ struct Builder {
 
   int64_t ws_far_total = 0, ws_near_total = 0;
   std::vector<int64_t> task_log_pos;
+  std::vector<int32_t> order;  // terms sorted by X-group
 
   // --------------------------------------------------------------- grouped term factors
   // workspace bound (doubles) for one batch of gathered factors, and for its cores
@@ -558,6 +559,7 @@ struct Builder {
     int64_t out, gat, core;
     int64_t o_gather, o_ct, o_cg, o_cm, o_ft, o_fg, o_fm;
   };
+  std::vector<GInfo> G;
 
   static int64_t nbands(int64_t rows, int T) { return (rows + T - 1) / T; }
   static int64_t bands_hit(int64_t a, int64_t len, int64_t nb, int T) {
@@ -598,12 +600,12 @@ struct Builder {
     auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
     for (const TRec& r : recs) cnt[key(r) + 1]++;
     for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-    std::vector<int32_t> order(nr);
+    order.assign(nr, 0);
     {
       std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
       for (size_t i = 0; i < nr; ++i) order[pos[key(recs[i])]++] = int32_t(i);
     }
-    std::vector<GInfo> G;
+    G.clear();
     for (int g = 0; g < 2 * nn; ++g) {
       if (cnt[g] == cnt[g + 1]) continue;
       GInfo gi{};
@@ -656,17 +658,38 @@ struct Builder {
     // pass 2 (sequential): batches and offsets
     int64_t gat_cur = 0, core_cur = 0;
     int64_t o_gather = 0, o_ct = 0, o_cg = 0, o_cm = 0, o_ft = 0, o_fg = 0, o_fm = 0;
-    P.batches.push_back(hx_plan::Batch{0, 0, 0, 0, 0, 0});
-    for (GInfo& g : G) {
+    auto close_batch = [&](int64_t gi_end) {
+      hx_plan::Batch& b = P.batches.back();
+      b.gather_end = o_gather;
+      b.core_end = o_ct;
+      b.fac_end = o_ft;
+      b.cg_end = o_cg;
+      b.cm_end = o_cm;
+      b.fg_end = o_fg;
+      b.fm_end = o_fm;
+      b.g_end = gi_end;
+    };
+    auto open_batch = [&](int64_t gi_begin) {
+      hx_plan::Batch b{};
+      b.gather_begin = o_gather;
+      b.core_begin = o_ct;
+      b.fac_begin = o_ft;
+      b.cg_begin = o_cg;
+      b.cm_begin = o_cm;
+      b.fg_begin = o_fg;
+      b.fm_begin = o_fm;
+      b.g_begin = gi_begin;
+      P.batches.push_back(b);
+    };
+    open_batch(0);
+    for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
+      GInfo& g = G[gi_];
       const int64_t gat_need = align16(g.kr * g.ktot);
       const int64_t core_need = align16(g.srows * g.ktot);
       if ((gat_cur + gat_need > budget || core_cur + core_need > budget) &&
           (gat_cur > 0 || core_cur > 0)) {
-        hx_plan::Batch& b = P.batches.back();
-        b.gather_end = o_gather;
-        b.core_end = o_ct;
-        b.fac_end = o_ft;
-        P.batches.push_back(hx_plan::Batch{o_gather, 0, o_ct, 0, o_ft, 0});
+        close_batch(gi_);
+        open_batch(gi_);
         gat_cur = core_cur = 0;
       }
       g.out = P.term_elems;
@@ -695,12 +718,7 @@ struct Builder {
       P.info.bytes_form += double(g.b1 - g.b0) * g.bytes + 8.0 * double(g.ktot) * double(g.kr + g.R);
       P.info.n_xgroups++;
     }
-    {
-      hx_plan::Batch& b = P.batches.back();
-      b.gather_end = o_gather;
-      b.core_end = o_ct;
-      b.fac_end = o_ft;
-    }
+    close_batch(ng);
     P.gather.resize(size_t(o_gather));
     P.core_tiles.resize(size_t(o_ct));
     P.core_groups.resize(size_t(o_cg));
@@ -708,12 +726,11 @@ struct Builder {
     P.fac_tiles.resize(size_t(o_ft));
     P.fac_groups.resize(size_t(o_fg));
     P.fac_terms.resize(size_t(o_fm));
-    // pass 3 (parallel): fill
+    // pass 3 (parallel): gather records and the computed-factor offsets of the
+    // materialization terms -- everything the materialization launch needs
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
       const GInfo& g = G[gi_];
-      const hx_operand& opX = g.side == 0 ? A : B;
-      const uint8_t xbuf = g.side == 0 ? hx::BUF_A : hx::BUF_B;
       // gather the thin factors side by side, patch the materialization terms
       int64_t col = 0;
       for (int32_t i = g.b0; i < g.b1; ++i) {
@@ -734,6 +751,18 @@ struct Builder {
         }
         col += r.k;
       }
+    }
+  }
+
+  // pass 4 for one batch (parallel over its groups): stacked-core and X G work lists.
+  // Deferred plans run this batch by batch inside hx_product, overlapping the device.
+  void fill_batch(int64_t bi) {
+    const hx_plan::Batch& bt = P.batches[size_t(bi)];
+#pragma omp parallel for schedule(dynamic, 16)
+    for (int64_t gi_ = bt.g_begin; gi_ < bt.g_end; ++gi_) {
+      const GInfo& g = G[gi_];
+      const hx_operand& opX = g.side == 0 ? A : B;
+      const uint8_t xbuf = g.side == 0 ? hx::BUF_A : hx::BUF_B;
       // stacked cores S (srows x ktot, ld srows): rows [off_l, off_l + k_l) = V_l^T G[rho_l]
       // (A side) or U_l^T G[rho_l] (B side)
       const int64_t nbs = nbands(g.srows, T);
@@ -890,7 +919,7 @@ struct Builder {
 }  // namespace
 
 extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
-                              const uint8_t* leaf_mask, int tile, hx_plan** out) {
+                              const uint8_t* leaf_mask, int tile, int flags, hx_plan** out) {
   return hx::guarded([&]() -> int {
     if (!tree || !a || !b || !out) return hx::fail(HX_EINVAL, "null argument");
     if (tile != 32 && tile != 64) return hx::fail(HX_EINVAL, "tile must be 32 or 64");
@@ -898,9 +927,18 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
     auto* plan = new hx_plan();
     std::memset(&plan->info, 0, sizeof(plan->info));
     plan->tile = tile;
+    plan->tree = *tree;
+    plan->opa = *a;
+    plan->opb = *b;
     try {
-      Builder bld(*tree, *a, *b, leaf_mask, tile, *plan);
-      bld.run();
+      auto bld = std::make_shared<Builder>(plan->tree, plan->opa, plan->opb, leaf_mask, tile,
+                                           *plan);
+      bld->run();
+      Builder* raw = bld.get();
+      plan->builder = bld;
+      plan->fill_batch = [raw](int64_t i) { raw->fill_batch(i); };
+      plan->batch_ready.assign(plan->batches.size(), 0);
+      if (!(flags & HX_PLAN_DEFER)) hx::plan_fill_all(plan);
     } catch (...) {
       delete plan;
       throw;
@@ -959,12 +997,23 @@ extern "C" int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kin
 
 extern "C" void hx_plan_free(hx_plan* plan) { delete plan; }
 
-extern "C" int hx_plan_mma_flops(const hx_plan* plan, double* flops) {
+namespace hx {
+void plan_fill_all(hx_plan* plan) {
+  for (size_t i = 0; i < plan->batches.size(); ++i)
+    if (!plan->batch_ready[i]) {
+      plan->fill_batch(int64_t(i));
+      plan->batch_ready[i] = 1;
+    }
+}
+}  // namespace hx
+
+extern "C" int hx_plan_mma_flops(hx_plan* plan, double* flops) {
   if (!plan || !flops) return hx::fail(HX_EINVAL, "null argument");
-  const hx::pvec<Tile>* tiles[3] = {&plan->core_tiles, &plan->fac_tiles, &plan->mat_tiles};
-  const hx::pvec<Group>* groups[3] = {&plan->core_groups, &plan->fac_groups,
-                                         &plan->mat_groups};
-  const hx::pvec<Term>* terms[3] = {&plan->core_terms, &plan->fac_terms, &plan->mat_terms};
+  hx::plan_fill_all(plan);
+  const hx::hvec<Tile>* tiles[3] = {&plan->core_tiles, &plan->fac_tiles, &plan->mat_tiles};
+  const hx::hvec<Group>* groups[3] = {&plan->core_groups, &plan->fac_groups,
+                                      &plan->mat_groups};
+  const hx::hvec<Term>* terms[3] = {&plan->core_terms, &plan->fac_terms, &plan->mat_terms};
   const double tt = double(plan->tile) * plan->tile;
   for (int b = 0; b < 3; ++b) {
     double f = 0, u = 0;

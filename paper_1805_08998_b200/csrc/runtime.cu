@@ -14,10 +14,14 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <unordered_set>
 #include <string>
 #include <vector>
 
 #include "dense_la.cuh"
+#include "dense_la_warp.cuh"
 #include "gemm.cuh"
 #include "hx_internal.h"
 
@@ -95,6 +99,76 @@ __global__ void gather_kernel(const CopyRec* __restrict__ recs, BufPtrs bufs) {
 
 }  // namespace
 
+// ---- page-locked host memory cache (plan work lists) ----------------------------------
+namespace hx {
+namespace pin_detail {
+std::mutex g_pin_mu;
+std::multimap<size_t, void*> g_pin_free;  // capacity -> block
+size_t g_pin_cached = 0;
+std::unordered_set<void*>& g_unpinned() {
+  static std::unordered_set<void*> s;
+  return s;
+}
+constexpr size_t PIN_MIN = size_t(1) << 20;        // below: ordinary heap
+constexpr size_t PIN_CACHE_MAX = size_t(8) << 30;  // cached bytes kept for reuse
+size_t pin_cap(size_t bytes) {
+  size_t c = PIN_MIN;
+  while (c < bytes) c <<= 1;
+  return c;
+}
+}  // namespace pin_detail
+using namespace pin_detail;
+
+void* pinned_alloc(size_t bytes) {
+  if (bytes < PIN_MIN) {
+    void* p = std::malloc(bytes ? bytes : 1);
+    if (!p) throw std::bad_alloc();
+    return p;
+  }
+  const size_t cap = pin_cap(bytes);
+  {
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    auto it = g_pin_free.find(cap);
+    if (it != g_pin_free.end()) {
+      void* p = it->second;
+      g_pin_free.erase(it);
+      g_pin_cached -= cap;
+      return p;
+    }
+  }
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, cap, cudaHostAllocPortable) != cudaSuccess) {
+    cudaGetLastError();
+    p = std::malloc(cap);  // no device / driver: still correct, just pageable
+    if (!p) throw std::bad_alloc();
+    // remember it is not page-locked: tag by registering nothing; freed with free()
+    std::lock_guard<std::mutex> g(g_pin_mu);
+    g_unpinned().insert(p);
+  }
+  return p;
+}
+
+void pinned_free(void* p, size_t bytes) {
+  if (!p) return;
+  if (bytes < PIN_MIN) {
+    std::free(p);
+    return;
+  }
+  const size_t cap = pin_cap(bytes);
+  std::lock_guard<std::mutex> g(g_pin_mu);
+  if (g_unpinned().erase(p)) {
+    std::free(p);
+    return;
+  }
+  if (g_pin_cached + cap <= PIN_CACHE_MAX) {
+    g_pin_free.emplace(cap, p);
+    g_pin_cached += cap;
+  } else {
+    cudaFreeHost(p);
+  }
+}
+}  // namespace hx
+
 struct FarBlock {
   int leaf;        // index into plan leaves
   int m, n, mu;
@@ -112,6 +186,7 @@ struct FarBlock {
 struct hx_ctx {
   int device = 0;
   cudaStream_t s = nullptr;
+  cudaStream_t s2 = nullptr;  // copy stream (materialization work lists)
   DArr<double> own[NUM_BUFS];
   double* attached[2] = {nullptr, nullptr};
   int64_t opnd_elems[2] = {0, 0};
@@ -236,47 +311,104 @@ void run_gemm_batch(hx_ctx* c, std::vector<Term>& terms, std::vector<Tile>& tile
               nullptr);
 }
 
+// QR jobs: small panels (p <= 256, q <= 32) one warp each, others one CTA each (panel in
+// shared memory when it fits, else in place in HBM/L2).
 void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
-  std::vector<QrJob> sm, gl;
+  std::vector<QrJob> all;
+  all.reserve(jobs.size());
   size_t smax = 0;
+  // warp jobs bucketed by panel height so that each launch sizes its smem slices tightly
+  const int pcls[3] = {64, 128, 256};
+  size_t wb[4] = {0, 0, 0, 0}, wslice[3] = {0, 0, 0};
+  for (int k = 0; k < 3; ++k) {
+    wb[k] = all.size();
+    for (const QrJob& j : jobs)
+      if (j.q <= 32 && j.p <= pcls[k] && (k == 0 || j.p > pcls[k - 1])) {
+        all.push_back(j);
+        wslice[k] = std::max(wslice[k], size_t(j.p + 1) * j.q + j.q);
+      }
+  }
+  wb[3] = all.size();
+  const size_t nw = all.size();
   for (const QrJob& j : jobs) {
     const size_t need = size_t(j.p) * j.q * sizeof(double);
-    if (need <= size_t(SMEM_CAP)) {
-      sm.push_back(j);
+    if (!(j.p <= 256 && j.q <= 32) && need <= size_t(SMEM_CAP)) {
+      all.push_back(j);
       smax = std::max(smax, need);
-    } else {
-      gl.push_back(j);
     }
   }
-  if (!sm.empty()) {
-    c->qr_jobs.upload(sm, c->s);
-    CK(cudaFuncSetAttribute(qr_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smax)));
-    qr_explicit_kernel<<<int(sm.size()), LA_THREADS, smax, c->s>>>(c->qr_jobs.p, 1);
+  const size_t ns = all.size() - nw;
+  for (const QrJob& j : jobs) {
+    const size_t need = size_t(j.p) * j.q * sizeof(double);
+    if (!(j.p <= 256 && j.q <= 32) && need > size_t(SMEM_CAP)) all.push_back(j);
+  }
+  const size_t ng = all.size() - nw - ns;
+  if (all.empty()) return;
+  c->qr_jobs.upload(all, c->s);
+  for (int k = 0; k < 3; ++k) {
+    const size_t n = wb[k + 1] - wb[k];
+    if (!n) continue;
+    const size_t per = wslice[k] * sizeof(double);
+    const int wpc = int(std::max<size_t>(1, std::min<size_t>(4, size_t(SMEM_CAP) / per)));
+    const size_t smem = per * size_t(wpc);
+    CK(cudaFuncSetAttribute(warp_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(SMEM_CAP)));
+    warp_qr_kernel<<<int((n + wpc - 1) / wpc), 32 * wpc, smem, c->s>>>(c->qr_jobs.p + wb[k],
+                                                                     int(n), int(wslice[k]));
     CK(cudaGetLastError());
     c->launches++;
-    // the job array is reused below: wait for the first launch's reads
-    if (!gl.empty()) CK(cudaStreamSynchronize(c->s));
   }
-  if (!gl.empty()) {
-    c->qr_jobs.upload(gl, c->s);
-    qr_explicit_kernel<<<int(gl.size()), LA_THREADS, 0, c->s>>>(c->qr_jobs.p, 0);
+  if (ns) {
+    CK(cudaFuncSetAttribute(qr_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(smax)));
+    qr_explicit_kernel<<<int(ns), LA_THREADS, smax, c->s>>>(c->qr_jobs.p + nw, 1);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+  if (ng) {
+    qr_explicit_kernel<<<int(ng), LA_THREADS, 0, c->s>>>(c->qr_jobs.p + nw + ns, 0);
     CK(cudaGetLastError());
     c->launches++;
   }
 }
 
+// Jacobi jobs: q <= 16 / q <= 32 one warp each (columns in registers), larger one CTA.
 void run_jacobi(hx_ctx* c, const std::vector<JacJob>& jobs) {
   if (jobs.empty()) return;
+  std::vector<JacJob> all;
+  all.reserve(jobs.size());
+  for (const JacJob& j : jobs)
+    if (j.q <= 16) all.push_back(j);
+  const size_t n16 = all.size();
+  for (const JacJob& j : jobs)
+    if (j.q > 16 && j.q <= 32) all.push_back(j);
+  const size_t n32 = all.size() - n16;
   int qmax = 0;
-  for (const JacJob& j : jobs) qmax = std::max(qmax, j.q);
-  const size_t smem = size_t(2) * qmax * qmax * sizeof(double);
-  c->jac_jobs.upload(jobs, c->s);
-  CK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          int(std::max<size_t>(smem, 1))));
-  jacobi_svd_kernel<<<int(jobs.size()), LA_THREADS, smem, c->s>>>(c->jac_jobs.p);
-  CK(cudaGetLastError());
-  c->launches++;
+  for (const JacJob& j : jobs)
+    if (j.q > 32) {
+      all.push_back(j);
+      qmax = std::max(qmax, j.q);
+    }
+  const size_t nb = all.size() - n16 - n32;
+  c->jac_jobs.upload(all, c->s);
+  if (n16) {
+    warp_jacobi_kernel<16><<<int((n16 + 3) / 4), 128, 0, c->s>>>(c->jac_jobs.p, int(n16));
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+  if (n32) {
+    warp_jacobi_kernel<32><<<int((n32 + 3) / 4), 128, 0, c->s>>>(c->jac_jobs.p + n16, int(n32));
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+  if (nb) {
+    const size_t smem = size_t(2) * qmax * qmax * sizeof(double);
+    CK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(std::max<size_t>(smem, 1))));
+    jacobi_svd_kernel<<<int(nb), LA_THREADS, smem, c->s>>>(c->jac_jobs.p + n16 + n32);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
 }
 
 int default_sketch(int mu) {
@@ -299,6 +431,7 @@ extern "C" int hx_ctx_create(int device, hx_ctx** out) {
     auto* c = new hx_ctx();
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     *out = c;
     return HX_OK;
@@ -333,7 +466,7 @@ extern "C" int hx_ctx_operand_alias(hx_ctx* c) {
   return HX_OK;
 }
 
-extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg,
+extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
                           hx_product_stats* st) {
   return guarded([&]() -> int {
     if (!c || !P || !cfg) return fail(HX_EINVAL, "null argument");
@@ -346,26 +479,57 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
     cudaStream_t s = c->s;
     CK(cudaEventRecord(c->ev[0], s));
 
-    // ---- plan upload and buffers
-    const pvec<Term>* T3[3] = {&P->core_terms, &P->fac_terms, &P->mat_terms};
-    const pvec<Tile>* L3[3] = {&P->core_tiles, &P->fac_tiles, &P->mat_tiles};
-    const pvec<Group>* G3[3] = {&P->core_groups, &P->fac_groups, &P->mat_groups};
-    for (int i = 0; i < 3; ++i) {
-      c->terms[i].upload(*T3[i], s);
-      c->tiles[i].upload(*L3[i], s);
-      c->groups[i].upload(*G3[i], s);
-    }
+    // ---- buffers: every size is known before the factor work lists are filled
     c->own[BUF_CORE].ensure(size_t(P->core_elems));
     c->own[BUF_TERM].ensure(size_t(P->term_elems));
     c->own[BUF_TILE].ensure(size_t(P->tile_elems));
     c->own[BUF_GATHER].ensure(size_t(P->gather_elems));
     c->sumsq.ensure(size_t(P->n_sumsq));
-    c->gather_recs.upload(P->gather, s);
+    for (int i = 0; i < 2; ++i) {
+      c->terms[i].ensure(i ? P->fac_terms.size() : P->core_terms.size());
+      c->tiles[i].ensure(i ? P->fac_tiles.size() : P->core_tiles.size());
+      c->groups[i].ensure(i ? P->fac_groups.size() : P->core_groups.size());
+    }
+    c->terms[2].ensure(P->mat_terms.size());
+    c->tiles[2].ensure(P->mat_tiles.size());
+    c->groups[2].ensure(P->mat_groups.size());
+    c->gather_recs.ensure(P->gather.size());
+    // gather records first on the compute stream; the materialization lists on the copy
+    // stream, overlapping the whole formation phase (host arrays are page-locked)
+    auto h2d = [](void* d, const void* h, size_t bytes, cudaStream_t st) {
+      if (bytes) CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
+    };
+    h2d(c->gather_recs.p, P->gather.data(), P->gather.size() * sizeof(CopyRec), s);
+    CK(cudaEventRecord(c->ev[6], s));
+    CK(cudaStreamWaitEvent(c->s2, c->ev[6], 0));  // buffers allocated before s2 copies
+    h2d(c->terms[2].p, P->mat_terms.data(), P->mat_terms.size() * sizeof(Term), c->s2);
+    h2d(c->tiles[2].p, P->mat_tiles.data(), P->mat_tiles.size() * sizeof(Tile), c->s2);
+    h2d(c->groups[2].p, P->mat_groups.data(), P->mat_groups.size() * sizeof(Group), c->s2);
+    CK(cudaEventRecord(c->ev[7], c->s2));
     BufPtrs bp = c->ptrs();
     CK(cudaEventRecord(c->ev[5], s));
 
-    // ---- 1. term formation: gather thin factors per X-group, cores, X G products
-    for (const hx_plan::Batch& bt : P->batches) {
+    // ---- 1. term formation: gather thin factors per X-group, cores, X G products.
+    // Deferred plans fill each batch's work lists here, on the host, while the device
+    // runs the previous batch.
+    for (size_t bi = 0; bi < P->batches.size(); ++bi) {
+      if (!P->batch_ready[bi]) {
+        P->fill_batch(int64_t(bi));
+        P->batch_ready[bi] = 1;
+      }
+      const hx_plan::Batch& bt = P->batches[bi];
+      h2d(c->tiles[0].p + bt.core_begin, P->core_tiles.data() + bt.core_begin,
+          size_t(bt.core_end - bt.core_begin) * sizeof(Tile), s);
+      h2d(c->groups[0].p + bt.cg_begin, P->core_groups.data() + bt.cg_begin,
+          size_t(bt.cg_end - bt.cg_begin) * sizeof(Group), s);
+      h2d(c->terms[0].p + bt.cm_begin, P->core_terms.data() + bt.cm_begin,
+          size_t(bt.cm_end - bt.cm_begin) * sizeof(Term), s);
+      h2d(c->tiles[1].p + bt.fac_begin, P->fac_tiles.data() + bt.fac_begin,
+          size_t(bt.fac_end - bt.fac_begin) * sizeof(Tile), s);
+      h2d(c->groups[1].p + bt.fg_begin, P->fac_groups.data() + bt.fg_begin,
+          size_t(bt.fg_end - bt.fg_begin) * sizeof(Group), s);
+      h2d(c->terms[1].p + bt.fm_begin, P->fac_terms.data() + bt.fm_begin,
+          size_t(bt.fm_end - bt.fm_begin) * sizeof(Term), s);
       const int ng = int(bt.gather_end - bt.gather_begin);
       if (ng > 0) {
         gather_kernel<<<ng, 256, 0, s>>>(c->gather_recs.p + bt.gather_begin, bp);
@@ -379,6 +543,7 @@ extern "C" int hx_product(hx_ctx* c, const hx_plan* P, const hx_product_cfg* cfg
     }
     CK(cudaEventRecord(c->ev[1], s));
     // ---- 2. materialization
+    CK(cudaStreamWaitEvent(s, c->ev[7], 0));
     launch_gemm(c, P->tile, c->tiles[2].p, c->groups[2].p, c->terms[2].p,
                 int(P->mat_tiles.size()), bp, c->sumsq.p);
     CK(cudaEventRecord(c->ev[2], s));
@@ -751,6 +916,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   c->retry_d.release();
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->s);
+  cudaStreamDestroy(c->s2);
   delete c;
 }
 

@@ -168,8 +168,10 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
     t0 = time.perf_counter()
+    # deferred: the per-batch factor work lists are filled inside hx_product while the
+    # device runs the previous batch (host planning overlaps device work)
     plan = _lib.Plan(tree_arrays(h.bct), dir_a, dir_a if same else dir_b, leaf_mask,
-                     plan_tile(h.bct))
+                     plan_tile(h.bct), flags=_lib.Plan.DEFER)
     plan_ms = (time.perf_counter() - t0) * 1e3
     dev_a = resident(h)
     if dev_a is not None:

@@ -75,6 +75,6 @@ def test_plan_rejects_bad_arguments():
 
     import ctypes as C
     h = C.c_void_p()
-    rc = _lib.lib().hx_plan_create(None, None, None, None, 64, C.byref(h))
+    rc = _lib.lib().hx_plan_create(None, None, None, None, 64, 0, C.byref(h))
     assert rc == -1
     assert "null" in _lib.last_error()

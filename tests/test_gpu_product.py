@@ -86,6 +86,28 @@ def test_product_parity(golden, name, tag):
     assert rep.launches > 0
 
 
+@pytest.mark.parametrize("sketch0", [8, 40, 64])
+def test_sketch_widths_and_kernel_paths(golden, sketch0):
+    """Narrow sketches force the adaptive retry; wide ones (> 32) run the CTA QR / Jacobi
+    kernels instead of the warp ones; 64 makes every block a dense-route QR."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import multiply
+
+    g = golden("cfg1.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "cfg1.npz")
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    C = multiply.multiply_device(A, B, cfg, sketch0=sketch0)
+    ranks_ref = g["dense-svd/ranks"]
+    for b, r_ref in zip(g["dense-svd/ids"], ranks_ref):
+        if r_ref >= 0:
+            assert abs(C.data[int(b)].rank - r_ref) <= 1
+    exact = oa.to_dense() @ ob.to_dense()
+    err = np.linalg.norm(hx.to_dense(C) - exact) / np.linalg.norm(exact)
+    assert err <= tol
+    if sketch0 == 8:
+        assert C.report.sketch_rounds >= 2
+
+
 def test_fixed_rank_policy(golden):
     import paper_1805_08998_b200 as hx
 
