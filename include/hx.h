@@ -175,6 +175,8 @@ int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tile
                   int64_t n_sumsq);
 
 int hx_ctx_synchronize(hx_ctx* ctx);
+/* Device memory available to the context (free + the workspace it already holds). */
+int hx_ctx_mem_info(hx_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes);
 void hx_ctx_free(hx_ctx* ctx);
 
 int hx_last_error(char* buf, size_t len);

@@ -230,13 +230,9 @@ __global__ void copy_kernel(const CopyJob* __restrict__ jobs) {
 
 }  // namespace hx
 
-namespace {
-template <class T>
-void upload_tmp(hx_ctx* c, DArr<T>& d, const std::vector<T>& v) {
-  d.upload(v, c->s);
-}
-}  // namespace
-
+// Far leaves are processed in batches whose cross workspace fits a fixed budget; each
+// batch's recompressed factors are stashed compactly, and the final pool is laid out once
+// every rank is known.
 extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points, int dim,
                            int kernel, double h, double eps, int8_t* payload, int32_t* rank,
                            int64_t* u_off, int64_t* v_off, int64_t* d_off, int8_t* degraded,
@@ -254,139 +250,203 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
     const int64_t npts = tree->c_hi[0] - tree->c_lo[0];
     DArr<double> dpts;
     dpts.upload(points, size_t(npts * dim), s);
-    std::vector<int> far, near;
+    std::vector<int> far;
     for (int b = 0; b < nn; ++b) {
       payload[b] = 0;
       rank[b] = 0;
       u_off[b] = v_off[b] = d_off[b] = 0;
       degraded[b] = 0;
       if (tree->kind[b] == 1) far.push_back(b);
-      else if (tree->kind[b] == 2) near.push_back(b);
     }
     auto lo = [&](int cl) { return tree->c_lo[cl]; };
     auto sz = [&](int cl) { return tree->c_hi[cl] - tree->c_lo[cl]; };
-    // ---- cross iteration, batched to bound the workspace
+    auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
     const int kglob = JAC_QMAX;
-    std::vector<int> far_rank(far.size(), 0), far_deg(far.size(), 0);
-    std::vector<int> trunc_rank(far.size(), 0);
-    // final pool offsets need the ranks: keep per-far-leaf workspace until packing
-    int64_t ws_total = 0;
-    std::vector<int64_t> ws_off(far.size());
-    for (size_t f = 0; f < far.size(); ++f) {
-      const int b = far[f];
-      const int64_t m = sz(tree->tau[b]), n = sz(tree->sigma[b]);
-      const int64_t kc = std::min<int64_t>(kglob, std::min(m, n));
-      ws_off[f] = ws_total;
-      ws_total += ((m + n) * kc + 2 * kc * kc * 2 + 3 * kc * kc + kc + 63) & ~int64_t(15);
-      ws_total += ((m + n + 7) / 8 + 15) & ~int64_t(15);  // flags (bytes) in doubles
-    }
-    DArr<double> ws;
-    ws.ensure(size_t(std::max<int64_t>(ws_total, 16)));
-    std::vector<AcaJob> aj(far.size());
+    const size_t nf = far.size();
+    std::vector<int> far_rank(nf, 0), far_deg(nf, 0), fin_rank(nf, 0);
+    // compact per-leaf results: left (m x r) then right (n x r) in a stash buffer
+    std::vector<DArr<double>> stash;
+    std::vector<int> stash_id(nf, -1);
+    std::vector<int64_t> stash_off(nf, 0);
+    const int64_t WS_BUDGET = int64_t(1) << 30;  // doubles of cross workspace per batch
     struct Slots {
       double *L, *U, *RL, *RU, *core, *W, *V, *sig;
       int m, n, kc;
     };
-    std::vector<Slots> sl(far.size());
-    for (size_t f = 0; f < far.size(); ++f) {
-      const int b = far[f];
-      Slots& x = sl[f];
-      x.m = int(sz(tree->tau[b]));
-      x.n = int(sz(tree->sigma[b]));
-      x.kc = std::min(kglob, std::min(x.m, x.n));
-      double* p = ws.p + ws_off[f];
-      x.L = p;
-      p += int64_t(x.m) * x.kc;
-      x.U = p;
-      p += int64_t(x.n) * x.kc;
-      x.RL = p;
-      p += int64_t(x.kc) * x.kc;
-      x.RU = p;
-      p += int64_t(x.kc) * x.kc;
-      x.core = p;
-      p += int64_t(x.kc) * x.kc;
-      x.W = p;
-      p += int64_t(x.kc) * x.kc;
-      x.V = p;
-      p += int64_t(x.kc) * x.kc;
-      x.sig = p;
-      p += x.kc;
-      aj[f] = AcaJob{int(lo(tree->tau[b])), int(lo(tree->sigma[b])), x.m, x.n, x.kc, x.L, x.U,
-                     reinterpret_cast<uint8_t*>(p)};
-    }
+    DArr<double> ws;
     DArr<AcaJob> daj;
     DArr<int> drank, ddeg;
-    if (!far.empty()) {
+    DArr<CopyJob> dcj;
+    size_t f0 = 0;
+    while (f0 < nf) {
+      // ---- batch [f0, f1) within the workspace budget
+      size_t f1 = f0;
+      int64_t ws_total = 0;
+      std::vector<int64_t> ws_off;
+      while (f1 < nf) {
+        const int b = far[f1];
+        const int64_t m = sz(tree->tau[b]), n = sz(tree->sigma[b]);
+        const int64_t kc = std::min<int64_t>(kglob, std::min(m, n));
+        const int64_t need = a16((m + n) * kc + 5 * kc * kc + kc) + a16((m + n + 7) / 8 + 1);
+        if (f1 > f0 && ws_total + need > WS_BUDGET) break;
+        ws_off.push_back(ws_total);
+        ws_total += need;
+        ++f1;
+      }
+      const size_t nb = f1 - f0;
+      ws.ensure(size_t(std::max<int64_t>(ws_total, 16)));
+      std::vector<AcaJob> aj(nb);
+      std::vector<Slots> sl(nb);
+      for (size_t q = 0; q < nb; ++q) {
+        const int b = far[f0 + q];
+        Slots& x = sl[q];
+        x.m = int(sz(tree->tau[b]));
+        x.n = int(sz(tree->sigma[b]));
+        x.kc = std::min(kglob, std::min(x.m, x.n));
+        double* p = ws.p + ws_off[q];
+        x.L = p;
+        p += int64_t(x.m) * x.kc;
+        x.U = p;
+        p += int64_t(x.n) * x.kc;
+        x.RL = p;
+        p += int64_t(x.kc) * x.kc;
+        x.RU = p;
+        p += int64_t(x.kc) * x.kc;
+        x.core = p;
+        p += int64_t(x.kc) * x.kc;
+        x.W = p;
+        p += int64_t(x.kc) * x.kc;
+        x.V = p;
+        p += int64_t(x.kc) * x.kc;
+        x.sig = p;
+        p += x.kc;
+        aj[q] = AcaJob{int(lo(tree->tau[b])), int(lo(tree->sigma[b])), x.m, x.n, x.kc, x.L, x.U,
+                       reinterpret_cast<uint8_t*>(ws.p + ws_off[q] +
+                                                  a16((int64_t(x.m) + x.n) * x.kc +
+                                                      5 * int64_t(x.kc) * x.kc + x.kc))};
+      }
       daj.upload(aj, s);
-      drank.ensure(far.size());
-      ddeg.ensure(far.size());
-      aca_kernel<<<int(far.size()), LA_THREADS, 0, s>>>(daj.p, dpts.p, dim, kernel, h, eps,
-                                                        drank.p, ddeg.p);
+      drank.ensure(nb);
+      ddeg.ensure(nb);
+      aca_kernel<<<int(nb), LA_THREADS, 0, s>>>(daj.p, dpts.p, dim, kernel, h, eps, drank.p,
+                                                ddeg.p);
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(far_rank.data(), drank.p, far.size() * sizeof(int),
-                         cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(far_deg.data(), ddeg.p, far.size() * sizeof(int),
-                         cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(far_rank.data() + f0, drank.p, nb * sizeof(int), cudaMemcpyDeviceToHost,
+                         s));
+      CK(cudaMemcpyAsync(far_deg.data() + f0, ddeg.p, nb * sizeof(int), cudaMemcpyDeviceToHost,
+                         s));
       CK(cudaStreamSynchronize(s));
-    }
-    // ---- eps/2 recompression of rank > 1 crosses (truncate / lowrank_svd)
-    std::vector<int> tr;
-    for (size_t f = 0; f < far.size(); ++f) {
-      trunc_rank[f] = far_rank[f];
-      if (!far_deg[f] && far_rank[f] > 1) tr.push_back(int(f));
-    }
-    if (!tr.empty()) {
-      std::vector<QrJob> qj;
-      for (int f : tr) {
-        qj.push_back(QrJob{sl[f].L, sl[f].RL, sl[f].m, far_rank[f]});
-        qj.push_back(QrJob{sl[f].U, sl[f].RU, sl[f].n, far_rank[f]});
+      // ---- eps/2 recompression of rank > 1 crosses (truncate / lowrank_svd)
+      std::vector<int> tr;
+      for (size_t q = 0; q < nb; ++q) {
+        fin_rank[f0 + q] = far_rank[f0 + q];
+        if (!far_deg[f0 + q] && far_rank[f0 + q] > 1) tr.push_back(int(q));
       }
-      run_qr(c, qj);
-      // core = R_L R_U^T through the grouped GEMM (BUF_WORK = workspace base)
-      double* saved_work = c->own[BUF_WORK].p;
-      c->own[BUF_WORK].p = ws.p;
-      std::vector<Term> tt;
-      std::vector<Tile> tl;
-      std::vector<Group> tg;
-      for (int f : tr) {
-        const int k = far_rank[f];
-        single_term_tiles(tt, tl, tg,
-                          mk(BUF_WORK, sl[f].RL - ws.p, k, 0, BUF_WORK, sl[f].RU - ws.p, k, 0, k,
-                             k, k),
-                          BUF_WORK, sl[f].core - ws.p, k, k);
+      if (!tr.empty()) {
+        std::vector<QrJob> qj;
+        for (int q : tr) {
+          qj.push_back(QrJob{sl[q].L, sl[q].RL, sl[q].m, far_rank[f0 + q]});
+          qj.push_back(QrJob{sl[q].U, sl[q].RU, sl[q].n, far_rank[f0 + q]});
+        }
+        run_qr(c, qj);
+        double* saved_work = c->own[BUF_WORK].p;
+        c->own[BUF_WORK].p = ws.p;
+        std::vector<Term> tt;
+        std::vector<Tile> tl;
+        std::vector<Group> tg;
+        for (int q : tr) {
+          const int k = far_rank[f0 + q];
+          single_term_tiles(tt, tl, tg,
+                            mk(BUF_WORK, sl[q].RL - ws.p, k, 0, BUF_WORK, sl[q].RU - ws.p, k, 0, k,
+                               k, k),
+                            BUF_WORK, sl[q].core - ws.p, k, k);
+        }
+        run_gemm_batch(c, tt, tl, tg);
+        c->own[BUF_WORK].p = saved_work;
+        std::vector<JacJob> jj;
+        for (int q : tr)
+          jj.push_back(JacJob{sl[q].core, sl[q].sig, sl[q].W, sl[q].V, far_rank[f0 + q]});
+        run_jacobi(c, jj);
+        std::vector<SelJob> sj;
+        for (int q : tr)
+          sj.push_back(SelJob{sl[q].sig, nullptr, far_rank[f0 + q], far_rank[f0 + q], 1});
+        const int nt = int(tr.size());
+        c->sel_jobs.upload(sj, s);
+        c->rank_d.ensure(size_t(nt));
+        c->retry_d.ensure(size_t(nt));
+        select_rank_kernel<<<(nt + 127) / 128, 128, 0, s>>>(c->sel_jobs.p, nt, 0, 0.5 * eps, 0,
+                                                            1, c->rank_d.p, c->retry_d.p);
+        CK(cudaGetLastError());
+        std::vector<int> rk(nt);
+        CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, nt * sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int a = 0; a < nt; ++a) fin_rank[f0 + tr[a]] = rk[a];
       }
-      run_gemm_batch(c, tt, tl, tg);
-      c->own[BUF_WORK].p = saved_work;
-      std::vector<JacJob> jj;
-      for (int f : tr) jj.push_back(JacJob{sl[f].core, sl[f].sig, sl[f].W, sl[f].V, far_rank[f]});
-      run_jacobi(c, jj);
-      std::vector<SelJob> sj;
-      for (int f : tr)
-        sj.push_back(SelJob{sl[f].sig, nullptr, far_rank[f], far_rank[f], 1});
-      const int nt = int(tr.size());
-      c->sel_jobs.upload(sj, s);
-      c->rank_d.ensure(size_t(nt));
-      c->retry_d.ensure(size_t(nt));
-      select_rank_kernel<<<(nt + 127) / 128, 128, 0, s>>>(c->sel_jobs.p, nt, 0, 0.5 * eps, 0, 1,
-                                                          c->rank_d.p, c->retry_d.p);
-      CK(cudaGetLastError());
-      std::vector<int> rk(nt);
-      CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, nt * sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
-      for (int a = 0; a < nt; ++a) trunc_rank[tr[a]] = rk[a];
+      // ---- compact factors of this batch into a stash buffer
+      int64_t st_total = 0;
+      for (size_t q = 0; q < nb; ++q) {
+        const size_t f = f0 + q;
+        if (far_deg[f] || fin_rank[f] == 0) continue;
+        stash_off[f] = st_total;
+        st_total += a16(int64_t(sl[q].m) * fin_rank[f]) + a16(int64_t(sl[q].n) * fin_rank[f]);
+      }
+      if (st_total > 0) {
+        stash.emplace_back();
+        DArr<double>& sb = stash.back();
+        sb.ensure(size_t(st_total));
+        const int sid = int(stash.size() - 1);
+        std::vector<SmallJob> jl;
+        std::vector<CopyJob> cj;
+        int qmax = 1, rows_max = 1;
+        for (size_t q = 0; q < nb; ++q) {
+          const size_t f = f0 + q;
+          if (far_deg[f] || fin_rank[f] == 0) continue;
+          stash_id[f] = sid;
+          const Slots& x = sl[q];
+          const int r = fin_rank[f];
+          double* left = sb.p + stash_off[f];
+          double* right = left + a16(int64_t(x.m) * r);
+          if (far_rank[f] <= 1) {
+            cj.push_back(CopyJob{x.L, left, int64_t(x.m) * r});
+            cj.push_back(CopyJob{x.U, right, int64_t(x.n) * r});
+          } else {
+            const int k = far_rank[f];
+            jl.push_back(SmallJob{x.L, x.W, x.sig, left, x.m, k, k, x.m, r});
+            jl.push_back(SmallJob{x.U, x.V, nullptr, right, x.n, k, k, x.n, r});
+            qmax = std::max(qmax, k);
+            rows_max = std::max(rows_max, std::max(x.m, x.n));
+          }
+        }
+        if (!cj.empty()) {
+          dcj.upload(cj, s);
+          copy_kernel<<<int(cj.size()), 256, 0, s>>>(dcj.p);
+          CK(cudaGetLastError());
+        }
+        if (!jl.empty()) {
+          c->small_jobs.upload(jl, s);
+          const size_t smem = size_t(qmax) * qmax * sizeof(double);
+          CK(cudaFuncSetAttribute(small_product_kernel,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+          dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
+          small_product_kernel<<<grid, 128, smem, s>>>(c->small_jobs.p);
+          CK(cudaGetLastError());
+        }
+        CK(cudaStreamSynchronize(s));  // job arrays and the workspace are reused next batch
+      }
+      f0 = f1;
     }
+    ws.release();
     // ---- final pool layout (leaf id order)
     std::vector<int> far_index(nn, -1);
-    for (size_t f = 0; f < far.size(); ++f) far_index[far[f]] = int(f);
+    for (size_t f = 0; f < nf; ++f) far_index[far[f]] = int(f);
     int64_t pos = 0;
-    auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
     for (int b = 0; b < nn; ++b) {
       if (tree->kind[b] == 0) continue;
       const int64_t m = sz(tree->tau[b]), n = sz(tree->sigma[b]);
       const int f = far_index[b];
       if (f >= 0 && !far_deg[f]) {
         payload[b] = 1;
-        rank[b] = trunc_rank[f];
+        rank[b] = fin_rank[f];
         u_off[b] = pos;
         pos += a16(m * rank[b]);
         v_off[b] = pos;
@@ -420,45 +480,25 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
       dense_block_kernel<<<grid, 256, 0, s>>>(ddj.p, dpts.p, dim, kernel, h);
       CK(cudaGetLastError());
     }
-    // low-rank payloads
-    std::vector<SmallJob> jl;
+    // low-rank payloads from the stash
     std::vector<CopyJob> cj;
-    int qmax = 1, rows_max = 1;
-    for (size_t f = 0; f < far.size(); ++f) {
+    for (size_t f = 0; f < nf; ++f) {
       const int b = far[f];
       if (payload[b] != 1 || rank[b] == 0) continue;
-      const Slots& x = sl[f];
-      double* left = pool + u_off[b];
-      double* right = pool + v_off[b];
-      if (far_rank[f] <= 1) {
-        cj.push_back(CopyJob{x.L, left, int64_t(x.m) * rank[b]});
-        cj.push_back(CopyJob{x.U, right, int64_t(x.n) * rank[b]});
-      } else {
-        const int k = far_rank[f];
-        jl.push_back(SmallJob{x.L, x.W, x.sig, left, x.m, k, k, x.m, rank[b]});
-        jl.push_back(SmallJob{x.U, x.V, nullptr, right, x.n, k, k, x.n, rank[b]});
-        qmax = std::max(qmax, k);
-        rows_max = std::max(rows_max, std::max(x.m, x.n));
-      }
+      const int64_t m = sz(tree->tau[b]), n = sz(tree->sigma[b]);
+      const double* left = stash[size_t(stash_id[f])].p + stash_off[f];
+      const double* right = left + a16(m * rank[b]);
+      cj.push_back(CopyJob{left, pool + u_off[b], m * rank[b]});
+      cj.push_back(CopyJob{right, pool + v_off[b], n * rank[b]});
     }
-    DArr<CopyJob> dcj;
     if (!cj.empty()) {
       dcj.upload(cj, s);
       copy_kernel<<<int(cj.size()), 256, 0, s>>>(dcj.p);
       CK(cudaGetLastError());
     }
-    if (!jl.empty()) {
-      c->small_jobs.upload(jl, s);
-      const size_t smem = size_t(qmax) * qmax * sizeof(double);
-      CK(cudaFuncSetAttribute(small_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(smem)));
-      dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
-      small_product_kernel<<<grid, 128, smem, s>>>(c->small_jobs.p);
-      CK(cudaGetLastError());
-    }
     CK(cudaStreamSynchronize(s));
+    for (auto& sb : stash) sb.release();
     dpts.release();
-    ws.release();
     daj.release();
     drank.release();
     ddeg.release();

@@ -877,6 +877,22 @@ extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const
   });
 }
 
+extern "C" int hx_ctx_mem_info(hx_ctx* c, int64_t* free_bytes, int64_t* total_bytes) {
+  return guarded([&]() -> int {
+    if (!c) return fail(HX_EINVAL, "null ctx");
+    CK(cudaSetDevice(c->device));
+    size_t f = 0, t = 0;
+    CK(cudaMemGetInfo(&f, &t));
+    // memory this context already holds for reuse counts as available
+    size_t held = 0;
+    for (int i = 0; i < NUM_BUFS; ++i)
+      if (i != BUF_A && i != BUF_B && i != BUF_WORK) held += c->own[i].cap * sizeof(double);
+    if (free_bytes) *free_bytes = int64_t(f + held);
+    if (total_bytes) *total_bytes = int64_t(t);
+    return HX_OK;
+  });
+}
+
 extern "C" int hx_ctx_synchronize(hx_ctx* c) {
   return guarded([&]() -> int {
     if (!c) return fail(HX_EINVAL, "null ctx");

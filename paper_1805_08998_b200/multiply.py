@@ -9,11 +9,19 @@ All arithmetic runs in ``libhx.so`` (``include/hx.h``): the flat term lists are 
 the C++ planner (the ``restrict`` bookkeeping), then term formation, block
 materialization and recompression run as sm_100a kernels.  There is no CPU path: a
 missing library or GPU raises.
+
+Execution is chunked: the output leaves are split into chunks of whole subtrees rooted at
+the first block level that holds a far leaf.  No term is created above that level
+(terms come from far operand blocks), so chunks share no work; each chunk's work lists
+are planned on a host thread while the device runs the previous chunk, and device
+memory is bounded by the largest chunk instead of the whole product.
 """
 
 from __future__ import annotations
 
 import ctypes as C
+import os
+import threading
 import time
 import warnings
 from dataclasses import dataclass, field
@@ -53,7 +61,7 @@ class MultReport:
     near_leaves: int = 0
     wall_s: float = 0.0
     warnings: list = field(default_factory=list)
-    # device-side breakdown (milliseconds, CUDA events) and plan statistics
+    # device-side breakdown (milliseconds, CUDA events, summed over chunks) and plan stats
     plan_ms: float = 0.0
     device_ms: float = 0.0
     form_ms: float = 0.0
@@ -63,6 +71,7 @@ class MultReport:
     out_elems: int = 0
     sketch_rounds: int = 0
     launches: int = 0
+    chunks: int = 0
     fro2: float = 0.0
 
 
@@ -134,26 +143,104 @@ def _host_directory(h):
     return pool, d
 
 
+# --------------------------------------------------------------------------- chunks
+
+def _subtree_end(arr):
+    """end[b] = one past the last pre-order id of b's subtree."""
+    n = arr.n_nodes
+    size = np.ones(n, dtype=np.int64)
+    child = arr.child
+    for b in range(n - 1, -1, -1):
+        c = child[b]
+        if c[0] >= 0:
+            size[b] += size[c].sum()
+    return np.arange(n) + size
+
+
+def chunk_units(bct):
+    """Disjoint pre-order id ranges covering every leaf: the subtrees rooted at the first
+    block level holding a far leaf, and the leaves above it; with their leaf areas."""
+    arr = block_arrays(bct)
+    cached = getattr(arr, "_hx_units", None)
+    if cached is not None:
+        return cached
+    kind, level = arr.kind_code, arr.level
+    far_lv = level[kind == 1]
+    lf = int(far_lv.min()) if far_lv.size else int(level.max())
+    end = _subtree_end(arr)
+    lo, hi = arr.tree.lo, arr.tree.hi
+    area = np.where(kind != 0, (hi[arr.tau] - lo[arr.tau]) * (hi[arr.sigma] - lo[arr.sigma]), 0)
+    carea = np.concatenate([[0], np.cumsum(area)])
+    roots = np.flatnonzero((level == lf) | ((level < lf) & (kind != 0)))
+    units = [(int(b), int(end[b]), float(carea[end[b]] - carea[b])) for b in roots]
+    try:
+        arr._hx_units = units
+    except AttributeError:  # pragma: no cover
+        pass
+    return units
+
+
+def chunk_masks(bct, n_chunks, base_mask=None):
+    """Leaf masks of about `n_chunks` chunks of consecutive units with equal leaf area."""
+    arr = block_arrays(bct)
+    units = chunk_units(bct)
+    total = sum(u[2] for u in units)
+    target = total / max(1, n_chunks)
+    leaf = arr.kind_code != 0
+    if base_mask is not None:
+        leaf = leaf & (np.asarray(base_mask) != 0)
+    masks, cur, acc = [], [], 0.0
+    for u in units:
+        cur.append(u)
+        acc += u[2]
+        if acc >= target and len(masks) < n_chunks - 1:
+            masks.append(cur)
+            cur, acc = [], 0.0
+    if cur:
+        masks.append(cur)
+    out = []
+    for group in masks:
+        m = np.zeros(arr.n_nodes, dtype=np.uint8)
+        for b0, b1, _ in group:
+            m[b0:b1] = leaf[b0:b1]
+        if m.any():
+            out.append(m)
+    return out
+
+
+def default_chunks(bct, dev=None):
+    """Chunks needed to keep one chunk's device workspace (materialized blocks plus term
+    factors, ~12x the leaf area on the BASELINE configs) within ~60% of free memory."""
+    env = os.environ.get("HX_CHUNKS")
+    if env:
+        return max(1, int(env))
+    area = sum(u[2] for u in chunk_units(bct))
+    free = 60e9
+    if dev is not None:
+        fb, tb = C.c_int64(), C.c_int64()
+        if _lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)) == 0:
+            free = float(fb.value)
+    need = area * 8.0 * 12.0
+    return max(1, int(np.ceil(need / (0.6 * free))))
+
+
+# --------------------------------------------------------------------------- product
+
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
-                    device_operands=True, fetch=True):
+                    device_operands=True, fetch=True, chunks=None):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
     assembly) instead of uploading the host copy.  ``leaf_mask`` restricts the product to
     the owned output leaves (multi-GPU partition).  ``fetch=False`` leaves the output
     blocks in device memory (only ranks and the report come back): the device-resident
-    measurement of bench.py."""
+    measurement of bench.py.  ``chunks``: number of pipelined chunks (default by size)."""
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     policy = cfg.policy
     kind, eps, kmax = _policy_args(policy)
-    warn = []
     if kind == 0 and eps <= np.finfo(float).eps:
-        with warnings.catch_warnings(record=True) as wl:
-            warnings.simplefilter("always")
-            eps = clamp_eps(eps)
-        for w in wl:
-            warnings.warn(w.message)
+        eps = clamp_eps(eps)
     t_start = time.perf_counter()
     same = k is h
 
@@ -167,12 +254,6 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
-    t0 = time.perf_counter()
-    # deferred: the per-batch factor work lists are filled inside hx_product while the
-    # device runs the previous batch (host planning overlaps device work)
-    plan = _lib.Plan(tree_arrays(h.bct), dir_a, dir_a if same else dir_b, leaf_mask,
-                     plan_tile(h.bct), flags=_lib.Plan.DEFER)
-    plan_ms = (time.perf_counter() - t0) * 1e3
     dev_a = resident(h)
     if dev_a is not None:
         dev.set_operand(0, dev_ptr=dev_a[1], n=dev_a[2])
@@ -189,61 +270,115 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     comp = cfg.compressor
     pc = _lib.HxProductCfg(kind, eps, kmax, TAG_CODES[comp.tag], int(comp.seed) & (2**64 - 1),
                            int(sketch0), int(oversample))
-    st = _lib.HxProductStats()
-    _lib.check(_lib.lib().hx_product(dev.h, plan.h, C.byref(pc), C.byref(st)), "hx_product")
-    leaves = plan.leaves()
-    nl = len(leaves["ids"])
-    rank = np.zeros(nl, np.int32)
-    deg = np.zeros(nl, np.int8)
-    off = np.zeros(nl, np.int64)
-    _lib.check(_lib.lib().hx_result_layout(dev.h, _lib.ptr(rank, _lib.i32p),
-                                           _lib.ptr(deg, _lib.i8p), _lib.ptr(off, _lib.i64p)),
-               "hx_result_layout")
-    data = {}
-    degraded = set()
-    ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
-    kinds = leaves["kind"].tolist()
-    rl, ol = rank.tolist(), off.tolist()
-    if fetch:
-        res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
-        _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p), res.size),
-                   "hx_result_download")
-    for i in range(nl if fetch else 0):
-        m, n, o = ms[i], ns[i], ol[i]
-        if kinds[i] == 1:
-            r = rl[i]
-            left = res[o:o + m * r].reshape(r, m).T
-            right = res[o + m * r:o + (m + n) * r].reshape(r, n).T
-            data[ids[i]] = LowRank(left, right)
-            if deg[i]:
-                degraded.add(ids[i])
-        else:
-            data[ids[i]] = res[o:o + m * n].reshape(n, m).T
+    ta = tree_arrays(h.bct)
+    tile = plan_tile(h.bct)
+    nch = default_chunks(h.bct, dev) if chunks is None else max(1, int(chunks))
+    masks = chunk_masks(h.bct, nch, leaf_mask) if (nch > 1 or leaf_mask is not None) else [None]
+    if leaf_mask is not None and not masks:
+        masks = []
+
+    plan_ms = [0.0]
+
+    def make_plan(mask):
+        t0 = time.perf_counter()
+        # deferred: the per-batch factor work lists are filled inside hx_product while the
+        # device runs the previous batch
+        p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile, flags=_lib.Plan.DEFER)
+        plan_ms[0] += (time.perf_counter() - t0) * 1e3
+        return p
+
     rep = MultReport()
-    rep.degraded_blocks = int(st.degraded_blocks)
-    rep.max_far_rank = int(st.max_far_rank)
-    rep.matvec_count = int(st.matvec_count)
-    rep.far_leaves = int(st.far_leaves)
-    rep.near_leaves = int(st.near_leaves)
-    rep.warnings = warn
-    rep.plan_ms = plan_ms
-    rep.device_ms = st.ms_total
-    rep.form_ms = st.ms_form
-    rep.materialize_ms = st.ms_mat
-    rep.recompress_ms = st.ms_recompress
-    rep.upload_ms = st.ms_upload
-    rep.out_elems = int(st.out_elems)
-    rep.sketch_rounds = int(st.sketch_rounds)
-    rep.launches = int(st.launches)
-    rep.fro2 = float(st.fro2_total)
+    data, degraded = {}, set()
+    leaves_all, ranks_all, infos = [], [], []
+    nxt = {"plan": None, "err": None}
+
+    def plan_async(mask):
+        try:
+            nxt["plan"] = make_plan(mask)
+        except BaseException as exc:  # re-raised on the main thread
+            nxt["err"] = exc
+
+    worker = None
+    plan = make_plan(masks[0]) if masks else None
+    for ci in range(len(masks)):
+        if ci + 1 < len(masks):
+            worker = threading.Thread(target=plan_async, args=(masks[ci + 1],))
+            worker.start()
+        st = _lib.HxProductStats()
+        _lib.check(_lib.lib().hx_product(dev.h, plan.h, C.byref(pc), C.byref(st)),
+                   "hx_product")
+        leaves = plan.leaves()
+        nl = len(leaves["ids"])
+        rank = np.zeros(nl, np.int32)
+        deg = np.zeros(nl, np.int8)
+        off = np.zeros(nl, np.int64)
+        _lib.check(_lib.lib().hx_result_layout(dev.h, _lib.ptr(rank, _lib.i32p),
+                                               _lib.ptr(deg, _lib.i8p),
+                                               _lib.ptr(off, _lib.i64p)), "hx_result_layout")
+        if fetch:
+            res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
+            _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p),
+                                                     res.size), "hx_result_download")
+            ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
+            kinds, rl, ol = leaves["kind"].tolist(), rank.tolist(), off.tolist()
+            for i in range(nl):
+                m, n, o = ms[i], ns[i], ol[i]
+                if kinds[i] == 1:
+                    r = rl[i]
+                    data[ids[i]] = LowRank(res[o:o + m * r].reshape(r, m).T,
+                                           res[o + m * r:o + (m + n) * r].reshape(r, n).T)
+                    if deg[i]:
+                        degraded.add(ids[i])
+                else:
+                    data[ids[i]] = res[o:o + m * n].reshape(n, m).T
+        rep.degraded_blocks += int(st.degraded_blocks)
+        rep.max_far_rank = max(rep.max_far_rank, int(st.max_far_rank))
+        rep.matvec_count += int(st.matvec_count)
+        rep.far_leaves += int(st.far_leaves)
+        rep.near_leaves += int(st.near_leaves)
+        rep.device_ms += st.ms_total
+        rep.form_ms += st.ms_form
+        rep.materialize_ms += st.ms_mat
+        rep.recompress_ms += st.ms_recompress
+        rep.upload_ms += st.ms_upload
+        rep.out_elems += int(st.out_elems)
+        rep.sketch_rounds = max(rep.sketch_rounds, int(st.sketch_rounds))
+        rep.launches += int(st.launches)
+        rep.fro2 += float(st.fro2_total)
+        leaves_all.append(leaves)
+        ranks_all.append(rank)
+        infos.append(plan.info)
+        plan.close()
+        if worker is not None:
+            worker.join()
+            worker = None
+            if nxt["err"] is not None:
+                raise nxt["err"]
+            plan, nxt["plan"] = nxt["plan"], None
+    rep.chunks = len(masks)
+    rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start
     out = HMatrix(h.bct, data, degraded)
     out.report = rep
-    out.plan_info = plan.info
-    out.plan_leaves = leaves
-    out.leaf_rank = rank
-    plan.close()
+    out.plan_info = _sum_info(infos)
+    out.plan_leaves = ({key: np.concatenate([lv[key] for lv in leaves_all]) for key in
+                        leaves_all[0]} if leaves_all else {})
+    out.leaf_rank = np.concatenate(ranks_all) if ranks_all else np.zeros(0, np.int32)
     return out
+
+
+def _sum_info(infos):
+    tot = _lib.HxPlanInfo()
+    for inf in infos:
+        for name, typ in tot._fields_:
+            if name == "created":
+                for i in range(3):
+                    tot.created[i] += inf.created[i]
+            elif name == "max_out_dim":
+                tot.max_out_dim = max(tot.max_out_dim, inf.max_out_dim)
+            else:
+                setattr(tot, name, getattr(tot, name) + getattr(inf, name))
+    return tot
 
 
 def hmult_new(h, k, cfg):

@@ -108,6 +108,31 @@ def test_sketch_widths_and_kernel_paths(golden, sketch0):
         assert C.report.sketch_rounds >= 2
 
 
+@pytest.mark.parametrize("chunks", [3, 7])
+def test_chunked_product_matches_single(golden, chunks):
+    """Pipelined chunks of whole subtrees give the same product as one chunk."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import multiply
+
+    g = golden("cfg1.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "cfg1.npz")
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    one = multiply.multiply_device(A, B, cfg, chunks=1)
+    many = multiply.multiply_device(A, B, cfg, chunks=chunks)
+    assert many.report.chunks > 1
+    assert set(one.data) == set(many.data)
+    for b, p in one.data.items():
+        q = many.data[b]
+        if hasattr(p, "left"):
+            assert p.rank == q.rank
+            d = np.linalg.norm(p.to_dense() - q.to_dense())
+            assert d <= 1e-12 * max(np.linalg.norm(p.to_dense()), 1e-300)
+        else:
+            assert np.array_equal(p, q)
+    assert many.report.far_leaves == one.report.far_leaves
+    assert abs(many.plan_info.flops_form - one.plan_info.flops_form) <= 1e-9 * one.plan_info.flops_form
+
+
 def test_fixed_rank_policy(golden):
     import paper_1805_08998_b200 as hx
 
