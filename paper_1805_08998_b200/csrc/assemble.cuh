@@ -207,7 +207,9 @@ __global__ void __launch_bounds__(LA_THREADS) aca_kernel(const AcaJob* __restric
   }
   if (tid == 0) {
     rank_out[blockIdx.x] = k;
-    deg_out[blockIdx.x] = degraded;
+    // stopping at the workspace cap without the two-hit criterion is not a certified
+    // approximation: store the block dense like a degraded one
+    deg_out[blockIdx.x] = degraded || (k == kcap && kcap < min(m, n) && hits < 2);
   }
 }
 
@@ -369,7 +371,7 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
         run_jacobi(c, jj);
         std::vector<SelJob> sj;
         for (int q : tr)
-          sj.push_back(SelJob{sl[q].sig, nullptr, far_rank[f0 + q], far_rank[f0 + q], 1});
+          sj.push_back(SelJob{sl[q].sig, nullptr, far_rank[f0 + q], far_rank[f0 + q], 1, 0});
         const int nt = int(tr.size());
         c->sel_jobs.upload(sj, s);
         c->rank_d.ensure(size_t(nt));
@@ -424,11 +426,8 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
         }
         if (!jl.empty()) {
           c->small_jobs.upload(jl, s);
-          const size_t smem = size_t(qmax) * qmax * sizeof(double);
-          CK(cudaFuncSetAttribute(small_product_kernel,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
           dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
-          small_product_kernel<<<grid, 128, smem, s>>>(c->small_jobs.p);
+          small_product_kernel<<<grid, 128, 0, s>>>(c->small_jobs.p);
           CK(cudaGetLastError());
         }
         CK(cudaStreamSynchronize(s));  // job arrays and the workspace are reused next batch

@@ -15,7 +15,8 @@
 namespace hx {
 
 constexpr int LA_THREADS = 256;
-constexpr int JAC_QMAX = 96;
+constexpr int JAC_QMAX = 512;      // widest sketch / SVD factor
+constexpr int JAC_SMEM_QMAX = 96;  // above: the Jacobi CTA works in place in HBM/L2
 
 struct QrJob {
   double* X;   // p x q column-major, ld = p; overwritten by explicit Q
@@ -33,10 +34,11 @@ struct JacJob {
 
 struct SelJob {
   const double* sig;
-  const double* fro2;  // ||T||_F^2 of the block
+  const double* fro2;  // ||T||_F^2 of the block, or the unsampled tail itself (resid = 1)
   int l;               // sketch width (number of singular values)
   int mu;              // min(m, n)
   int exact;           // 1: the sketch spans the whole block (no unsampled tail)
+  int resid;           // 1: *fro2 is ||T - Q Q^T T||_F^2 measured directly
 };
 
 struct SmallJob {
@@ -172,10 +174,12 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
   const int q = jb.q;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
-  double* M = dsm;              // q x q, ld q
-  double* V = dsm + q * q;      // q x q, ld q
+  // q <= JAC_SMEM_QMAX: M, V in shared memory; wider factors: M in place of R, V in W
+  const bool big = q > JAC_SMEM_QMAX;
+  double* M = big ? const_cast<double*>(jb.R) : dsm;   // q x q, ld q
+  double* V = big ? jb.W : dsm + q * q;                 // q x q, ld q
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
-    M[e] = jb.R[e];
+    if (!big) M[e] = jb.R[e];
     V[e] = (e % q == e / q) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -246,12 +250,17 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
     order[pos] = c;
   }
   __syncthreads();
+  // V first: for wide factors the working V lives in jb.W, which is written last
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int x = e % q, pos = e / q;
+    jb.V[e] = V[order[pos] * q + x];
+  }
+  __syncthreads();
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
     const int x = e % q, pos = e / q;
     const int c = order[pos];
     const double s = norms[c];
     jb.W[e] = s > 0.0 ? M[c * q + x] / s : 0.0;
-    jb.V[e] = V[c * q + x];
   }
   for (int pos = threadIdx.x; pos < q; pos += blockDim.x) jb.sig[pos] = norms[order[pos]];
 }
@@ -273,7 +282,7 @@ __global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int p
   }
   double s2 = 0.0;
   for (int i = 0; i < l; ++i) s2 += jb.sig[i] * jb.sig[i];
-  double extra = jb.exact ? 0.0 : fmax(0.0, *jb.fro2 - s2);
+  double extra = jb.exact ? 0.0 : (jb.resid ? fmax(0.0, *jb.fro2) : fmax(0.0, *jb.fro2 - s2));
   // tails from the back: tail[r] = sqrt(extra + sum_{i>=r} s_i^2), summed smallest first
   // like the reference's reversed cumsum; total = tail[0]
   double tot2 = extra;
@@ -299,28 +308,36 @@ __global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int p
 }
 
 // out(rows x r) = P(rows x q) * C(:, :r) * diag(scale); grid (job, row chunk of 128).
+constexpr int SMALL_STAGE = 6144;  // doubles of C staged per pass (48 KB static smem)
+
 __global__ void __launch_bounds__(128) small_product_kernel(const SmallJob* __restrict__ jobs) {
-  extern __shared__ __align__(16) double cs[];
+  __shared__ double cs[SMALL_STAGE];
   const SmallJob jb = jobs[blockIdx.x];
   const int r = jb.r, q = jb.q;
   if (r == 0) return;
-  for (int e = threadIdx.x; e < q * r; e += blockDim.x) {
-    const int kk = e % q, c = e / q;
-    const double s = jb.scale ? jb.scale[c] : 1.0;
-    cs[e] = jb.C[kk + int64_t(c) * jb.ldc] * s;
-  }
-  __syncthreads();
-  for (int row0 = blockIdx.y * 128; row0 < jb.rows; row0 += 128 * gridDim.y) {
-    const int i = row0 + threadIdx.x;
-    if (i >= jb.rows) continue;
-    for (int c = 0; c < r; ++c) {
-      double acc = 0.0;
-      if (jb.P) {
-        for (int kk = 0; kk < q; ++kk) acc += jb.P[i + int64_t(kk) * jb.ld_p] * cs[kk + c * q];
-      } else {
-        acc = cs[i + c * q];
+  const int cc = max(1, SMALL_STAGE / q);  // output columns per staged pass
+  for (int c0 = 0; c0 < r; c0 += cc) {
+    const int c1 = min(r, c0 + cc);
+    __syncthreads();
+    for (int e = threadIdx.x; e < q * (c1 - c0); e += blockDim.x) {
+      const int kk = e % q, c = c0 + e / q;
+      const double s = jb.scale ? jb.scale[c] : 1.0;
+      cs[e] = jb.C[kk + int64_t(c) * jb.ldc] * s;
+    }
+    __syncthreads();
+    for (int row0 = blockIdx.y * 128; row0 < jb.rows; row0 += 128 * gridDim.y) {
+      const int i = row0 + threadIdx.x;
+      if (i >= jb.rows) continue;
+      for (int c = c0; c < c1; ++c) {
+        const double* cc_col = cs + (c - c0) * q;
+        double acc = 0.0;
+        if (jb.P) {
+          for (int kk = 0; kk < q; ++kk) acc += jb.P[i + int64_t(kk) * jb.ld_p] * cc_col[kk];
+        } else {
+          acc = cc_col[i];
+        }
+        jb.out[i + int64_t(c) * jb.rows] = acc;
       }
-      jb.out[i + int64_t(c) * jb.rows] = acc;
     }
   }
 }

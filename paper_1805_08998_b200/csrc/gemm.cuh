@@ -345,14 +345,18 @@ __global__ void __launch_bounds__(C::THREADS) grouped_gemm_kernel(
         if (r < tl.rows && c < tl.cols) {
           double* dst = out + r + int64_t(c) * tl.out_ld;
           double v = acc[a][b][h];
-          if (tl.mode == MODE_ADD) v += *dst;
-          *dst = v;
+          if (tl.mode == MODE_RESID_SUMSQ) {
+            v = *dst - v;  // residual of the tile against its approximation; not stored
+          } else {
+            if (tl.mode == MODE_ADD) v += *dst;
+            *dst = v;
+          }
           ss += v * v;
         }
       }
     }
   }
-  if (tl.mode == MODE_STORE_SUMSQ) {
+  if (tl.mode == MODE_STORE_SUMSQ || tl.mode == MODE_RESID_SUMSQ) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
     if (lane == 0) red[warp] = ss;

@@ -44,7 +44,8 @@ struct CopyRec {
 enum TileMode : uint8_t {
   MODE_STORE = 0,       // out  = sum
   MODE_ADD = 1,         // out += sum
-  MODE_STORE_SUMSQ = 2  // out  = sum, and sumsq[aux] = sum of squares of the tile
+  MODE_STORE_SUMSQ = 2,  // out  = sum, and sumsq[aux] = sum of squares of the tile
+  MODE_RESID_SUMSQ = 3   // out unchanged, sumsq[aux] = sum of squares of (out - sum)
 };
 
 struct Term {

@@ -205,6 +205,8 @@ struct hx_ctx {
   DArr<SelJob> sel_jobs;
   DArr<SmallJob> small_jobs;
   DArr<int> rank_d, retry_d;
+  DArr<double> rsum, resid;  // explicit-tail sums of squares (per tile, per block)
+  DArr<int> tb, te;
   std::vector<DArr<double>> work;  // one workspace per sketch round
   std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
   int64_t omega_rows = 0;
@@ -402,7 +404,8 @@ void run_jacobi(hx_ctx* c, const std::vector<JacJob>& jobs) {
     c->launches++;
   }
   if (nb) {
-    const size_t smem = size_t(2) * qmax * qmax * sizeof(double);
+    const int qs = std::min(qmax, JAC_SMEM_QMAX);  // wider factors run in place in HBM
+    const size_t smem = size_t(2) * qs * qs * sizeof(double);
     CK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(std::max<size_t>(smem, 1))));
     jacobi_svd_kernel<<<int(nb), LA_THREADS, smem, c->s>>>(c->jac_jobs.p + n16 + n32);
@@ -682,6 +685,59 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       }
       if (!tl.empty()) CK(cudaStreamSynchronize(s));  // rterms reused
       run_gemm_batch(c, tt, tl, tg);
+      // Tight tolerances: ||T||^2 - sum s_i^2 cancels below ~1e-15 ||T||^2, so the
+      // unsampled tail is measured directly as ||T - Q Bt^T||_F^2 (before QR(Bt)).
+      const bool explicit_tail = cfg->policy == 0 && cfg->eps < 1e-6;
+      std::vector<int> tail_b, tail_e;
+      if (explicit_tail) {
+        CK(cudaStreamSynchronize(s));  // rterms reused
+        tt.clear();
+        tl.clear();
+        tg.clear();
+        int slots = 0;
+        for (int i : active) {
+          FarBlock& f = fb[i];
+          tail_b.push_back(slots);
+          if (!f.dense) {
+            const int32_t g = int32_t(tg.size());
+            tg.push_back(Group{int32_t(tt.size()), int32_t(tt.size()) + 1});
+            tt.push_back(mk(BUF_WORK, int64_t(f.Y - wb), f.m, 0, BUF_WORK, int64_t(f.Bt - wb),
+                            f.n, 0, f.l, f.m, f.n));
+            for (int j = 0; j < f.n; j += 64)
+              for (int ii = 0; ii < f.m; ii += 64) {
+                Tile t;
+                std::memset(&t, 0, sizeof(t));
+                t.out_off = f.t_off + ii + int64_t(j) * f.m;
+                t.out_ld = f.m;
+                t.row0 = ii;
+                t.col0 = j;
+                t.rows = int16_t(std::min(64, f.m - ii));
+                t.cols = int16_t(std::min(64, f.n - j));
+                t.g_begin = g;
+                t.g_end = g + 1;
+                t.aux = slots++;
+                t.out_buf = BUF_TILE;
+                t.mode = MODE_RESID_SUMSQ;
+                tl.push_back(t);
+              }
+          }
+          tail_e.push_back(slots);
+        }
+        c->rsum.ensure(size_t(std::max(slots, 1)));
+        c->resid.ensure(size_t(std::max<size_t>(active.size(), 1)));
+        c->rterms.upload(tt, s);
+        c->rtiles.upload(tl, s);
+        c->rgroups.upload(tg, s);
+        launch_gemm(c, 64, c->rtiles.p, c->rgroups.p, c->rterms.p, int(tl.size()), c->ptrs(),
+                    c->rsum.p);
+        c->tb.upload(tail_b, s);
+        c->te.upload(tail_e, s);
+        const int na = int(active.size());
+        segment_sum_kernel<<<(na + 255) / 256, 256, 0, s>>>(c->rsum.p, c->tb.p, c->te.p,
+                                                            c->resid.p, na);
+        CK(cudaGetLastError());
+        c->launches++;
+      }
       run_qr(c, qj);
       // SVD of the small factor
       std::vector<JacJob> jj;
@@ -692,9 +748,13 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       run_jacobi(c, jj);
       // rank selection
       std::vector<SelJob> sj;
-      for (int i : active) {
-        FarBlock& f = fb[i];
-        sj.push_back(SelJob{f.sig, f.fro2, f.l, f.mu, (f.dense || f.l == f.mu) ? 1 : 0});
+      for (size_t a = 0; a < active.size(); ++a) {
+        FarBlock& f = fb[active[a]];
+        const int exact = (f.dense || f.l == f.mu) ? 1 : 0;
+        if (explicit_tail && !exact)
+          sj.push_back(SelJob{f.sig, c->resid.p + a, f.l, f.mu, 0, 1});
+        else
+          sj.push_back(SelJob{f.sig, f.fro2, f.l, f.mu, exact, 0});
       }
       const int na = int(active.size());
       c->sel_jobs.upload(sj, s);
@@ -756,11 +816,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     }
     if (!jl.empty()) {
       c->small_jobs.upload(jl, s);
-      const size_t smem = size_t(qmax) * qmax * sizeof(double);
-      CK(cudaFuncSetAttribute(small_product_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              int(smem)));
       dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
-      small_product_kernel<<<grid, 128, smem, s>>>(c->small_jobs.p);
+      small_product_kernel<<<grid, 128, 0, s>>>(c->small_jobs.p);
       CK(cudaGetLastError());
       c->launches++;
     }

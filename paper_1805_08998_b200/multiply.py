@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import collections
 import threading
 import time
 import warnings
@@ -157,55 +158,89 @@ def _subtree_end(arr):
     return np.arange(n) + size
 
 
+def _tree_meta(bct):
+    arr = block_arrays(bct)
+    meta = getattr(arr, "_hx_meta", None)
+    if meta is None:
+        kind = arr.kind_code
+        lo, hi = arr.tree.lo, arr.tree.hi
+        area = np.where(kind != 0,
+                        (hi[arr.tau] - lo[arr.tau]) * (hi[arr.sigma] - lo[arr.sigma]), 0)
+        meta = (_subtree_end(arr), np.concatenate([[0], np.cumsum(area)]))
+        try:
+            arr._hx_meta = meta
+        except AttributeError:  # pragma: no cover
+            pass
+    return meta
+
+
 def chunk_units(bct):
     """Disjoint pre-order id ranges covering every leaf: the subtrees rooted at the first
     block level holding a far leaf, and the leaves above it; with their leaf areas."""
     arr = block_arrays(bct)
-    cached = getattr(arr, "_hx_units", None)
-    if cached is not None:
-        return cached
     kind, level = arr.kind_code, arr.level
     far_lv = level[kind == 1]
     lf = int(far_lv.min()) if far_lv.size else int(level.max())
-    end = _subtree_end(arr)
-    lo, hi = arr.tree.lo, arr.tree.hi
-    area = np.where(kind != 0, (hi[arr.tau] - lo[arr.tau]) * (hi[arr.sigma] - lo[arr.sigma]), 0)
-    carea = np.concatenate([[0], np.cumsum(area)])
+    end, carea = _tree_meta(bct)
     roots = np.flatnonzero((level == lf) | ((level < lf) & (kind != 0)))
-    units = [(int(b), int(end[b]), float(carea[end[b]] - carea[b])) for b in roots]
-    try:
-        arr._hx_units = units
-    except AttributeError:  # pragma: no cover
-        pass
-    return units
+    return [(int(b), int(end[b]), float(carea[end[b]] - carea[b])) for b in roots]
 
 
-def chunk_masks(bct, n_chunks, base_mask=None):
-    """Leaf masks of about `n_chunks` chunks of consecutive units with equal leaf area."""
+def split_chunk(bct, group):
+    """Halve a chunk (list of units); a single unit splits into its child subtrees (their
+    common ancestors' terms are then planned for each part)."""
+    if len(group) > 1:
+        h = len(group) // 2
+        return [group[:h], group[h:]]
+    b0, b1, _ = group[0]
     arr = block_arrays(bct)
+    end, carea = _tree_meta(bct)
+    kids = [int(c) for c in arr.child[b0] if c >= 0]
+    if not kids:
+        return [group]
+    parts = [[(c, int(end[c]), float(carea[end[c]] - carea[c]))] for c in kids]
+    return parts
+
+
+def chunk_groups(bct, n_chunks):
+    """About `n_chunks` chunks of consecutive units with equal leaf area."""
     units = chunk_units(bct)
     total = sum(u[2] for u in units)
     target = total / max(1, n_chunks)
-    leaf = arr.kind_code != 0
-    if base_mask is not None:
-        leaf = leaf & (np.asarray(base_mask) != 0)
-    masks, cur, acc = [], [], 0.0
+    groups, cur, acc = [], [], 0.0
     for u in units:
         cur.append(u)
         acc += u[2]
-        if acc >= target and len(masks) < n_chunks - 1:
-            masks.append(cur)
+        if acc >= target and len(groups) < n_chunks - 1:
+            groups.append(cur)
             cur, acc = [], 0.0
     if cur:
-        masks.append(cur)
-    out = []
-    for group in masks:
-        m = np.zeros(arr.n_nodes, dtype=np.uint8)
-        for b0, b1, _ in group:
-            m[b0:b1] = leaf[b0:b1]
-        if m.any():
-            out.append(m)
-    return out
+        groups.append(cur)
+    return groups
+
+
+def group_mask(bct, group, base_mask=None):
+    arr = block_arrays(bct)
+    leaf = arr.kind_code != 0
+    m = np.zeros(arr.n_nodes, dtype=np.uint8)
+    for b0, b1, _ in group:
+        m[b0:b1] = leaf[b0:b1]
+    if base_mask is not None:
+        m &= (np.asarray(base_mask) != 0).astype(np.uint8)
+    return m
+
+
+def chunk_masks(bct, n_chunks, base_mask=None):
+    """Leaf masks of about `n_chunks` chunks (multi-GPU helpers and tests)."""
+    out = [group_mask(bct, g, base_mask) for g in chunk_groups(bct, n_chunks)]
+    return [m for m in out if m.any()]
+
+
+def plan_bytes(info):
+    """Device workspace a plan needs (the buffers hx_product sizes from it)."""
+    return 8.0 * (info.term_elems + info.tile_elems + info.core_elems + info.gather_elems) + \
+        48.0 * (info.mat_terms + info.core_terms + info.fac_terms) + \
+        40.0 * (info.mat_tiles + info.core_tiles + info.fac_tiles)
 
 
 def default_chunks(bct, dev=None):
@@ -273,13 +308,18 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     ta = tree_arrays(h.bct)
     tile = plan_tile(h.bct)
     nch = default_chunks(h.bct, dev) if chunks is None else max(1, int(chunks))
-    masks = chunk_masks(h.bct, nch, leaf_mask) if (nch > 1 or leaf_mask is not None) else [None]
-    if leaf_mask is not None and not masks:
-        masks = []
+    queue = collections.deque(chunk_groups(h.bct, nch))
+    fb, tb = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)), "hx_ctx_mem_info")
+    budget = 0.8 * float(fb.value) - 4e9
 
     plan_ms = [0.0]
 
-    def make_plan(mask):
+    def make_plan(group):
+        mask = group_mask(h.bct, group, leaf_mask) if (len(queue_all) > 1 or leaf_mask
+                                                       is not None or group_split[0]) else None
+        if mask is not None and not mask.any():
+            return None
         t0 = time.perf_counter()
         # deferred: the per-batch factor work lists are filled inside hx_product while the
         # device runs the previous batch
@@ -287,23 +327,47 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         plan_ms[0] += (time.perf_counter() - t0) * 1e3
         return p
 
+    queue_all = list(queue)
+    group_split = [False]
     rep = MultReport()
     data, degraded = {}, set()
     leaves_all, ranks_all, infos = [], [], []
     nxt = {"plan": None, "err": None}
 
-    def plan_async(mask):
+    def plan_async(group):
         try:
-            nxt["plan"] = make_plan(mask)
+            nxt["plan"] = make_plan(group)
         except BaseException as exc:  # re-raised on the main thread
             nxt["err"] = exc
 
     worker = None
-    plan = make_plan(masks[0]) if masks else None
-    for ci in range(len(masks)):
-        if ci + 1 < len(masks):
-            worker = threading.Thread(target=plan_async, args=(masks[ci + 1],))
+    n_run = 0
+    group = queue.popleft()
+    plan = make_plan(group)
+    while plan is not None or queue or worker is not None:
+        # a chunk whose workspace would not fit is split and planned again
+        while plan is not None and plan_bytes(plan.info) > budget:
+            parts = split_chunk(h.bct, group)
+            if len(parts) == 1:
+                break
+            group_split[0] = True
+            plan.close()
+            group = parts[0]
+            queue.extendleft(reversed(parts[1:]))
+            plan = make_plan(group)
+        if queue:
+            ngroup = queue.popleft()
+            worker = threading.Thread(target=plan_async, args=(ngroup,))
             worker.start()
+        if plan is None:  # nothing owned in this chunk
+            if worker is not None:
+                worker.join()
+                worker = None
+                if nxt["err"] is not None:
+                    raise nxt["err"]
+                plan, nxt["plan"], group = nxt["plan"], None, ngroup
+            continue
+        n_run += 1
         st = _lib.HxProductStats()
         _lib.check(_lib.lib().hx_product(dev.h, plan.h, C.byref(pc), C.byref(st)),
                    "hx_product")
@@ -349,13 +413,14 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         ranks_all.append(rank)
         infos.append(plan.info)
         plan.close()
+        plan = None
         if worker is not None:
             worker.join()
             worker = None
             if nxt["err"] is not None:
                 raise nxt["err"]
-            plan, nxt["plan"] = nxt["plan"], None
-    rep.chunks = len(masks)
+            plan, nxt["plan"], group = nxt["plan"], None, ngroup
+    rep.chunks = n_run
     rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start
     out = HMatrix(h.bct, data, degraded)

@@ -157,6 +157,57 @@ def test_fixed_rank_policy(golden):
             assert np.linalg.norm(q - p) <= 1e-12 * np.linalg.norm(p)
 
 
+@pytest.mark.parametrize("tag", ["dense-svd", "aca"])
+def test_product_a_neq_b_3d(tag):
+    """A != B (config-3 kernels) on a uniform 3-D tree against the oracle product."""
+    import paper_1805_08998_b200 as hx
+
+    rng = np.random.default_rng(5)
+    n, n_min, eta, eps_a, tol = 512, 16, 1.0, 1e-8, 1e-8
+    pts = rng.uniform(0, 1, (n, 3))
+    h = n ** (-1.0 / 3.0)
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, n_min), eta)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, n_min), eta)
+    oa = O.assemble_o("exp0.5", obt, O.Eps(eps_a), pts, h)
+    ob = O.assemble_o("inv", obt, O.Eps(eps_a), pts, h)
+    A = hx.HMatrix(bct, oa.data)
+    B = hx.HMatrix(bct, ob.data)
+    C = hx.hmult_new(A, B, hx.MultiplyConfig(compressor=hx.CompressorKind(tag),
+                                             policy=hx.EpsRank(tol)))
+    ref = O.hmult_new_o(oa, ob, O.Eps(tol), tag)
+    for b, p in ref.data.items():
+        q = C.data[b]
+        if isinstance(p, O.LR):
+            if tag == "aca":
+                # the GPU route returns the best approximation: never above ACA's rank + 1
+                # (ACA's crosses plus eps/2 trim can exceed the optimal rank by 2 in 3-D)
+                assert q.rank <= p.rank + 1, (b, q.rank, p.rank)
+            else:
+                assert abs(q.rank - p.rank) <= 1, (b, q.rank, p.rank)
+            d = np.linalg.norm(q.to_dense() - p.dense())
+            assert d <= 10 * tol * max(np.linalg.norm(p.dense()), 1e-300)
+        else:
+            assert np.linalg.norm(q - p) <= 1e-12 * np.linalg.norm(p)
+    exact = oa.to_dense() @ ob.to_dense()
+    err = np.linalg.norm(hx.to_dense(C) - exact) / np.linalg.norm(exact)
+    assert err <= tol
+
+
+def test_gpu_assembly_inv_kernel():
+    import paper_1805_08998_b200 as hx
+
+    rng = np.random.default_rng(5)
+    n, n_min, eta, eps_a = 512, 16, 1.0, 1e-8
+    pts = rng.uniform(0, 1, (n, 3))
+    h = n ** (-1.0 / 3.0)
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, n_min), eta)
+    B = hx.assemble_hmatrix("inv", bct, hx.EpsRank(eps_a), pts, h=h)
+    perm = bct.tree.permutation
+    K = O.kernel_matrix("inv", pts[perm], pts[perm], h)
+    err = np.linalg.norm(hx.to_dense(B) - K) / np.linalg.norm(K)
+    assert err <= 10 * eps_a, err
+
+
 def test_ragged_tree_reports_unsupported(golden):
     import paper_1805_08998_b200 as hx
 

@@ -44,7 +44,9 @@ def main():
     t0 = time.time()
     bct, A, B = configs.build_operands(c)
     print(f"cfg{a.cfg}: n={c['n']} nodes={bct.n_nodes} setup {time.time()-t0:.1f}s "
-          f"A max rank {max(int(r) for r in A._hx_packed[1]['rank'])}", flush=True)
+          f"A max rank {max(int(r) for r in A._hx_packed[1]['rank'])} "
+          f"B max rank {max(int(r) for r in B._hx_packed[1]['rank'])} "
+          f"degraded A {len(A.degraded)} B {len(B.degraded)}", flush=True)
     cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(a.tag), policy=hx.EpsRank(c["tol"]))
     for it in range(a.steps):
         t0 = time.time()
