@@ -177,6 +177,14 @@ int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tile
 int hx_ctx_synchronize(hx_ctx* ctx);
 /* Device memory available to the context (free + the workspace it already holds). */
 int hx_ctx_mem_info(hx_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes);
+
+/* Y = M X (transpose = 0) or M^T X (transpose = 1) for the H-matrix attached in operand
+ * slot `which` (0 or 1) of the context: X and Y are host n x s column-major blocks in
+ * tree ordering.  Replaces hmat_vec / hmat_vec_transpose / _node_matmat
+ * (pkg/src/hmat/hmatrix.py:138-211) for a block of s probe vectors at once; used to
+ * estimate ||C - A B|| of products too large to materialize. */
+int hx_hmatvec(hx_ctx* ctx, const hx_tree* tree, const hx_operand* op, int which,
+               int transpose, const double* X, double* Y, int s);
 void hx_ctx_free(hx_ctx* ctx);
 
 int hx_last_error(char* buf, size_t len);

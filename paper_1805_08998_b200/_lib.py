@@ -86,6 +86,8 @@ SIGNATURES = {
     "hx_pool_free": [C.c_void_p, C.c_void_p],
     "hx_ctx_synchronize": [C.c_void_p],
     "hx_ctx_mem_info": [C.c_void_p, i64p, i64p],
+    "hx_hmatvec": [C.c_void_p, C.POINTER(HxTree), C.POINTER(HxOperand), C.c_int, C.c_int,
+                   f64p, f64p, C.c_int],
     "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                       C.c_int64, C.POINTER(f64p), i64p, f64p, C.c_int64],
     "hx_ctx_free": [C.c_void_p],

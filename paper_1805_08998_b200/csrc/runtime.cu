@@ -934,6 +934,144 @@ extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const
   });
 }
 
+// H-matrix times a block of s vectors, Y = M X or M^T X (hmat_vec / _node_matmat,
+// hmatrix.py:138-202), for the operand in slot `which` of the context.  The same grouped
+// GEMM as the product: cores W_l = V_l^T X[sigma_l] stacked, then row bands of Y summing
+// U_l W_l and D_l X[sigma_l] over the leaves covering each band.
+extern "C" int hx_hmatvec(hx_ctx* c, const hx_tree* tree, const hx_operand* op, int which,
+                          int transpose, const double* X, double* Y, int s) {
+  return guarded([&]() -> int {
+    if (!c || !tree || !op || !X || !Y || s < 1 || which < 0 || which > 1)
+      return fail(HX_EINVAL, "bad arguments");
+    CK(cudaSetDevice(c->device));
+    cudaStream_t st = c->s;
+    const int64_t n = tree->c_hi[0] - tree->c_lo[0];
+    auto lo = [&](int cl) { return tree->c_lo[cl]; };
+    auto sz = [&](int cl) { return tree->c_hi[cl] - tree->c_lo[cl]; };
+    // input rows / output rows of a leaf
+    auto in_cl = [&](int b) { return transpose ? tree->tau[b] : tree->sigma[b]; };
+    auto out_cl = [&](int b) { return transpose ? tree->sigma[b] : tree->tau[b]; };
+    std::vector<int> lr, dn;
+    std::vector<int64_t> off;
+    int64_t srows = 0;
+    for (int b = 0; b < tree->n_nodes; ++b) {
+      if (tree->kind[b] == 0) continue;
+      if (op->payload[b] == 1) {
+        if (op->rank[b] == 0) continue;
+        lr.push_back(b);
+        off.push_back(srows);
+        srows += op->rank[b];
+      } else {
+        dn.push_back(b);
+      }
+    }
+    std::vector<Term> terms;
+    std::vector<Group> groups;
+    std::vector<Tile> tiles;
+    const int T = 64;
+    auto tiles_over = [&](uint8_t out_buf, int64_t R, int64_t C, int32_t gbase) {
+      for (int64_t i = 0, band = 0; i < R; i += T, ++band)
+        for (int64_t j = 0; j < C; j += T) {
+          Tile t;
+          std::memset(&t, 0, sizeof(t));
+          t.out_off = i + j * R;
+          t.out_ld = int32_t(R);
+          t.row0 = int32_t(i);
+          t.col0 = int32_t(j);
+          t.rows = int16_t(std::min<int64_t>(T, R - i));
+          t.cols = int16_t(std::min<int64_t>(T, C - j));
+          t.g_begin = gbase + int32_t(band);
+          t.g_end = t.g_begin + 1;
+          t.aux = -1;
+          t.out_buf = out_buf;
+          t.mode = MODE_STORE;
+          tiles.push_back(t);
+        }
+    };
+    // cores: S rows [off_l, off_l + k_l) = (V_l or U_l)^T X[in rows]
+    const int64_t nbs = (srows + T - 1) / T;
+    {
+      std::vector<std::vector<Term>> bands(static_cast<size_t>(nbs));
+      for (size_t q = 0; q < lr.size(); ++q) {
+        const int b = lr[q];
+        const int k = op->rank[b];
+        const int ic = in_cl(b);
+        const int64_t f = transpose ? op->u_off[b] : op->v_off[b];
+        const Term tm = mk(uint8_t(which), f, int32_t(sz(ic)), 1, BUF_GATHER, lo(ic), int32_t(n),
+                           1, int32_t(sz(ic)), k, s);
+        Term t2 = tm;
+        t2.r_lo = int32_t(off[q]);
+        for (int64_t bb = off[q] / T; bb <= (off[q] + k - 1) / T; ++bb) bands[size_t(bb)].push_back(t2);
+      }
+      for (auto& v : bands) {
+        groups.push_back(Group{int32_t(terms.size()), int32_t(terms.size() + v.size())});
+        terms.insert(terms.end(), v.begin(), v.end());
+      }
+      tiles_over(BUF_CORE, srows, s, 0);
+    }
+    const size_t core_tiles = tiles.size();
+    // Y bands
+    const int64_t nb = (n + T - 1) / T;
+    const int32_t gy = int32_t(groups.size());
+    {
+      std::vector<std::vector<Term>> bands(static_cast<size_t>(nb));
+      for (size_t q = 0; q < lr.size(); ++q) {
+        const int b = lr[q];
+        const int k = op->rank[b];
+        const int oc = out_cl(b);
+        const int64_t f = transpose ? op->v_off[b] : op->u_off[b];
+        const Term tm = mk(uint8_t(which), f, int32_t(sz(oc)), 0, BUF_CORE, off[q],
+                           int32_t(srows), 1, k, int32_t(sz(oc)), s);
+        Term t2 = tm;
+        t2.r_lo = int32_t(lo(oc));
+        for (int64_t bb = lo(oc) / T; bb <= (lo(oc) + sz(oc) - 1) / T; ++bb)
+          bands[size_t(bb)].push_back(t2);
+      }
+      for (int b : dn) {
+        const int oc = out_cl(b), ic = in_cl(b);
+        // D (tau x sigma, ld |tau|): forward P = D (i-contig), transpose P = D^T (k-contig)
+        Term t2 = mk(uint8_t(which), op->d_off[b], int32_t(sz(tree->tau[b])),
+                     uint8_t(transpose ? 1 : 0), BUF_GATHER, lo(ic), int32_t(n), 1,
+                     int32_t(sz(ic)), int32_t(sz(oc)), s);
+        t2.r_lo = int32_t(lo(oc));
+        for (int64_t bb = lo(oc) / T; bb <= (lo(oc) + sz(oc) - 1) / T; ++bb)
+          bands[size_t(bb)].push_back(t2);
+      }
+      for (auto& v : bands) {
+        groups.push_back(Group{int32_t(terms.size()), int32_t(terms.size() + v.size())});
+        terms.insert(terms.end(), v.begin(), v.end());
+      }
+      tiles_over(BUF_TERM, n, s, gy);
+    }
+    DArr<double> dx, dy, ds;
+    DArr<Term> dt;
+    DArr<Tile> dl;
+    DArr<Group> dg;
+    dx.upload(X, size_t(n) * s, st);
+    dy.ensure(size_t(n) * s);
+    ds.ensure(size_t(std::max<int64_t>(srows, 1)) * s);
+    dt.upload(terms, st);
+    dl.upload(tiles, st);
+    dg.upload(groups, st);
+    BufPtrs bp = c->ptrs();
+    bp.p[BUF_GATHER] = dx.p;
+    bp.p[BUF_CORE] = ds.p;
+    bp.p[BUF_TERM] = dy.p;
+    launch_gemm(c, 64, dl.p, dg.p, dt.p, int(core_tiles), bp, nullptr);
+    launch_gemm(c, 64, dl.p + core_tiles, dg.p, dt.p, int(tiles.size() - core_tiles), bp,
+                nullptr);
+    CK(cudaMemcpyAsync(Y, dy.p, size_t(n) * s * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    dx.release();
+    dy.release();
+    ds.release();
+    dt.release();
+    dl.release();
+    dg.release();
+    return HX_OK;
+  });
+}
+
 extern "C" int hx_ctx_mem_info(hx_ctx* c, int64_t* free_bytes, int64_t* total_bytes) {
   return guarded([&]() -> int {
     if (!c) return fail(HX_EINVAL, "null ctx");

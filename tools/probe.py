@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--tag", default="dense-svd")
     ap.add_argument("--check", action="store_true")
+    ap.add_argument("--estimate", type=int, default=0, help="probes of the GPU estimator")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     t0 = time.time()
@@ -62,6 +63,12 @@ def main():
     for m in np.unique(ms):
         rr = ranks[ms == m]
         print(f"  far {m}: n={len(rr)} rank {rr.min()}-{rr.max()} mean {rr.mean():.2f}")
+    if a.estimate:
+        from paper_1805_08998_b200.matvec import product_error
+        t0 = time.time()
+        est, cn = product_error(C, A, B, probes=a.estimate)
+        print(f"estimated ||C - AB||/||C|| = {est:.3e} ({a.estimate} probes, tol {c['tol']}) "
+              f"||C|| ~ {cn:.4e} check {time.time()-t0:.1f}s", flush=True)
     if a.check:
         import torch
         t0 = time.time()
