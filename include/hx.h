@@ -62,6 +62,16 @@ typedef struct hx_operand {
   const int64_t* d_off;    /* [n_nodes] element offset of dense payload              */
 } hx_operand;
 
+/* Pool offsets for an operand with the given payload kinds and ranks, in the panel order
+ * hx_assemble uses: left factors grouped by row cluster, right factors by column
+ * cluster, then the dense leaves.  The factors of the low-rank leaves of one block
+ * column (row) are then adjacent -- one column-major |sigma| x sum(k) matrix -- which the
+ * planner exploits to stack cores panel-wise.  Any other layout stays valid input to
+ * hx_plan_create (only slower).  Replaces the leaf-by-leaf storage of HMatrix.data
+ * (pkg/src/hmat/hmatrix.py:48-65) for the device pools. */
+int hx_operand_layout(const hx_tree* tree, const int8_t* payload, const int32_t* rank,
+                      int64_t* u_off, int64_t* v_off, int64_t* d_off, int64_t* pool_elems);
+
 typedef struct hx_plan hx_plan;
 typedef struct hx_ctx hx_ctx;
 
@@ -89,8 +99,10 @@ typedef struct hx_plan_info {
  * tile: CTA tile side (32 or 64).
  * flags: HX_PLAN_DEFER leaves the per-batch core / X G work lists to hx_product, which
  * fills them batch by batch while the device runs the previous batches; the caller's
- * tree / operand arrays must then stay alive until hx_product returns. */
+ * tree / operand arrays must then stay alive until hx_product returns.
+ * HX_PLAN_LOG keeps the restrict log for hx_plan_term_log (parity tests). */
 #define HX_PLAN_DEFER 1
+#define HX_PLAN_LOG 2
 int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
                    const uint8_t* leaf_mask, int tile, int flags, hx_plan** out);
 int hx_plan_info_get(const hx_plan* plan, hx_plan_info* info);
@@ -177,6 +189,9 @@ int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tile
 int hx_ctx_synchronize(hx_ctx* ctx);
 /* Device memory available to the context (free + the workspace it already holds). */
 int hx_ctx_mem_info(hx_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes);
+/* Release the product workspace (work lists, term/tile buffers, results not yet
+ * downloaded); operand pools stay attached. */
+int hx_ctx_trim(hx_ctx* ctx);
 
 /* Y = M X (transpose = 0) or M^T X (transpose = 1) for the H-matrix attached in operand
  * slot `which` (0 or 1) of the context: X and Y are host n x s column-major blocks in

@@ -86,6 +86,8 @@ SIGNATURES = {
     "hx_pool_free": [C.c_void_p, C.c_void_p],
     "hx_ctx_synchronize": [C.c_void_p],
     "hx_ctx_mem_info": [C.c_void_p, i64p, i64p],
+    "hx_ctx_trim": [C.c_void_p],
+    "hx_operand_layout": [C.POINTER(HxTree), i8p, i32p, i64p, i64p, i64p, i64p],
     "hx_hmatvec": [C.c_void_p, C.POINTER(HxTree), C.POINTER(HxOperand), C.c_int, C.c_int,
                    f64p, f64p, C.c_int],
     "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
@@ -158,6 +160,7 @@ class Plan:
     """Owning wrapper of an ``hx_plan``."""
 
     DEFER = 1  # HX_PLAN_DEFER: factor work lists filled by hx_product, batch by batch
+    LOG = 2    # HX_PLAN_LOG: keep the restrict log (term_log)
 
     def __init__(self, tree_arrays, opa, opb, leaf_mask=None, tile=64, flags=0):
         self.tree = TreeBuf(tree_arrays)

@@ -239,6 +239,7 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
                            int kernel, double h, double eps, int8_t* payload, int32_t* rank,
                            int64_t* u_off, int64_t* v_off, int64_t* d_off, int8_t* degraded,
                            double** pool_dev, int64_t* pool_elems) {
+  using hx::panel_layout;
   return guarded([&]() -> int {
     if (!c || !tree || !points || !payload || !rank || !u_off || !v_off || !d_off ||
         !degraded || !pool_dev || !pool_elems)
@@ -435,28 +436,21 @@ extern "C" int hx_assemble(hx_ctx* c, const hx_tree* tree, const double* points,
       f0 = f1;
     }
     ws.release();
-    // ---- final pool layout (leaf id order)
+    // ---- final pool layout: panel order (see panel_layout)
     std::vector<int> far_index(nn, -1);
     for (size_t f = 0; f < nf; ++f) far_index[far[f]] = int(f);
-    int64_t pos = 0;
     for (int b = 0; b < nn; ++b) {
       if (tree->kind[b] == 0) continue;
-      const int64_t m = sz(tree->tau[b]), n = sz(tree->sigma[b]);
       const int f = far_index[b];
       if (f >= 0 && !far_deg[f]) {
         payload[b] = 1;
         rank[b] = fin_rank[f];
-        u_off[b] = pos;
-        pos += a16(m * rank[b]);
-        v_off[b] = pos;
-        pos += a16(n * rank[b]);
       } else {
         payload[b] = 2;
-        d_off[b] = pos;
-        pos += a16(m * n);
         if (f >= 0) degraded[b] = 1;
       }
     }
+    const int64_t pos = panel_layout(tree, payload, rank, u_off, v_off, d_off);
     double* pool = nullptr;
     if (cudaMalloc(&pool, size_t(std::max<int64_t>(pos, 16)) * sizeof(double)) != cudaSuccess) {
       cudaGetLastError();

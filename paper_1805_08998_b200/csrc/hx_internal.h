@@ -95,6 +95,13 @@ void set_error(const std::string& msg);
 int fail(int code, const std::string& msg);
 void plan_fill_all(hx_plan* plan);
 
+// Operand pool offsets in panel order (payload and rank given): left factors grouped by
+// row cluster (ascending column start), right factors by column cluster (ascending row
+// start), then dense leaves; 16-element padding only at panel ends, so the factors of a
+// block row / column panel form one column-major matrix.  Returns the pool size.
+int64_t panel_layout(const hx_tree* tree, const int8_t* payload, const int32_t* rank,
+                     int64_t* u_off, int64_t* v_off, int64_t* d_off);
+
 template <class F>
 int guarded(F&& f) {
   try {
@@ -144,6 +151,7 @@ struct hx_plan {
   int64_t near_ws_begin = 0;  // near-leaf blocks sit after all far blocks in BUF_TILE
   int32_t n_sumsq = 0;
   std::vector<int32_t> log_block, log_a, log_b, log_rank;
+  bool logged = false;
   std::vector<int8_t> log_kind;
   hx_plan_info info;
 };

@@ -111,6 +111,7 @@ struct Builder {
   hx_plan& P;
   std::vector<uint8_t> owned_sub;
   hx::pvec<TRec> recs;
+  bool logging = false;  // HX_PLAN_LOG: keep the restrict log (parity tests)
 
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
@@ -215,11 +216,13 @@ struct Builder {
       o.terms.push_back(make_term(hx::BUF_A, A.u_off[pc], int32_t(m), 0, hx::BUF_TERM, -1,
                                   int32_t(n), 0, k, lo(tc), lo(sc), m, n));
     if (log_block >= 0) {
-      o.log_block.push_back(log_block);
-      o.log_kind.push_back(int8_t(kind_log));
-      o.log_a.push_back(pc);
-      o.log_b.push_back(qc);
-      o.log_rank.push_back(k);
+      if (logging) {
+        o.log_block.push_back(log_block);
+        o.log_kind.push_back(int8_t(kind_log));
+        o.log_a.push_back(pc);
+        o.log_b.push_back(qc);
+        o.log_rank.push_back(k);
+      }
       o.created[kind_log]++;
     }
     return k;
@@ -445,6 +448,7 @@ struct Builder {
 
   // --------------------------------------------------------------- merge of the outputs
   void merge(std::vector<Out>& outs) {
+    tg0 = std::chrono::steady_clock::now();
     const size_t no = outs.size();
     std::vector<int64_t> b_terms(no + 1, 0), b_tg(no + 1, 0), b_tiles(no + 1, 0),
         b_sumsq(no + 1, 0), b_far(no + 1, 0), b_near(no + 1, 0), b_recs(no + 1, 0),
@@ -468,6 +472,7 @@ struct Builder {
     ws_far_total = b_far[no];
     ws_near_total = b_near[no];
     P.n_sumsq = int32_t(b_sumsq[no]);
+    lap("merge alloc");
 #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t i = 0; i < int64_t(no); ++i) {
       const Out& o = outs[i];
@@ -503,9 +508,10 @@ struct Builder {
         P.leaves[size_t(b_leaves[i]) + l] = L;
       }
     }
+    lap("merge copy");
     // restrict log in the reference's visiting order: each subtree's log goes right after
     // the top-part entries logged before the subtree was deferred
-    {
+    if (logging) {
       const Out& top = outs[0];
       size_t pos = 0;
       auto append = [&](const Out& o, size_t a, size_t e) {
@@ -523,6 +529,7 @@ struct Builder {
       }
       append(top, pos, top.log_block.size());
     }
+    lap("merge log");
     hx_plan_info& I = P.info;
     for (const Out& o : outs) {
       I.n_terms_real += o.n_terms_real;
@@ -561,6 +568,56 @@ struct Builder {
   };
   std::vector<GInfo> G;
 
+  // Stacked-core layout of one X-group.  The low-rank leaves of X are ordered by their
+  // middle cluster (sigma_l on the A side, tau_l on the B side) and then by output rows;
+  // consecutive leaves sharing the middle cluster whose middle factors are adjacent in the
+  // pool (the panel layout of hx_assemble / pack_operand) form one run = one term
+  // [V_l1 .. V_lp]^T G[mid] of Sum k rows, so a 64-row core tile is filled by one panel
+  // instead of one 10-50-row leaf.  `idx` holds positions in g.leaves; soff[i] is the
+  // first stacked row of leaf g.leaves[i].
+  struct CoreRun {
+    int32_t first, count;  // range in idx
+    int64_t row, rows;     // stacked rows
+  };
+  void core_layout(const GInfo& g, const hx_operand& opX, std::vector<int32_t>& idx,
+                   std::vector<CoreRun>& runs, std::vector<int64_t>* soff) const {
+    idx.clear();
+    runs.clear();
+    const int nl = int(g.leaves.size());
+    for (int i = 0; i < nl; ++i) {
+      const int l = g.leaves[size_t(i)];
+      if (isF(opX, l) && opX.rank[l] > 0) idx.push_back(i);
+    }
+    auto mid = [&](int l) { return g.side == 0 ? t.sigma[l] : t.tau[l]; };
+    auto outc = [&](int l) { return g.side == 0 ? t.tau[l] : t.sigma[l]; };
+    auto midf = [&](int l) { return g.side == 0 ? opX.v_off[l] : opX.u_off[l]; };
+    std::sort(idx.begin(), idx.end(), [&](int32_t a, int32_t b) {
+      const int la = g.leaves[size_t(a)], lb = g.leaves[size_t(b)];
+      const int ma = mid(la), mb = mid(lb);
+      if (ma != mb) return ma < mb;
+      return lo(outc(la)) < lo(outc(lb));
+    });
+    if (soff) soff->assign(size_t(nl), -1);
+    int64_t row = 0;
+    for (int32_t j = 0; j < int32_t(idx.size()); ++j) {
+      const int l = g.leaves[size_t(idx[size_t(j)])];
+      const int kl = opX.rank[l];
+      bool ext = false;
+      if (!runs.empty()) {
+        const int p = g.leaves[size_t(idx[size_t(j - 1)])];
+        ext = mid(p) == mid(l) && midf(l) == midf(p) + sz(mid(p)) * int64_t(opX.rank[p]);
+      }
+      if (ext) {
+        runs.back().count++;
+        runs.back().rows += kl;
+      } else {
+        runs.push_back(CoreRun{j, 1, row, kl});
+      }
+      if (soff) (*soff)[size_t(idx[size_t(j)])] = row;
+      row += kl;
+    }
+  }
+
   static int64_t nbands(int64_t rows, int T) { return (rows + T - 1) / T; }
   static int64_t bands_hit(int64_t a, int64_t len, int64_t nb, int T) {
     const int64_t b0 = std::max<int64_t>(a / T, 0);
@@ -592,30 +649,68 @@ struct Builder {
     }
   }
 
+  bool verbose = std::getenv("HX_PLAN_VERBOSE") != nullptr;
+  std::chrono::steady_clock::time_point tg0;
+  void lap(const char* what) {
+    if (!verbose) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[hx plan]   %s %.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tg0).count());
+    tg0 = now;
+  }
+
   void build_groups() {
+    tg0 = std::chrono::steady_clock::now();
     const int nn = t.n_nodes;
     const size_t nr = recs.size();
     // counting sort of the terms by (side, X)
     std::vector<int32_t> cnt(2 * size_t(nn) + 1, 0);
     auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
-    for (const TRec& r : recs) cnt[key(r) + 1]++;
-    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-    order.assign(nr, 0);
+    // parallel counting sort: per-thread histograms over contiguous slices of recs, then
+    // (key, thread)-ordered offsets, so the order is the same as a sequential stable sort
+    const int nk = 2 * nn;
+    const int nth = std::max(1, std::min(omp_get_max_threads(), int(nr / 65536) + 1));
+    std::vector<int32_t> hist(size_t(nth) * size_t(nk), 0);
+    order.resize(nr);
+#pragma omp parallel num_threads(nth)
     {
-      std::vector<int32_t> pos(cnt.begin(), cnt.end() - 1);
-      for (size_t i = 0; i < nr; ++i) order[pos[key(recs[i])]++] = int32_t(i);
+      const int th = omp_get_thread_num();
+      const size_t a = nr * size_t(th) / size_t(nth), e = nr * size_t(th + 1) / size_t(nth);
+      int32_t* h = &hist[size_t(th) * size_t(nk)];
+      for (size_t i = a; i < e; ++i) h[key(recs[i])]++;
+#pragma omp barrier
+#pragma omp single
+      {
+        int32_t run = 0;
+        for (int k = 0; k < nk; ++k) {
+          cnt[size_t(k)] = run;
+          for (int q = 0; q < nth; ++q) {
+            int32_t& x = hist[size_t(q) * size_t(nk) + size_t(k)];
+            const int32_t c = x;
+            x = run;
+            run += c;
+          }
+        }
+        cnt[size_t(nk)] = run;
+      }
+      for (size_t i = a; i < e; ++i) order[size_t(h[key(recs[i])]++)] = int32_t(i);
     }
+    lap("order");
+    std::vector<int32_t> gpos(size_t(nk) + 1, 0);
+    for (int g = 0; g < nk; ++g) gpos[size_t(g) + 1] = gpos[size_t(g)] + (cnt[g] != cnt[g + 1]);
     G.clear();
-    for (int g = 0; g < 2 * nn; ++g) {
+    G.resize(size_t(gpos[size_t(nk)]));
+#pragma omp parallel for schedule(static)
+    for (int g = 0; g < nk; ++g) {
       if (cnt[g] == cnt[g + 1]) continue;
-      GInfo gi{};
+      GInfo& gi = G[size_t(gpos[size_t(g)])];
       gi.b0 = cnt[g];
       gi.b1 = cnt[g + 1];
       gi.side = int8_t(g >= nn ? 1 : 0);
       gi.X = g - gi.side * nn;
-      G.push_back(std::move(gi));
     }
     const int64_t ng = int64_t(G.size());
+    lap("sort");
     // pass 1 (parallel): leaves of X and work counts
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
@@ -643,18 +738,20 @@ struct Builder {
         g.n_fac_terms += bands_hit(lo(ol) - lo(g.rows_cl), sz(ol), nb, T);
       }
       const int64_t nbs = nbands(g.srows, T);
-      int64_t r = 0, terms = 0;
-      for (int l : g.leaves)
-        if (isF(opX, l) && opX.rank[l] > 0) {
-          terms += bands_hit(r, opX.rank[l], nbs, T);
-          r += opX.rank[l];
-        }
+      int64_t terms = 0;
+      {
+        thread_local std::vector<int32_t> idx;
+        thread_local std::vector<CoreRun> runs;
+        core_layout(g, opX, idx, runs, nullptr);
+        for (const CoreRun& cr : runs) terms += bands_hit(cr.row, cr.rows, nbs, T);
+      }
       g.n_core_terms = terms;
       g.n_core_groups = nbs;
       g.n_core_tiles = nbs * ct;
       g.n_fac_groups = nb;
       g.n_fac_tiles = nb * ct;
     }
+    lap("pass1");
     // pass 2 (sequential): batches and offsets
     int64_t gat_cur = 0, core_cur = 0;
     int64_t o_gather = 0, o_ct = 0, o_cg = 0, o_cm = 0, o_ft = 0, o_fg = 0, o_fm = 0;
@@ -726,6 +823,7 @@ struct Builder {
     P.fac_tiles.resize(size_t(o_ft));
     P.fac_groups.resize(size_t(o_fg));
     P.fac_terms.resize(size_t(o_fm));
+    lap("pass2");
     // pass 3 (parallel): gather records and the computed-factor offsets of the
     // materialization terms -- everything the materialization launch needs
 #pragma omp parallel for schedule(dynamic, 64)
@@ -752,6 +850,7 @@ struct Builder {
         col += r.k;
       }
     }
+    lap("pass3");
   }
 
   // pass 4 for one batch (parallel over its groups): stacked-core and X G work lists.
@@ -767,61 +866,77 @@ struct Builder {
       // (A side) or U_l^T G[rho_l] (B side)
       const int64_t nbs = nbands(g.srows, T);
       const int64_t nb = nbands(g.R, T);
+      thread_local std::vector<int32_t> idx;
+      thread_local std::vector<CoreRun> runs;
+      thread_local std::vector<int64_t> soff;
+      core_layout(g, opX, idx, runs, &soff);
       {
+        // runs ascend in stacked rows, so their (run, band) pieces come out band-sorted
         int64_t w = g.o_cm;
-        for (int64_t band = 0; band < nbs; ++band) {
-          const int64_t ba = band * T, be = std::min<int64_t>(g.srows, ba + T);
-          const int32_t tb = int32_t(w);
-          int64_t off = 0;
-          for (int l : g.leaves) {
-            if (!isF(opX, l) || opX.rank[l] == 0) continue;
-            const int kl = opX.rank[l];
-            if (off < be && off + kl > ba) {
-              const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];
-              const int64_t roff = lo(rl) - lo(g.rho);
-              const int64_t mid_f = g.side == 0 ? opX.v_off[l] : opX.u_off[l];
-              P.core_terms[size_t(w++)] =
-                  make_term(xbuf, mid_f, int32_t(sz(rl)), 1, hx::BUF_GATHER, g.gat + roff,
-                            int32_t(g.kr), 1, int32_t(sz(rl)), off, 0, kl, g.ktot);
-            }
-            off += kl;
+        int64_t band_next = 0;
+        for (const CoreRun& cr : runs) {
+          const int l = g.leaves[size_t(idx[size_t(cr.first)])];
+          const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];
+          const int64_t roff = lo(rl) - lo(g.rho);
+          const int64_t mid_f = g.side == 0 ? opX.v_off[l] : opX.u_off[l];
+          const Term tm = make_term(xbuf, mid_f, int32_t(sz(rl)), 1, hx::BUF_GATHER,
+                                    g.gat + roff, int32_t(g.kr), 1, int32_t(sz(rl)), cr.row, 0,
+                                    cr.rows, g.ktot);
+          for (int64_t band = cr.row / T; band <= (cr.row + cr.rows - 1) / T; ++band) {
+            while (band_next <= band)
+              P.core_groups[size_t(g.o_cg + band_next++)].t_begin = int32_t(w);
+            P.core_terms[size_t(w++)] = tm;
           }
-          P.core_groups[size_t(g.o_cg + band)] = Group{tb, int32_t(w)};
         }
+        while (band_next < nbs) P.core_groups[size_t(g.o_cg + band_next++)].t_begin = int32_t(w);
+        for (int64_t band = 0; band < nbs; ++band)
+          P.core_groups[size_t(g.o_cg + band)].t_end =
+              band + 1 < nbs ? P.core_groups[size_t(g.o_cg + band + 1)].t_begin : int32_t(w);
         write_band_tiles(&P.core_tiles[size_t(g.o_ct)], hx::BUF_CORE, g.core, g.srows, g.ktot, 0,
                          int32_t(g.o_cg));
       }
-      // row bands of X G (A side) / X^T G (B side)
+      // row bands of X G (A side) / X^T G (B side): count per band, then place (leaves in
+      // DFS order within a band)
       {
-        int64_t w = g.o_fm;
+        thread_local std::vector<int32_t> pos;
+        pos.assign(size_t(nb) + 1, 0);
+        const int nl = int(g.leaves.size());
+        const int64_t base = lo(g.rows_cl);
+        for (int i = 0; i < nl; ++i) {
+          const int l = g.leaves[size_t(i)];
+          if (isF(opX, l) && opX.rank[l] == 0) continue;
+          const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];
+          for (int64_t band = (lo(ol) - base) / T; band <= (lo(ol) + sz(ol) - 1 - base) / T;
+               ++band)
+            pos[size_t(band) + 1]++;
+        }
         for (int64_t band = 0; band < nb; ++band) {
-          const int64_t ba = lo(g.rows_cl) + band * T;
-          const int64_t be = std::min<int64_t>(lo(g.rows_cl) + g.R, ba + T);
-          const int32_t tb = int32_t(w);
-          int64_t off = 0;
-          for (int l : g.leaves) {
-            const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];  // middle-cluster part
-            const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];  // output rows
-            const bool lr = isF(opX, l);
-            const int kl = lr ? opX.rank[l] : 0;
-            if (lr && kl == 0) continue;
-            if (lo(ol) < be && lo(ol) + sz(ol) > ba) {
-              const int64_t roff = lo(rl) - lo(g.rho);
-              if (lr) {
-                const int64_t out_f = g.side == 0 ? opX.u_off[l] : opX.v_off[l];
-                P.fac_terms[size_t(w++)] =
-                    make_term(xbuf, out_f, int32_t(sz(ol)), 0, hx::BUF_CORE, g.core + off,
-                              int32_t(g.srows), 1, kl, lo(ol), 0, sz(ol), g.ktot);
-              } else {
-                P.fac_terms[size_t(w++)] =
-                    make_term(xbuf, opX.d_off[l], int32_t(sz(t.tau[l])),
-                              uint8_t(g.side == 0 ? 0 : 1), hx::BUF_GATHER, g.gat + roff,
-                              int32_t(g.kr), 1, int32_t(sz(rl)), lo(ol), 0, sz(ol), g.ktot);
-              }
-            }
-            off += kl;
+          pos[size_t(band) + 1] += pos[size_t(band)];
+          P.fac_groups[size_t(g.o_fg + band)] =
+              Group{int32_t(g.o_fm + pos[size_t(band)]), int32_t(g.o_fm + pos[size_t(band) + 1])};
+        }
+        for (int i = 0; i < nl; ++i) {
+          const int l = g.leaves[size_t(i)];
+          const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];  // middle-cluster part
+          const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];  // output rows
+          const bool lr = isF(opX, l);
+          const int kl = lr ? opX.rank[l] : 0;
+          if (lr && kl == 0) continue;
+          const int64_t roff = lo(rl) - lo(g.rho);
+          Term tm;
+          if (lr) {
+            const int64_t out_f = g.side == 0 ? opX.u_off[l] : opX.v_off[l];
+            tm = make_term(xbuf, out_f, int32_t(sz(ol)), 0, hx::BUF_CORE,
+                           g.core + soff[size_t(i)], int32_t(g.srows), 1, kl, lo(ol), 0, sz(ol),
+                           g.ktot);
+          } else {
+            tm = make_term(xbuf, opX.d_off[l], int32_t(sz(t.tau[l])),
+                           uint8_t(g.side == 0 ? 0 : 1), hx::BUF_GATHER, g.gat + roff,
+                           int32_t(g.kr), 1, int32_t(sz(rl)), lo(ol), 0, sz(ol), g.ktot);
           }
-          P.fac_groups[size_t(g.o_fg + band)] = Group{tb, int32_t(w)};
+          for (int64_t band = (lo(ol) - base) / T; band <= (lo(ol) + sz(ol) - 1 - base) / T;
+               ++band)
+            P.fac_terms[size_t(g.o_fm + pos[size_t(band)]++)] = tm;
         }
         write_band_tiles(&P.fac_tiles[size_t(g.o_ft)], hx::BUF_TERM, g.out, g.R, g.ktot,
                          lo(g.rows_cl), int32_t(g.o_fg));
@@ -903,9 +1018,15 @@ struct Builder {
                      std::chrono::duration<double, std::milli>(
                          std::chrono::steady_clock::now() - t0).count());
     }
+    const auto tm0 = std::chrono::steady_clock::now();
     merge(outs);
+    const auto tm1 = std::chrono::steady_clock::now();
     outs.clear();
     const auto t1 = std::chrono::steady_clock::now();
+    if (std::getenv("HX_PLAN_VERBOSE"))
+      std::fprintf(stderr, "[hx plan] merge %.1f ms, free %.1f ms\n",
+                   std::chrono::duration<double, std::milli>(tm1 - tm0).count(),
+                   std::chrono::duration<double, std::milli>(t1 - tm1).count());
     build_groups();
     const auto t2 = std::chrono::steady_clock::now();
     place_near();
@@ -933,6 +1054,8 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
     try {
       auto bld = std::make_shared<Builder>(plan->tree, plan->opa, plan->opb, leaf_mask, tile,
                                            *plan);
+      bld->logging = (flags & HX_PLAN_LOG) != 0;
+      plan->logged = bld->logging;
       bld->run();
       Builder* raw = bld.get();
       plan->builder = bld;
@@ -987,6 +1110,7 @@ extern "C" int hx_plan_leaves(const hx_plan* plan, int32_t* ids, int8_t* kind, i
 extern "C" int hx_plan_term_log(const hx_plan* plan, int32_t* block, int8_t* kind,
                                 int32_t* a_node, int32_t* b_node, int32_t* rank) {
   if (!plan) return hx::fail(HX_EINVAL, "null plan");
+  if (!plan->logged) return hx::fail(HX_EINVAL, "plan created without HX_PLAN_LOG");
   if (block) std::copy(plan->log_block.begin(), plan->log_block.end(), block);
   if (kind) std::copy(plan->log_kind.begin(), plan->log_kind.end(), kind);
   if (a_node) std::copy(plan->log_a.begin(), plan->log_a.end(), a_node);
@@ -1034,4 +1158,50 @@ extern "C" int hx_plan_mma_flops(hx_plan* plan, double* flops) {
     flops[3 + b] = u;
   }
   return HX_OK;
+}
+
+int64_t hx::panel_layout(const hx_tree* tree, const int8_t* payload, const int32_t* rank,
+                         int64_t* u_off, int64_t* v_off, int64_t* d_off) {
+  const int nn = tree->n_nodes;
+  auto lo = [&](int cl) { return tree->c_lo[cl]; };
+  auto sz = [&](int cl) { return tree->c_hi[cl] - tree->c_lo[cl]; };
+  std::vector<int> lr, dn;
+  for (int b = 0; b < nn; ++b) {
+    if (tree->kind[b] == 0) continue;
+    u_off[b] = v_off[b] = d_off[b] = 0;
+    (payload[b] == 1 ? lr : dn).push_back(b);
+  }
+  int64_t pos = 0;
+  // one factor region: leaves sorted by (panel cluster, start of the other cluster)
+  auto region = [&](const int32_t* panel, const int32_t* other, int64_t* off) {
+    std::vector<int> o(lr);
+    std::sort(o.begin(), o.end(), [&](int a, int b) {
+      if (panel[a] != panel[b]) return panel[a] < panel[b];
+      return lo(other[a]) < lo(other[b]);
+    });
+    for (size_t i = 0; i < o.size(); ++i) {
+      const int b = o[i];
+      off[b] = pos;
+      pos += sz(panel[b]) * int64_t(rank[b]);
+      if (i + 1 == o.size() || panel[o[i + 1]] != panel[b]) pos = align16(pos);
+    }
+  };
+  region(tree->tau, tree->sigma, u_off);
+  region(tree->sigma, tree->tau, v_off);
+  for (int b : dn) {
+    d_off[b] = pos;
+    pos = align16(pos + sz(tree->tau[b]) * sz(tree->sigma[b]));
+  }
+  return pos;
+}
+
+extern "C" int hx_operand_layout(const hx_tree* tree, const int8_t* payload, const int32_t* rank,
+                                 int64_t* u_off, int64_t* v_off, int64_t* d_off,
+                                 int64_t* pool_elems) {
+  if (!tree || !payload || !rank || !u_off || !v_off || !d_off || !pool_elems)
+    return hx::fail(HX_EINVAL, "null argument");
+  return hx::guarded([&]() -> int {
+    *pool_elems = hx::panel_layout(tree, payload, rank, u_off, v_off, d_off);
+    return HX_OK;
+  });
 }

@@ -462,6 +462,48 @@ extern "C" int hx_ctx_operand(hx_ctx* c, int which, const double* host, const do
   });
 }
 
+extern "C" int hx_ctx_trim(hx_ctx* c) {
+  return guarded([&]() -> int {
+    if (!c) return fail(HX_EINVAL, "null ctx");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->s));
+    CK(cudaStreamSynchronize(c->s2));
+    for (int i = BUF_TERM; i < NUM_BUFS; ++i) c->own[i].release();
+    for (int i = 0; i < 3; ++i) {
+      c->terms[i].release();
+      c->tiles[i].release();
+      c->groups[i].release();
+    }
+    c->sumsq.release();
+    c->fro2.release();
+    c->seg_b.release();
+    c->seg_e.release();
+    c->gather_recs.release();
+    c->rterms.release();
+    c->rtiles.release();
+    c->rgroups.release();
+    c->qr_jobs.release();
+    c->jac_jobs.release();
+    c->sel_jobs.release();
+    c->small_jobs.release();
+    c->rank_d.release();
+    c->retry_d.release();
+    c->rsum.release();
+    c->resid.release();
+    c->tb.release();
+    c->te.release();
+    for (auto& w : c->work) w.release();
+    c->omega_rows = 0;
+    c->omega_cols = 0;
+    c->omega_seed = ~0ULL;
+    c->out_far = c->near_begin = c->near_elems = 0;
+    c->res_rank.clear();
+    c->res_deg.clear();
+    c->res_off.clear();
+    return HX_OK;
+  });
+}
+
 extern "C" int hx_ctx_operand_alias(hx_ctx* c) {
   if (!c) return fail(HX_EINVAL, "null ctx");
   c->alias = true;

@@ -12,6 +12,8 @@ kind, rank, offsets) -- the ``hx_operand`` of ``include/hx.h``.
 
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
 
 from . import clustering
@@ -108,24 +110,22 @@ def pack_operand(h):
     v_off = np.zeros(nn, dtype=np.int64)
     d_off = np.zeros(nn, dtype=np.int64)
     leaves = np.flatnonzero(arr.kind_code != 0)
-    sizes = []
-    pos = 0
     for b in leaves:
         p = h.data[int(b)]
         if _is_lowrank(p):
-            m, k = p.left.shape
-            n = p.right.shape[0]
             payload[b] = 1
-            rank[b] = k
-            u_off[b] = pos
-            pos += (m * k + 15) & ~15
-            v_off[b] = pos
-            pos += (n * k + 15) & ~15
+            rank[b] = p.left.shape[1]
         else:
-            m, n = p.shape
             payload[b] = 2
-            d_off[b] = pos
-            pos += (m * n + 15) & ~15
+    # panel order of the device pools (hx_operand_layout, include/hx.h)
+    from . import _lib
+    tb = _lib.TreeBuf(tree_arrays(h.bct))
+    total = np.zeros(1, dtype=np.int64)
+    _lib.check(_lib.lib().hx_operand_layout(
+        C.byref(tb.st), _lib.ptr(payload, _lib.i8p), _lib.ptr(rank, _lib.i32p),
+        _lib.ptr(u_off, _lib.i64p), _lib.ptr(v_off, _lib.i64p), _lib.ptr(d_off, _lib.i64p),
+        _lib.ptr(total, _lib.i64p)), "hx_operand_layout")
+    pos = int(total[0])
     pool = np.zeros(max(pos, 16), dtype=np.float64)
     for b in leaves:
         p = h.data[int(b)]

@@ -29,7 +29,11 @@ def _attach(h, dev, slot, device):
         dev.set_operand(slot, dev_ptr=res[1], n=res[2])
     else:
         pool, d = _host_directory(h)
-        dev.set_operand(slot, pool=pool)
+        try:
+            dev.set_operand(slot, pool=pool)
+        except MemoryError:  # the last product's workspace still holds the device
+            _lib.check(_lib.lib().hx_ctx_trim(dev.h), "hx_ctx_trim")
+            dev.set_operand(slot, pool=pool)
     return d
 
 

@@ -39,7 +39,8 @@ def _plan_case(g, n_min_tile=None):
     A = O.assemble_o("exp", obt, O.Eps(eps_a), pts)
     H = hx.HMatrix(bct, A.data)
     pool, d = hmatrix.pack_operand(H)
-    plan = _lib.Plan(hmatrix.tree_arrays(bct), d, d, tile=multiply.plan_tile(bct))
+    plan = _lib.Plan(hmatrix.tree_arrays(bct), d, d, tile=multiply.plan_tile(bct),
+                     flags=_lib.Plan.LOG)
     return bct, A, plan, tol
 
 
