@@ -100,9 +100,15 @@ typedef struct hx_plan_info {
  * flags: HX_PLAN_DEFER leaves the per-batch core / X G work lists to hx_product, which
  * fills them batch by batch while the device runs the previous batches; the caller's
  * tree / operand arrays must then stay alive until hx_product returns.
- * HX_PLAN_LOG keeps the restrict log for hx_plan_term_log (parity tests). */
+ * HX_PLAN_LOG keeps the restrict log for hx_plan_term_log (parity tests).
+ * HX_PLAN_IMPLICIT(l): far leaves with min(m, n) >= 2^l are never materialized; hx_product
+ * sketches them straight from their terms (range pass Z = R^T Omega, Y = L Z; co-range
+ * W = L^T Q, B^T = R W) and estimates the unsampled tail from extra probe columns.  The
+ * route the canonical work model prices as "sketch". */
 #define HX_PLAN_DEFER 1
 #define HX_PLAN_LOG 2
+#define HX_PLAN_IMPLICIT_SHIFT 8
+#define HX_PLAN_IMPLICIT(l) ((int)(l) << HX_PLAN_IMPLICIT_SHIFT)
 int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
                    const uint8_t* leaf_mask, int tile, int flags, hx_plan** out);
 int hx_plan_info_get(const hx_plan* plan, hx_plan_info* info);

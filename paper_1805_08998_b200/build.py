@@ -13,7 +13,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["plan.cpp", "errors.cpp", "runtime.cu"]
 HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "dense_la.cuh", "dense_la_warp.cuh",
-           "assemble.cuh"]
+           "qr_rows.cuh", "gather_gemm.cuh", "assemble.cuh"]
 OUT = os.path.join(HERE, "libhx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

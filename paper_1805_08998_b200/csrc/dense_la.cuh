@@ -3,7 +3,7 @@
 // The reference truncates each far block with an exact SVD and the epsilon-rank rule
 // (dense_svd_compress, compressors.py:431-438; select_rank, lowrank.py:75-90).  Here each
 // CTA owns one block and runs, in shared memory when it fits (else in place in HBM/L2):
-//   qr_explicit_kernel  Householder QR (LAPACK dgeqr2 + dorg2r semantics), R saved, Q formed
+//   (Householder QR of the panels: qr_rows.cuh)
 //   jacobi_svd_kernel   one-sided (Hestenes) Jacobi SVD of the small q x q factor, parallel
 //                       round-robin pair ordering, singular values sorted descending
 //   select_rank_kernel  epsilon / fixed rank from the singular values plus the exact
@@ -65,92 +65,6 @@ __device__ double block_sum(double v, double* red) {
   const int nw = blockDim.x >> 5;
   for (int w = 0; w < nw; ++w) s += red[w];
   return s;
-}
-
-// Apply H = I - tau v v^T, v = (1, M[j+1:p, j]), to columns c0..q-1 of M (rows j..p-1).
-__device__ void apply_reflector(double* M, int ld, int p, int q, int j, int c0, double tau) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const double* v = M + int64_t(j) * ld;
-  for (int c = c0 + warp; c < q; c += nw) {
-    double* col = M + int64_t(c) * ld;
-    double w = 0.0;
-    for (int i = j + 1 + lane; i < p; i += 32) w += v[i] * col[i];
-    w = warp_sum(w) + col[j];
-    w *= tau;
-    if (lane == 0) col[j] -= w;
-    for (int i = j + 1 + lane; i < p; i += 32) col[i] -= w * v[i];
-  }
-}
-
-__device__ void householder_qr_explicit(double* M, int ld, int p, int q, double* Rout,
-                                        double* tau_s, double* red) {
-  // factor
-  for (int j = 0; j < q; ++j) {
-    double* x = M + int64_t(j) * ld;
-    double part = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) part += x[i] * x[i];
-    const double xn2 = block_sum(part, red);
-    const double alpha = x[j];
-    double tau, beta;
-    if (xn2 == 0.0) {
-      tau = 0.0;
-      beta = alpha;
-    } else {
-      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      const double scal = 1.0 / (alpha - beta);
-      for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) x[i] *= scal;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      x[j] = beta;
-      tau_s[j] = tau;
-    }
-    __syncthreads();
-    if (tau != 0.0) apply_reflector(M, ld, p, q, j, j + 1, tau);
-    __syncthreads();
-  }
-  // R (q x q, upper)
-  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
-    const int i = e % q, c = e / q;
-    Rout[e] = (i <= c) ? M[i + int64_t(c) * ld] : 0.0;
-  }
-  __syncthreads();
-  // explicit Q in place (dorg2r)
-  for (int j = q - 1; j >= 0; --j) {
-    const double tau = tau_s[j];
-    if (j < q - 1) {
-      if (threadIdx.x == 0) M[j + int64_t(j) * ld] = 1.0;
-      __syncthreads();
-      if (tau != 0.0) apply_reflector(M, ld, p, q, j, j + 1, tau);
-      __syncthreads();
-    }
-    double* x = M + int64_t(j) * ld;
-    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) x[i] *= -tau;
-    for (int i = threadIdx.x; i < j; i += blockDim.x) x[i] = 0.0;
-    if (threadIdx.x == 0) x[j] = 1.0 - tau;
-    __syncthreads();
-  }
-}
-
-// One CTA per job.  use_smem: copy X into dynamic shared memory (p*q doubles) first.
-__global__ void __launch_bounds__(LA_THREADS) qr_explicit_kernel(const QrJob* __restrict__ jobs,
-                                                                 int use_smem) {
-  extern __shared__ __align__(16) double dsm[];
-  __shared__ double tau_s[JAC_QMAX * 2];
-  __shared__ double red[LA_THREADS / 32];
-  const QrJob jb = jobs[blockIdx.x];
-  const int p = jb.p, q = jb.q;
-  if (use_smem) {
-    for (int64_t e = threadIdx.x; e < int64_t(p) * q; e += blockDim.x) dsm[e] = jb.X[e];
-    __syncthreads();
-    householder_qr_explicit(dsm, p, p, q, jb.R, tau_s, red);
-    __syncthreads();
-    for (int64_t e = threadIdx.x; e < int64_t(p) * q; e += blockDim.x) jb.X[e] = dsm[e];
-  } else {
-    householder_qr_explicit(jb.X, p, p, q, jb.R, tau_s, red);
-  }
 }
 
 // Round-robin (circle method) pairing: round r of qe-1, pair k of qe/2.
@@ -343,12 +257,13 @@ __global__ void __launch_bounds__(128) small_product_kernel(const SmallJob* __re
 }
 
 __global__ void segment_sum_kernel(const double* __restrict__ vals, const int* __restrict__ begin,
-                                   const int* __restrict__ end, double* __restrict__ out, int n) {
+                                   const int* __restrict__ end, double* __restrict__ out, int n,
+                                   double scale = 1.0) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   double s = 0.0;
   for (int i = begin[b]; i < end[b]; ++i) s += vals[i];
-  out[b] = s;
+  out[b] = s * scale;
 }
 
 }  // namespace hx

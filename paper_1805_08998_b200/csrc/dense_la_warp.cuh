@@ -3,8 +3,6 @@
 // The CTA kernels of dense_la.cuh spend most of their time in __syncthreads between the
 // q column steps of a QR and the q-1 rounds of every Jacobi sweep.  For small blocks one
 // warp owns one block and synchronises only with __syncwarp:
-//   warp_qr_kernel      Householder QR (dgeqr2 + dorg2r semantics, same as the CTA
-//                       kernel) of a p x q panel staged in shared memory (p <= 256, q <= 32)
 //   warp_jacobi_kernel  one-sided Jacobi SVD of a q x q factor, one column per lane held in
 //                       registers, partner columns exchanged with shuffles (q <= QM)
 #pragma once
@@ -13,90 +11,6 @@
 #include "dense_la.cuh"
 
 namespace hx {
-
-// Apply H = I - tau v v^T (v = (1, M[j+1:p, j])) to columns j+1..q-1 of M (ld), one
-// column per lane.
-__device__ __forceinline__ void warp_apply_reflector(double* M, int ld, int p, int q, int j,
-                                                     double tau, int lane) {
-  const double* v = M + j * ld;
-  for (int c = j + 1 + lane; c < q; c += 32) {
-    double* col = M + c * ld;
-    double w = col[j];
-    for (int i = j + 1; i < p; ++i) w += v[i] * col[i];
-    w *= tau;
-    col[j] -= w;
-    for (int i = j + 1; i < p; ++i) col[i] -= w * v[i];
-  }
-}
-
-// In-place Householder QR of M (p x q, column-major, ld) by one warp: R (q x q, ld q) is
-// written to Rout, M is overwritten by the explicit Q.
-__device__ void warp_householder_qr(double* M, int ld, int p, int q, double* Rout,
-                                    double* tau_s, int lane) {
-  for (int j = 0; j < q; ++j) {
-    double* x = M + j * ld;
-    double part = 0.0;
-    for (int i = j + 1 + lane; i < p; i += 32) part += x[i] * x[i];
-    const double xn2 = warp_sum(part);
-    const double alpha = x[j];
-    double tau, beta;
-    if (xn2 == 0.0) {
-      tau = 0.0;
-      beta = alpha;
-    } else {
-      beta = -copysign(hypot(alpha, sqrt(xn2)), alpha);
-      tau = (beta - alpha) / beta;
-      const double scal = 1.0 / (alpha - beta);
-      for (int i = j + 1 + lane; i < p; i += 32) x[i] *= scal;
-    }
-    __syncwarp();
-    if (lane == 0) {
-      x[j] = beta;
-      tau_s[j] = tau;
-    }
-    __syncwarp();
-    if (tau != 0.0) warp_apply_reflector(M, ld, p, q, j, tau, lane);
-    __syncwarp();
-  }
-  for (int e = lane; e < q * q; e += 32) {
-    const int i = e % q, c = e / q;
-    Rout[e] = (i <= c) ? M[i + c * ld] : 0.0;
-  }
-  __syncwarp();
-  for (int j = q - 1; j >= 0; --j) {
-    const double tau = tau_s[j];
-    if (j < q - 1) {
-      if (lane == 0) M[j + j * ld] = 1.0;
-      __syncwarp();
-      if (tau != 0.0) warp_apply_reflector(M, ld, p, q, j, tau, lane);
-      __syncwarp();
-    }
-    double* x = M + j * ld;
-    for (int i = j + 1 + lane; i < p; i += 32) x[i] *= -tau;
-    for (int i = lane; i < j; i += 32) x[i] = 0.0;
-    if (lane == 0) x[j] = 1.0 - tau;
-    __syncwarp();
-  }
-}
-
-// One warp per job; each warp stages its panel in its own slice of dynamic shared memory
-// (ld = p + 1: lanes walking different columns hit different banks).
-__global__ void warp_qr_kernel(const QrJob* __restrict__ jobs, int n_jobs, int slice) {
-  extern __shared__ __align__(16) double dsm[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jid = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (jid >= n_jobs) return;
-  const QrJob jb = jobs[jid];
-  const int p = jb.p, q = jb.q, ld = p + 1;
-  double* M = dsm + warp * slice;
-  double* tau_s = M + ld * q;
-  for (int c = 0; c < q; ++c)
-    for (int i = lane; i < p; i += 32) M[i + c * ld] = jb.X[i + int64_t(c) * p];
-  __syncwarp();
-  warp_householder_qr(M, ld, p, q, jb.R, tau_s, lane);
-  for (int c = 0; c < q; ++c)
-    for (int i = lane; i < p; i += 32) jb.X[i + int64_t(c) * p] = M[i + c * ld];
-}
 
 // One-sided Jacobi SVD of R (q x q, column-major) with lane c holding column c of R and of
 // V in registers.  Pairs follow the same round-robin (circle) ordering as the CTA kernel.

@@ -89,6 +89,10 @@ struct OutLeaf {
   int32_t sumsq_begin, sumsq_end;
   int64_t K;
   double fdd, edd;
+  // implicit route (far leaves with min(m, n) >= the plan's threshold): no tiles and no
+  // workspace; the leaf's terms are the groups [g_begin, g_end) of mat_groups
+  int8_t implicit;
+  int32_t g_begin, g_end;
 };
 
 void set_error(const std::string& msg);

@@ -112,6 +112,7 @@ struct Builder {
   std::vector<uint8_t> owned_sub;
   hx::pvec<TRec> recs;
   bool logging = false;  // HX_PLAN_LOG: keep the restrict log (parity tests)
+  int64_t implicit_min = 0;  // far leaves with min(m, n) >= this take the implicit route
 
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
@@ -316,16 +317,31 @@ struct Builder {
     L.K = K;
     L.fdd = fdd;
     L.edd = edd;
-    ws = align16(ws + m * n);
+    L.implicit = 0;
+    L.g_begin = L.g_end = -1;
     L.tile_begin = int32_t(o.tiles.size());
     L.sumsq_begin = o.n_sumsq;
+    // implicit route: the terms inherited from the root path (full-leaf extent, most of the
+    // stacked rank of a large leaf) are only sketched; the tiles materialize the sub-block
+    // terms of the leaf (pending-pair expansions, small extents) into T_sub
+    const bool impl = far && implicit_min > 0 && std::min(m, n) >= implicit_min;
+    if (impl) {
+      L.implicit = 1;
+      L.g_begin = int32_t(o.tile_groups.size());
+      o.tile_groups.insert(o.tile_groups.end(), w.path.begin(), w.path.end());
+      L.g_end = int32_t(o.tile_groups.size());
+    }
+    ws = align16(ws + m * n);
     int32_t prev_gb = -1, prev_ge = -1;
     std::vector<GRef> cur, prev;
     for (int64_t j = 0; j < n; j += T) {
       for (int64_t i = 0; i < m; i += T) {
         const int64_t r0 = lo(tc) + i, r1 = lo(tc) + std::min<int64_t>(m, i + T);
         const int64_t c0 = lo(sc) + j, c1 = lo(sc) + std::min<int64_t>(n, j + T);
-        cur.assign(w.path.begin(), w.path.end());
+        if (impl)
+          cur.clear();
+        else
+          cur.assign(w.path.begin(), w.path.end());
         for (const VGroup& v : vg)
           if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0) cur.push_back(v.g);
         int32_t gb, ge;
@@ -505,6 +521,10 @@ struct Builder {
         L.tile_end += int32_t(b_tiles[i]);
         L.sumsq_begin += int32_t(b_sumsq[i]);
         L.sumsq_end += int32_t(b_sumsq[i]);
+        if (L.implicit) {
+          L.g_begin += int32_t(b_tg[i]);
+          L.g_end += int32_t(b_tg[i]);
+        }
         P.leaves[size_t(b_leaves[i]) + l] = L;
       }
     }
@@ -1055,6 +1075,8 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
       auto bld = std::make_shared<Builder>(plan->tree, plan->opa, plan->opb, leaf_mask, tile,
                                            *plan);
       bld->logging = (flags & HX_PLAN_LOG) != 0;
+      const int ish = (flags >> HX_PLAN_IMPLICIT_SHIFT) & 31;
+      bld->implicit_min = ish ? (int64_t(1) << ish) : 0;
       plan->logged = bld->logging;
       bld->run();
       Builder* raw = bld.get();

@@ -22,7 +22,9 @@
 
 #include "dense_la.cuh"
 #include "dense_la_warp.cuh"
+#include "gather_gemm.cuh"
 #include "gemm.cuh"
+#include "qr_rows.cuh"
 #include "hx_internal.h"
 
 using namespace hx;
@@ -169,6 +171,17 @@ void pinned_free(void* p, size_t bytes) {
 }
 }  // namespace hx
 
+// One term of an implicit-route leaf, clipped to the leaf (leaf-local row / column ranges).
+struct ImplTerm {
+  Term t;         // the materialization term (global coordinates, see hx_types.h)
+  int lr;         // 1: factor pair (rows of Z / W gathered), 0: dense x dense (plain GEMM)
+  int k;
+  int ri, rn;     // leaf rows covered
+  int ci, cn;     // leaf columns covered
+  int64_t zrow;   // first row in the leaf's Z block (range pass)
+  int64_t wrow;   // first row in the leaf's W block (co-range pass)
+};
+
 struct FarBlock {
   int leaf;        // index into plan leaves
   int m, n, mu;
@@ -178,9 +191,61 @@ struct FarBlock {
   int rank = 0;
   int done = 0;
   int round = -1;
+  // implicit route: terms and the row count of their stacked Z / W blocks
+  int implicit = 0;
+  std::vector<ImplTerm> it;
+  int64_t zrows = 0;
+  int64_t zoff = 0;  // Z / W block in BUF_CORE for this round
   // pointers into that round's workspace
   double *Y = nullptr, *Bt = nullptr, *R = nullptr, *W = nullptr, *V = nullptr, *sig = nullptr;
+  double* C1 = nullptr;  // Q^T Y_probe (implicit route)
   double* fro2 = nullptr;
+};
+
+// Several grouped-GEMM batches built on the host and uploaded at once; batch i is the tile
+// range [cuts[i], cuts[i + 1]).
+struct GemmSet {
+  std::vector<Term> terms;
+  std::vector<Tile> tiles;
+  std::vector<Group> groups;
+  std::vector<size_t> cuts{0};
+  int32_t group(const Term* t, size_t n) {
+    const int32_t g = int32_t(groups.size());
+    groups.push_back(Group{int32_t(terms.size()), int32_t(terms.size() + n)});
+    terms.insert(terms.end(), t, t + n);
+    return g;
+  }
+  // tiles over an R x C output (ld) whose terms use coordinates (row0 + i, col0 + j)
+  void cover(int32_t g, uint8_t out_buf, int64_t out_off, int32_t ld, int R, int C, int row0,
+             int col0, uint8_t mode = MODE_STORE, int32_t* aux = nullptr) {
+    for (int j = 0; j < C; j += 64)
+      for (int i = 0; i < R; i += 64) {
+        Tile tl;
+        std::memset(&tl, 0, sizeof(tl));
+        tl.out_off = out_off + i + int64_t(j) * ld;
+        tl.out_ld = ld;
+        tl.row0 = row0 + i;
+        tl.col0 = col0 + j;
+        tl.rows = int16_t(std::min(64, R - i));
+        tl.cols = int16_t(std::min(64, C - j));
+        tl.g_begin = g;
+        tl.g_end = g + 1;
+        tl.aux = aux ? (*aux)++ : -1;
+        tl.out_buf = out_buf;
+        tl.mode = mode;
+        tiles.push_back(tl);
+      }
+  }
+  void cut() { cuts.push_back(tiles.size()); }
+  size_t count(int b) const { return cuts[size_t(b) + 1] - cuts[size_t(b)]; }
+};
+
+struct GatherSet {
+  std::vector<GTile> tiles;
+  std::vector<GSeg> segs;
+  std::vector<size_t> cuts{0};
+  void cut() { cuts.push_back(tiles.size()); }
+  size_t count(int b) const { return cuts[size_t(b) + 1] - cuts[size_t(b)]; }
 };
 
 struct hx_ctx {
@@ -206,7 +271,13 @@ struct hx_ctx {
   DArr<SmallJob> small_jobs;
   DArr<int> rank_d, retry_d;
   DArr<double> rsum, resid;  // explicit-tail sums of squares (per tile, per block)
-  DArr<int> tb, te;
+  DArr<double> esum, est;    // implicit route: probe residual sums (per tile, per block)
+  DArr<int> tb, te, eb, ee;
+  DArr<Term> xterms;         // one upload of all grouped-GEMM batches of a sketch round
+  DArr<Tile> xtiles;
+  DArr<Group> xgroups;
+  DArr<GTile> gtiles;        // row-gathered GEMM tiles / segments of a sketch round
+  DArr<GSeg> gsegs;
   std::vector<DArr<double>> work;  // one workspace per sketch round
   std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
   int64_t omega_rows = 0;
@@ -315,62 +386,85 @@ void run_gemm_batch(hx_ctx* c, std::vector<Term>& terms, std::vector<Tile>& tile
 
 // QR jobs: small panels (p <= 256, q <= 32) one warp each, others one CTA each (panel in
 // shared memory when it fits, else in place in HBM/L2).
+// Row-parallel Householder QR (qr_rows.cuh): panels up to QR_WARP_ROWS rows one warp each
+// (bucketed by height so that each launch sizes its smem slices tightly), taller ones one
+// CTA each, in shared memory when the panel fits.
+constexpr int QR_WARP_ROWS = 128;
+
+// Shared memory bounds occupancy here, so jobs are bucketed by their smem need (powers of
+// two) and every launch sizes its slices for its own bucket.
 void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
-  std::vector<QrJob> all;
-  all.reserve(jobs.size());
-  size_t smax = 0;
-  // warp jobs bucketed by panel height so that each launch sizes its smem slices tightly
-  const int pcls[3] = {64, 128, 256};
-  size_t wb[4] = {0, 0, 0, 0}, wslice[3] = {0, 0, 0};
-  for (int k = 0; k < 3; ++k) {
-    wb[k] = all.size();
-    for (const QrJob& j : jobs)
-      if (j.q <= 32 && j.p <= pcls[k] && (k == 0 || j.p > pcls[k - 1])) {
-        all.push_back(j);
-        wslice[k] = std::max(wslice[k], size_t(j.p + 1) * j.q + j.q);
-      }
-  }
-  wb[3] = all.size();
-  const size_t nw = all.size();
-  for (const QrJob& j : jobs) {
-    const size_t need = size_t(j.p) * j.q * sizeof(double);
-    if (!(j.p <= 256 && j.q <= 32) && need <= size_t(SMEM_CAP)) {
-      all.push_back(j);
-      smax = std::max(smax, need);
-    }
-  }
-  const size_t ns = all.size() - nw;
-  for (const QrJob& j : jobs) {
-    const size_t need = size_t(j.p) * j.q * sizeof(double);
-    if (!(j.p <= 256 && j.q <= 32) && need > size_t(SMEM_CAP)) all.push_back(j);
-  }
-  const size_t ng = all.size() - nw - ns;
-  if (all.empty()) return;
+  if (jobs.empty()) return;
+  auto slice_of = [](const QrJob& j) { return size_t(j.p) * j.q + j.q + 32; };  // doubles
+  auto warp_job = [&](const QrJob& j) {
+    return j.p <= QR_WARP_ROWS && slice_of(j) * sizeof(double) <= size_t(SMEM_CAP);
+  };
+  // register-resident kernel: q <= 32, p <= 256; key 192 + 4 (QM == 32) + log2(NW) with
+  // two rows per thread for QM = 16 and one for QM = 32
+  auto reg_job = [](const QrJob& j) { return j.q <= 32 && j.q <= j.p && j.p <= 256; };
+  auto lg_nw = [](int rows_per_warp, int p) {
+    int l = 0;
+    while ((rows_per_warp << l) < p) ++l;
+    return l;
+  };
+  // bucket key: kind (0 warp, 1 CTA smem, 2 CTA global) and log2 of the smem bytes
+  auto bucket = [&](const QrJob& j) {
+    if (reg_job(j)) return j.q > 16 ? 196 + lg_nw(32, j.p) : 192 + lg_nw(64, j.p);
+    const size_t need = warp_job(j) ? slice_of(j) * sizeof(double)
+                                    : size_t(j.p) * j.q * sizeof(double);
+    const int kind = warp_job(j) ? 0 : (need <= size_t(SMEM_CAP) ? 1 : 2);
+    int lg = 0;
+    while ((size_t(1) << lg) < need && lg < 40) ++lg;
+    return kind == 2 ? 2 * 64 : kind * 64 + lg;
+  };
+  std::vector<std::pair<int, int>> keyed(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) keyed[i] = {bucket(jobs[i]), int(i)};
+  std::sort(keyed.begin(), keyed.end());
+  std::vector<QrJob> all(jobs.size());
+  for (size_t i = 0; i < jobs.size(); ++i) all[i] = jobs[size_t(keyed[i].second)];
   c->qr_jobs.upload(all, c->s);
-  for (int k = 0; k < 3; ++k) {
-    const size_t n = wb[k + 1] - wb[k];
-    if (!n) continue;
-    const size_t per = wslice[k] * sizeof(double);
-    const int wpc = int(std::max<size_t>(1, std::min<size_t>(4, size_t(SMEM_CAP) / per)));
-    const size_t smem = per * size_t(wpc);
-    CK(cudaFuncSetAttribute(warp_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static bool attr = false;
+  if (!attr) {
+    CK(cudaFuncSetAttribute(qr_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(SMEM_CAP)));
-    warp_qr_kernel<<<int((n + wpc - 1) / wpc), 32 * wpc, smem, c->s>>>(c->qr_jobs.p + wb[k],
-                                                                     int(n), int(wslice[k]));
-    CK(cudaGetLastError());
-    c->launches++;
+    CK(cudaFuncSetAttribute(qr_rows_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(SMEM_CAP)));
+    attr = true;
   }
-  if (ns) {
-    CK(cudaFuncSetAttribute(qr_explicit_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            int(smax)));
-    qr_explicit_kernel<<<int(ns), LA_THREADS, smax, c->s>>>(c->qr_jobs.p + nw, 1);
+  for (size_t a = 0; a < all.size();) {
+    size_t e = a;
+    size_t need = 0;
+    while (e < all.size() && keyed[e].first == keyed[a].first) {
+      need = std::max(need, warp_job(all[e]) ? slice_of(all[e])
+                                             : size_t(all[e].p) * all[e].q);
+      ++e;
+    }
+    const int n = int(e - a);
+    const int kind = keyed[a].first / 64;
+    if (kind == 3) {
+      const QrJob* jp = c->qr_jobs.p + a;
+      switch (keyed[a].first - 192) {
+        case 0: qr_reg_kernel<1, 16, 2><<<n, 32, 0, c->s>>>(jp); break;
+        case 1: qr_reg_kernel<2, 16, 2><<<n, 64, 0, c->s>>>(jp); break;
+        case 2: qr_reg_kernel<4, 16, 2><<<n, 128, 0, c->s>>>(jp); break;
+        case 4: qr_reg_kernel<1, 32, 1><<<n, 32, 0, c->s>>>(jp); break;
+        case 5: qr_reg_kernel<2, 32, 1><<<n, 64, 0, c->s>>>(jp); break;
+        case 6: qr_reg_kernel<4, 32, 1><<<n, 128, 0, c->s>>>(jp); break;
+        default: qr_reg_kernel<8, 32, 1><<<n, 256, 0, c->s>>>(jp); break;
+      }
+    } else if (kind == 0) {
+      const size_t per = need * sizeof(double);
+      const int wpc = int(std::max<size_t>(1, std::min<size_t>(4, size_t(SMEM_CAP) / per)));
+      qr_rows_warp_kernel<<<(n + wpc - 1) / wpc, 32 * wpc, per * size_t(wpc), c->s>>>(
+          c->qr_jobs.p + a, n, int(need));
+    } else if (kind == 1) {
+      qr_rows_cta_kernel<<<n, LA_THREADS, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
+    } else {
+      qr_rows_cta_kernel<<<n, LA_THREADS, 0, c->s>>>(c->qr_jobs.p + a, 0);
+    }
     CK(cudaGetLastError());
     c->launches++;
-  }
-  if (ng) {
-    qr_explicit_kernel<<<int(ng), LA_THREADS, 0, c->s>>>(c->qr_jobs.p + nw + ns, 0);
-    CK(cudaGetLastError());
-    c->launches++;
+    a = e;
   }
 }
 
@@ -482,6 +576,13 @@ extern "C" int hx_ctx_trim(hx_ctx* c) {
     c->rterms.release();
     c->rtiles.release();
     c->rgroups.release();
+    c->xterms.release();
+    c->xtiles.release();
+    c->xgroups.release();
+    c->gtiles.release();
+    c->gsegs.release();
+    c->esum.release();
+    c->est.release();
     c->qr_jobs.release();
     c->jac_jobs.release();
     c->sel_jobs.release();
@@ -639,14 +740,148 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaGetLastError());
       c->launches++;
     }
+    // implicit-route leaves: their terms clipped to the leaf; Z rows ordered by column range
+    // (factor pairs first), W rows by row range, so that each gathered tile shares one range
+    int64_t zmax = 0;
+    for (FarBlock& f : fb) {
+      const OutLeaf& L = P->leaves[f.leaf];
+      if (!L.implicit) continue;
+      f.implicit = 1;
+      for (int32_t g = L.g_begin; g < L.g_end; ++g) {
+        const Group gr = P->mat_groups[g];
+        for (int32_t ti = gr.t_begin; ti < gr.t_end; ++ti) {
+          const Term& tm = P->mat_terms[ti];
+          if (tm.k <= 0) continue;
+          ImplTerm x;
+          x.t = tm;
+          x.k = tm.k;
+          x.lr = (tm.a_kc == 0 && tm.b_kc == 0) ? 1 : 0;
+          const int64_t r0 = std::max<int64_t>(tm.r_lo, L.row0);
+          const int64_t r1 = std::min<int64_t>(int64_t(tm.r_lo) + tm.rows, L.row0 + L.m);
+          const int64_t c0 = std::max<int64_t>(tm.c_lo, L.col0);
+          const int64_t c1 = std::min<int64_t>(int64_t(tm.c_lo) + tm.cols, L.col0 + L.n);
+          if (r1 <= r0 || c1 <= c0) continue;
+          x.ri = int(r0 - L.row0);
+          x.rn = int(r1 - r0);
+          x.ci = int(c0 - L.col0);
+          x.cn = int(c1 - c0);
+          f.it.push_back(x);
+        }
+      }
+      std::vector<int> o(f.it.size());
+      for (size_t i = 0; i < o.size(); ++i) o[i] = int(i);
+      std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
+        const ImplTerm &x = f.it[a], &y = f.it[b];
+        if (x.lr != y.lr) return x.lr > y.lr;
+        if (x.ci != y.ci) return x.ci < y.ci;
+        return x.cn < y.cn;
+      });
+      // rows of each term start at an even row (16-byte aligned k-contiguous reads)
+      int64_t r = 0;
+      for (int i : o) {
+        f.it[i].zrow = r;
+        r = (r + f.it[i].k + 1) & ~int64_t(1);
+      }
+      f.zrows = r;
+      std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
+        const ImplTerm &x = f.it[a], &y = f.it[b];
+        if (x.lr != y.lr) return x.lr > y.lr;
+        if (x.ri != y.ri) return x.ri < y.ri;
+        return x.rn < y.rn;
+      });
+      r = 0;
+      for (int i : o) {
+        f.it[i].wrow = r;
+        r = (r + f.it[i].k + 1) & ~int64_t(1);
+      }
+    }
+    (void)zmax;
+    if (std::getenv("HX_IMPL_STATS")) {
+      double full = 0, part = 0, part_area = 0, dd = 0, nl_impl = 0, full_terms = 0, part_terms = 0;
+      for (const FarBlock& f : fb) {
+        if (!f.implicit) continue;
+        nl_impl += 1;
+        for (const ImplTerm& x : f.it) {
+          if (!x.lr) { dd += x.k; continue; }
+          if (x.rn == f.m && x.cn == f.n) { full += x.k; full_terms += 1; }
+          else { part += x.k; part_area += double(x.k) * x.rn * x.cn; part_terms += 1; }
+        }
+      }
+      std::fprintf(stderr, "[hx impl] leaves %.0f: full-range rows %.0f (%.0f terms), partial rows "
+                   "%.0f (%.0f terms, mean area %.0f), dxd rows %.0f\n", nl_impl, full, full_terms,
+                   part, part_terms, part > 0 ? part_area / part : 0.0, dd);
+    }
+
+    // Rows of one gathered operand (segments in output-row order, kb / ke in B-row
+    // coordinates) packed into tiles of 64 consecutive output rows; a tile's K range is the
+    // union of its rows' ranges (rows are zero-filled outside their own).
+    auto gather_rows = [](GatherSet& gs, const std::vector<GSeg>& sg, uint8_t out_buf,
+                          int64_t out_off, int32_t out_ld, uint8_t b_buf, int64_t b_base,
+                          int32_t b_ld, int C) {
+      std::vector<GSeg> cur;
+      int rows = 0;
+      int64_t row_base = 0;
+      int kmin = 1 << 30, kmax = 0;
+      auto flush = [&]() {
+        if (!rows) return;
+        if (kmax <= kmin) kmin = kmax = 0;  // pad rows only
+        for (GSeg& x : cur) {
+          x.kb -= kmin;
+          x.ke -= kmin;
+        }
+        for (int j = 0; j < C; j += 64) {
+          GTile t;
+          std::memset(&t, 0, sizeof(t));
+          t.out_off = out_off + row_base + int64_t(j) * out_ld;
+          t.out_ld = out_ld;
+          t.b_off = b_base + kmin + int64_t(j) * b_ld;
+          t.b_ld = b_ld;
+          t.seg_begin = int32_t(gs.segs.size());
+          gs.segs.insert(gs.segs.end(), cur.begin(), cur.end());
+          t.seg_end = int32_t(gs.segs.size());
+          t.klen = kmax - kmin;
+          t.rows = int16_t(rows);
+          t.cols = int16_t(std::min(64, C - j));
+          t.out_buf = out_buf;
+          t.b_buf = b_buf;
+          gs.tiles.push_back(t);
+        }
+        row_base += rows;
+        rows = 0;
+        kmin = 1 << 30;
+        kmax = 0;
+        cur.clear();
+      };
+      for (GSeg x : sg) {
+        while (x.rows > 0) {
+          const int n = std::min<int>(x.rows, 64 - rows);
+          GSeg part = x;
+          part.rows = int16_t(n);
+          cur.push_back(part);
+          if (x.ke > x.kb) {  // pad segments (kb == ke) only write zero rows
+            kmin = std::min(kmin, x.kb);
+            kmax = std::max(kmax, x.ke);
+          }
+          rows += n;
+          x.off += int64_t(n) * x.ld;
+          x.rows = int16_t(x.rows - n);
+          if (rows == 64) flush();
+        }
+      }
+      flush();
+    };
+
+    constexpr int PR = 8;  // probe columns of the implicit route's tail estimate
     int64_t matvecs = 0;
     int rounds = 0;
     std::vector<int> active;
     for (int i = 0; i < int(fb.size()); ++i) active.push_back(i);
+    const bool explicit_tail = cfg->policy == 0 && cfg->eps < 1e-6;
     while (!active.empty()) {
       if (rounds >= 6) throw std::runtime_error("sketch adaptation did not converge");
+      auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
       // sketch widths for this round
-      int64_t wsz = 0;
+      int64_t wsz = 0, zsz = 0;
       for (int i : active) {
         FarBlock& f = fb[i];
         int l;
@@ -658,37 +893,54 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
           l = 2 * f.l;
         }
         l = std::min(l, f.mu);
-        if (l > lcap) {
-          if (f.mu <= lcap) l = f.mu;
-          else throw hx::Unsupported("block needs a sketch wider than " + std::to_string(lcap));
+        const int cap = f.implicit ? lcap - PR : lcap;
+        if (l > cap) {
+          if (f.mu <= cap) l = f.mu;
+          else throw hx::Unsupported("block needs a sketch wider than " + std::to_string(cap));
         }
         f.l = l;
-        f.dense = (f.m >= f.n && l == f.n) ? 1 : 0;
+        f.dense = (!f.implicit && f.m >= f.n && l == f.n) ? 1 : 0;
         f.round = rounds;
         const int64_t q = l;
-        wsz += (f.dense ? 0 : (int64_t(f.m) + f.n) * q) + 3 * q * q + q + 64;
+        if (f.implicit) {
+          wsz += a16(int64_t(f.m) * (q + PR)) + a16(int64_t(f.n) * q) + a16(q * PR);
+          f.zoff = zsz;
+          zsz += a16(f.zrows * (q + PR));
+        } else if (!f.dense) {
+          wsz += a16(int64_t(f.m) * q) + a16(int64_t(f.n) * q);
+        }
+        wsz += 3 * a16(q * q) + a16(q);
       }
       if (int(c->work.size()) <= rounds) c->work.resize(rounds + 1);
-      c->work[rounds].ensure(size_t(wsz));
+      c->work[rounds].ensure(size_t(std::max<int64_t>(wsz, 16)));
       double* wb = c->work[rounds].p;
       c->own[BUF_WORK].p = wb;  // buffer id BUF_WORK points at this round's workspace
+      if (zsz > 0) c->own[BUF_CORE].ensure(size_t(zsz));  // Z / W blocks (cores are dead)
       bp = c->ptrs();
       int64_t pos = 0;
       auto take = [&](int64_t nelem) {
         double* p = wb + pos;
-        pos += (nelem + 15) & ~int64_t(15);
+        pos += a16(nelem);
         return p;
       };
-      std::vector<Term> tt;
-      std::vector<Tile> tl;
-      std::vector<Group> tg;
-      std::vector<QrJob> qj;
+      auto woff = [&](const double* p) { return int64_t(p - wb); };
+      // every work list of the round is known up front: one upload, then launches in order
+      GemmSet gm;
+      GatherSet ga;
+      std::vector<QrJob> qy, qb;
+      std::vector<int> tail_b, tail_e, est_b, est_e;
+      int tail_slots = 0, est_slots = 0;
+      // -- batch 0 / gather 0: Z = R^T Omega of the implicit leaves
       for (int i : active) {
         FarBlock& f = fb[i];
         const int l = f.l;
         if (f.dense) {
           f.Y = c->buf(BUF_TILE) + f.t_off;  // QR in place of the materialized block
           f.Bt = nullptr;
+        } else if (f.implicit) {
+          f.Y = take(int64_t(f.m) * (l + PR));
+          f.Bt = take(int64_t(f.n) * l);
+          f.C1 = take(int64_t(l) * PR);
         } else {
           f.Y = take(int64_t(f.m) * l);
           f.Bt = take(int64_t(f.n) * l);
@@ -697,90 +949,228 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         f.W = take(int64_t(l) * l);
         f.V = take(int64_t(l) * l);
         f.sig = take(l);
-        if (!f.dense) {
-          // Y = T * Omega[:, :l]
-          single_term_tiles(tt, tl, tg,
-                            mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows),
-                               1, f.n, f.m, l),
-                            BUF_WORK, int64_t(f.Y - wb), f.m, l);
-          matvecs += 2 * l;
-        } else {
-          matvecs += f.n;
+        if (!f.implicit) continue;
+        const OutLeaf& L = P->leaves[f.leaf];
+        const int Lw = l + PR;
+        std::vector<GSeg> run;
+        int64_t have = 0;  // rows covered so far (pad segments fill the alignment gaps)
+        std::vector<int> o(f.it.size());
+        for (size_t q = 0; q < o.size(); ++q) o[q] = int(q);
+        std::sort(o.begin(), o.end(), [&](int a, int b) { return f.it[a].zrow < f.it[b].zrow; });
+        for (int q : o) {
+          const ImplTerm& x = f.it[q];
+          const Term& tm = x.t;
+          const int64_t jo = L.col0 + x.ci - tm.c_lo;  // first leaf column, term-local
+          if (x.lr) {
+            if (x.zrow > have)
+              run.push_back(GSeg{tm.b_off, 0, int16_t(x.zrow - have), tm.b_buf, 0, 0, 0});
+            have = x.zrow + x.k;
+            run.push_back(GSeg{tm.b_off + jo, tm.b_ld, int16_t(x.k), tm.b_buf, 0, x.ci,
+                               x.ci + x.cn});
+          } else {
+            // dense x dense: Z_t = D_B[:, cols] Omega[cols, :]
+            const Term z = mk(tm.b_buf, tm.b_off + jo * tm.b_ld, tm.b_ld, 0, BUF_OMEGA, x.ci,
+                              int32_t(c->omega_rows), 1, x.cn, x.k, Lw);
+            const int32_t g = gm.group(&z, 1);
+            gm.cover(g, BUF_CORE, f.zoff + x.zrow, int32_t(f.zrows), x.k, Lw, 0, 0);
+          }
         }
-        qj.push_back(QrJob{f.Y, f.R, f.m, f.dense ? f.n : l});
+        gather_rows(ga, run, BUF_CORE, f.zoff, int32_t(f.zrows), BUF_OMEGA, 0,
+                    int32_t(c->omega_rows), Lw);
+        matvecs += 2 * Lw;
       }
-      run_gemm_batch(c, tt, tl, tg);
-      run_qr(c, qj);
-      // Bt = T^T Q for sketched blocks, then QR(Bt)
-      tt.clear();
-      tl.clear();
-      tg.clear();
-      qj.clear();
+      gm.cut();  // gemm batch 0
+      ga.cut();  // gather batch 0
+      // -- batch 1: Y = T Omega (materialized) / Y = sum L_t Z_t (implicit)
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        const int l = f.l;
+        if (f.dense) {
+          matvecs += f.n;
+        } else if (f.implicit) {
+          const OutLeaf& L = P->leaves[f.leaf];
+          std::vector<Term> ts;
+          for (const ImplTerm& x : f.it) {
+            Term y = mk(x.t.a_buf, x.t.a_off, x.t.a_ld, x.t.a_kc, BUF_CORE, f.zoff + x.zrow,
+                        int32_t(f.zrows), 1, x.k, x.t.rows, l + PR);
+            y.r_lo = x.t.r_lo;
+            ts.push_back(y);
+          }
+          // + T_sub Omega (the materialized sub-block terms)
+          Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1, f.n,
+                      f.m, l + PR);
+          y.r_lo = int32_t(L.row0);
+          ts.push_back(y);
+          const int32_t g = gm.group(ts.data(), ts.size());
+          gm.cover(g, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0);
+        } else {
+          const Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
+                            f.n, f.m, l);
+          const int32_t g = gm.group(&y, 1);
+          gm.cover(g, BUF_WORK, woff(f.Y), f.m, f.m, l, 0, 0);
+          matvecs += 2 * l;
+        }
+        qy.push_back(QrJob{f.Y, f.R, f.m, f.dense ? f.n : l});
+      }
+      gm.cut();  // gemm batch 1
+      // -- batches 2, 3 (implicit): C1 = Q^T Y_probe; ||Y_probe - Q C1||^2 per tile
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        if (f.implicit) {
+          const int l = f.l;
+          const Term t1 = mk(BUF_WORK, woff(f.Y), f.m, 1, BUF_WORK, woff(f.Y) + int64_t(f.m) * l,
+                             f.m, 1, f.m, l, PR);
+          const int32_t g = gm.group(&t1, 1);
+          gm.cover(g, BUF_WORK, woff(f.C1), l, l, PR, 0, 0);
+        }
+      }
+      gm.cut();  // gemm batch 2
+      for (size_t a = 0; a < active.size(); ++a) {
+        FarBlock& f = fb[active[a]];
+        est_b.push_back(est_slots);
+        if (f.implicit) {
+          const int l = f.l;
+          const Term t2 = mk(BUF_WORK, woff(f.Y), f.m, 0, BUF_WORK, woff(f.C1), l, 1, l, f.m, PR);
+          const int32_t g = gm.group(&t2, 1);
+          gm.cover(g, BUF_WORK, woff(f.Y) + int64_t(f.m) * l, f.m, f.m, PR, 0, 0,
+                   MODE_RESID_SUMSQ, &est_slots);
+        }
+        est_e.push_back(est_slots);
+      }
+      gm.cut();  // gemm batch 3
+      // -- gather 1 + batch 4: W = L^T Q (implicit), rows sharing a row range
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        if (!f.implicit) continue;
+        const OutLeaf& L = P->leaves[f.leaf];
+        const int l = f.l;
+        std::vector<GSeg> run;
+        int64_t have = 0;  // rows covered so far (pad segments fill the alignment gaps)
+        std::vector<int> o(f.it.size());
+        for (size_t q = 0; q < o.size(); ++q) o[q] = int(q);
+        std::sort(o.begin(), o.end(), [&](int a, int b) { return f.it[a].wrow < f.it[b].wrow; });
+        for (int q : o) {
+          const ImplTerm& x = f.it[q];
+          const Term& tm = x.t;
+          const int64_t io = L.row0 + x.ri - tm.r_lo;  // first leaf row, term-local
+          if (x.lr) {
+            if (x.wrow > have)
+              run.push_back(GSeg{tm.a_off, 0, int16_t(x.wrow - have), tm.a_buf, 0, 0, 0});
+            have = x.wrow + x.k;
+            run.push_back(GSeg{tm.a_off + io, tm.a_ld, int16_t(x.k), tm.a_buf, 0, x.ri,
+                               x.ri + x.rn});
+          } else {
+            // dense x dense: W_t = D_A[rows, :]^T Q[rows, :]
+            const Term w = mk(tm.a_buf, tm.a_off + io, tm.a_ld, 1, BUF_WORK, woff(f.Y) + x.ri,
+                              f.m, 1, x.rn, x.k, l);
+            const int32_t g = gm.group(&w, 1);
+            gm.cover(g, BUF_CORE, f.zoff + x.wrow, int32_t(f.zrows), x.k, l, 0, 0);
+          }
+        }
+        gather_rows(ga, run, BUF_CORE, f.zoff, int32_t(f.zrows), BUF_WORK, woff(f.Y), f.m, l);
+      }
+      gm.cut();  // gemm batch 4
+      ga.cut();  // gather batch 1
+      // -- batch 5: Bt = T^T Q (materialized) / Bt = sum R_t W_t (implicit)
       for (int i : active) {
         FarBlock& f = fb[i];
         if (f.dense) continue;
-        single_term_tiles(tt, tl, tg,
-                          mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, int64_t(f.Y - wb), f.m, 1, f.m,
-                             f.n, f.l),
-                          BUF_WORK, int64_t(f.Bt - wb), f.n, f.l);
-        qj.push_back(QrJob{f.Bt, f.R, f.n, f.l});
-      }
-      if (!tl.empty()) CK(cudaStreamSynchronize(s));  // rterms reused
-      run_gemm_batch(c, tt, tl, tg);
-      // Tight tolerances: ||T||^2 - sum s_i^2 cancels below ~1e-15 ||T||^2, so the
-      // unsampled tail is measured directly as ||T - Q Bt^T||_F^2 (before QR(Bt)).
-      const bool explicit_tail = cfg->policy == 0 && cfg->eps < 1e-6;
-      std::vector<int> tail_b, tail_e;
-      if (explicit_tail) {
-        CK(cudaStreamSynchronize(s));  // rterms reused
-        tt.clear();
-        tl.clear();
-        tg.clear();
-        int slots = 0;
-        for (int i : active) {
-          FarBlock& f = fb[i];
-          tail_b.push_back(slots);
-          if (!f.dense) {
-            const int32_t g = int32_t(tg.size());
-            tg.push_back(Group{int32_t(tt.size()), int32_t(tt.size()) + 1});
-            tt.push_back(mk(BUF_WORK, int64_t(f.Y - wb), f.m, 0, BUF_WORK, int64_t(f.Bt - wb),
-                            f.n, 0, f.l, f.m, f.n));
-            for (int j = 0; j < f.n; j += 64)
-              for (int ii = 0; ii < f.m; ii += 64) {
-                Tile t;
-                std::memset(&t, 0, sizeof(t));
-                t.out_off = f.t_off + ii + int64_t(j) * f.m;
-                t.out_ld = f.m;
-                t.row0 = ii;
-                t.col0 = j;
-                t.rows = int16_t(std::min(64, f.m - ii));
-                t.cols = int16_t(std::min(64, f.n - j));
-                t.g_begin = g;
-                t.g_end = g + 1;
-                t.aux = slots++;
-                t.out_buf = BUF_TILE;
-                t.mode = MODE_RESID_SUMSQ;
-                tl.push_back(t);
-              }
+        const int l = f.l;
+        if (f.implicit) {
+          const OutLeaf& L = P->leaves[f.leaf];
+          std::vector<Term> ts;
+          for (const ImplTerm& x : f.it) {
+            // R_t(j, kk) = Q_t(kk, j)
+            Term y = mk(x.t.b_buf, x.t.b_off, x.t.b_ld, uint8_t(x.t.b_kc ? 1 : 0), BUF_CORE,
+                        f.zoff + x.wrow, int32_t(f.zrows), 1, x.k, x.t.cols, l);
+            y.r_lo = x.t.c_lo;
+            ts.push_back(y);
           }
-          tail_e.push_back(slots);
+          // + T_sub^T Q
+          Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
+          y.r_lo = int32_t(L.col0);
+          ts.push_back(y);
+          const int32_t g = gm.group(ts.data(), ts.size());
+          gm.cover(g, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0);
+        } else {
+          const Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
+          const int32_t g = gm.group(&y, 1);
+          gm.cover(g, BUF_WORK, woff(f.Bt), f.n, f.n, l, 0, 0);
         }
-        c->rsum.ensure(size_t(std::max(slots, 1)));
-        c->resid.ensure(size_t(std::max<size_t>(active.size(), 1)));
-        c->rterms.upload(tt, s);
-        c->rtiles.upload(tl, s);
-        c->rgroups.upload(tg, s);
-        launch_gemm(c, 64, c->rtiles.p, c->rgroups.p, c->rterms.p, int(tl.size()), c->ptrs(),
-                    c->rsum.p);
-        c->tb.upload(tail_b, s);
-        c->te.upload(tail_e, s);
-        const int na = int(active.size());
-        segment_sum_kernel<<<(na + 255) / 256, 256, 0, s>>>(c->rsum.p, c->tb.p, c->te.p,
-                                                            c->resid.p, na);
+        qb.push_back(QrJob{f.Bt, f.R, f.n, l});
+      }
+      gm.cut();  // gemm batch 5
+      // -- batch 6: tight tolerances, materialized blocks: ||T||^2 - sum s_i^2 cancels below
+      // ~1e-15 ||T||^2, so the unsampled tail is measured directly as ||T - Q Bt^T||_F^2
+      for (int i : active) {
+        FarBlock& f = fb[i];
+        tail_b.push_back(tail_slots);
+        if (explicit_tail && !f.dense && !f.implicit) {
+          const Term y = mk(BUF_WORK, woff(f.Y), f.m, 0, BUF_WORK, woff(f.Bt), f.n, 0, f.l, f.m,
+                            f.n);
+          const int32_t g = gm.group(&y, 1);
+          gm.cover(g, BUF_TILE, f.t_off, f.m, f.m, f.n, 0, 0, MODE_RESID_SUMSQ, &tail_slots);
+        }
+        tail_e.push_back(tail_slots);
+      }
+      gm.cut();  // gemm batch 6
+      // upload and run
+      const int na = int(active.size());
+      c->xterms.upload(gm.terms, s);
+      c->xtiles.upload(gm.tiles, s);
+      c->xgroups.upload(gm.groups, s);
+      if (!ga.tiles.empty()) {
+        c->gtiles.upload(ga.tiles, s);
+        c->gsegs.upload(ga.segs, s);
+      }
+      c->rsum.ensure(size_t(std::max(tail_slots, 1)));
+      c->resid.ensure(size_t(std::max(na, 1)));
+      c->esum.ensure(size_t(std::max(est_slots, 1)));
+      c->est.ensure(size_t(std::max(na, 1)));
+      auto gemm_batch = [&](int b, double* sums) {
+        const size_t n = gm.count(b);
+        if (n) launch_gemm(c, 64, c->xtiles.p + gm.cuts[size_t(b)], c->xgroups.p, c->xterms.p,
+                           int(n), bp, sums);
+      };
+      auto gather_batch = [&](int b) {
+        const size_t n = ga.count(b);
+        if (!n) return;
+        static bool gattr = false;
+        if (!gattr) {
+          CK(cudaFuncSetAttribute(gather_gemm_kernel<Gemm64>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm64::SMEM));
+          gattr = true;
+        }
+        gather_gemm_kernel<Gemm64><<<int(n), Gemm64::THREADS, Gemm64::SMEM, s>>>(
+            c->gtiles.p + ga.cuts[size_t(b)], c->gsegs.p, bp, int(n));
         CK(cudaGetLastError());
         c->launches++;
+      };
+      auto seg_sums = [&](const std::vector<int>& b, const std::vector<int>& e, DArr<int>& db,
+                          DArr<int>& de, const double* vals, double* out, double scale) {
+        db.upload(b, s);
+        de.upload(e, s);
+        segment_sum_kernel<<<(na + 255) / 256, 256, 0, s>>>(vals, db.p, de.p, out, na, scale);
+        CK(cudaGetLastError());
+        c->launches++;
+      };
+      gather_batch(0);
+      gemm_batch(0, nullptr);
+      gemm_batch(1, nullptr);
+      run_qr(c, qy);
+      if (est_slots) {
+        gemm_batch(2, nullptr);
+        gemm_batch(3, c->esum.p);
+        seg_sums(est_b, est_e, c->eb, c->ee, c->esum.p, c->est.p, 1.0 / PR);
       }
-      run_qr(c, qj);
+      gather_batch(1);
+      gemm_batch(4, nullptr);
+      gemm_batch(5, nullptr);
+      if (tail_slots) {
+        gemm_batch(6, c->rsum.p);
+        seg_sums(tail_b, tail_e, c->tb, c->te, c->rsum.p, c->resid.p, 1.0);
+      }
+      run_qr(c, qb);
       // SVD of the small factor
       std::vector<JacJob> jj;
       for (int i : active) {
@@ -792,13 +1182,14 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       std::vector<SelJob> sj;
       for (size_t a = 0; a < active.size(); ++a) {
         FarBlock& f = fb[active[a]];
-        const int exact = (f.dense || f.l == f.mu) ? 1 : 0;
-        if (explicit_tail && !exact)
+        const int exact = (f.dense || (!f.implicit && f.l == f.mu)) ? 1 : 0;
+        if (f.implicit)
+          sj.push_back(SelJob{f.sig, c->est.p + a, f.l, f.mu, 0, 1});
+        else if (explicit_tail && !exact)
           sj.push_back(SelJob{f.sig, c->resid.p + a, f.l, f.mu, 0, 1});
         else
           sj.push_back(SelJob{f.sig, f.fro2, f.l, f.mu, exact, 0});
       }
-      const int na = int(active.size());
       c->sel_jobs.upload(sj, s);
       c->rank_d.ensure(size_t(na));
       c->retry_d.ensure(size_t(na));

@@ -261,8 +261,21 @@ def default_chunks(bct, dev=None):
 
 # --------------------------------------------------------------------------- product
 
+IMPLICIT_MIN = 512  # far leaves with min(m, n) >= this are sketched without materialization
+
+
+def implicit_flags(implicit_min=None):
+    """HX_PLAN_IMPLICIT bits for a threshold (power of two; 0 disables; env HX_IMPLICIT)."""
+    if implicit_min is None:
+        implicit_min = int(os.environ.get("HX_IMPLICIT", IMPLICIT_MIN))
+    if implicit_min <= 0:
+        return 0
+    lg = int(np.ceil(np.log2(implicit_min)))
+    return (lg & 31) << 8
+
+
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
-                    device_operands=True, fetch=True, chunks=None):
+                    device_operands=True, fetch=True, chunks=None, implicit_min=None):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
@@ -314,6 +327,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     budget = 0.8 * float(fb.value) - 4e9
 
     plan_ms = [0.0]
+    iflags = implicit_flags(implicit_min)
 
     def make_plan(group):
         mask = group_mask(h.bct, group, leaf_mask) if (len(queue_all) > 1 or leaf_mask
@@ -323,7 +337,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         t0 = time.perf_counter()
         # deferred: the per-batch factor work lists are filled inside hx_product while the
         # device runs the previous batch
-        p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile, flags=_lib.Plan.DEFER)
+        p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile,
+                      flags=_lib.Plan.DEFER | iflags)
         plan_ms[0] += (time.perf_counter() - t0) * 1e3
         return p
 

@@ -48,6 +48,31 @@ def test_product_parity(golden, name, tag):
     bct, A, B, oa, ob, tol = _operands(g, name)
     cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(tag), policy=hx.EpsRank(tol))
     C = hx.hmult_new(A, B, cfg)
+    _check_parity(g, tag, bct, C, oa, ob, tol)
+
+
+@pytest.mark.parametrize("name,imin", [("small2d.npz", 32), ("cfg1.npz", 64),
+                                       ("cfg1.npz", 128)])
+def test_implicit_route_parity(golden, name, imin):
+    """Far blocks with min(m, n) >= imin are sketched straight from their terms (gathered
+    range / co-range passes, probe-column tail estimate) instead of being materialized;
+    the same parity contract as the materializing route."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import multiply
+
+    g = golden(name)
+    bct, A, B, oa, ob, tol = _operands(g, name)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    C = multiply.multiply_device(A, B, cfg, implicit_min=imin)
+    # some blocks took the route: it adds the gathered range / co-range launches
+    assert C.report.launches > multiply.multiply_device(A, B, cfg,
+                                                        implicit_min=0).report.launches
+    _check_parity(g, "dense-svd", bct, C, oa, ob, tol)
+
+
+def _check_parity(g, tag, bct, C, oa, ob, tol):
+    import paper_1805_08998_b200 as hx
+
     leaf_ids = g[f"{tag}/ids"]
     ranks_ref = g[f"{tag}/ranks"]
     fros_ref = g[f"{tag}/fros"]

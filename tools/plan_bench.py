@@ -44,6 +44,7 @@ def main():
     ap.add_argument("cfg", type=int)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fill", action="store_true", help="also fill every batch")
+    ap.add_argument("--sizes", action="store_true", help="materialization flops by leaf size")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     t0 = time.time()
@@ -61,6 +62,17 @@ def main():
             _lib.check(_lib.lib().hx_plan_mma_flops(p.h, _lib.ptr(mma, _lib.f64p)), "fill")
             msg += f" + fill/count {1e3 * (time.perf_counter() - t1):.1f} ms"
         print(msg, "terms", p.info.n_terms_real, p.info.n_terms_expand, flush=True)
+        if a.sizes:
+            lv = p.leaves()
+            for kind in (1, 2):
+                sel = lv["kind"] == kind
+                m, n, K, fdd = lv["m"][sel], lv["n"][sel], lv["K"][sel], lv["fdd"][sel]
+                for s in np.unique(m):
+                    q = m == s
+                    mat = (2.0 * m[q] * n[q] * K[q] + fdd[q]).sum()
+                    print(f"  {'far' if kind == 1 else 'near'} {s:5d}: {q.sum():6d} leaves "
+                          f"K mean {K[q].mean():7.1f} mat {mat / 1e9:8.1f} GF")
+            a.sizes = False
         p.close()
 
 
