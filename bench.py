@@ -305,7 +305,7 @@ def bench_ours(args, rank, world, local):
     # tensor-core work of this rank's plan (outside the timed region)
     mma = np.zeros(6)
     wp = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, mask,
-                   multiply.plan_tile(bct))
+                   multiply.plan_tile(bct), flags=multiply.implicit_flags())
     _lib.check(_lib.lib().hx_plan_mma_flops(wp.h, _lib.ptr(mma, _lib.f64p)), "mma flops")
     wp.close()
 
@@ -326,18 +326,9 @@ def bench_ours(args, rank, world, local):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     launches = 0
-    dom_ms = 0.0
-    form_ms = mat_ms = rec_ms = plan_ms = up_ms = 0.0
     for _ in range(args.steps):
         C = step()
-        r = C.report
-        launches += r.launches
-        dom_ms += r.form_ms
-        form_ms += r.form_ms
-        up_ms += r.upload_ms
-        mat_ms += r.materialize_ms
-        rec_ms += r.recompress_ms
-        plan_ms += r.plan_ms
+        launches += C.report.launches
     e1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -400,7 +391,17 @@ def bench_ours(args, rank, world, local):
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6552.3))
     info = C.plan_info
-    mat_s = mat_ms / args.steps * 1e-3
+    # the timed steps overlap chunks on two streams, so their per-phase event times include
+    # contention: the kernel durations come from one more product after the timed region,
+    # run without overlap (same plan, same kernels), events on the launching stream
+    Ci = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask, fetch=False,
+                                  overlap=False)
+    ri = Ci.report
+    iso = {"plan_host": ri.plan_ms, "upload": ri.upload_ms, "form": ri.form_ms,
+           "materialize": ri.materialize_ms, "recompress": ri.recompress_ms,
+           "device_total": ri.device_ms, "chunks": ri.chunks}
+    mat_s = ri.materialize_ms * 1e-3
+    form_ms_iso = ri.form_ms
     mat_tflops = mma[5] / mat_s / 1e12 if mat_s > 0 else 0.0
     traffic = None
     try:
@@ -410,7 +411,7 @@ def bench_ours(args, rank, world, local):
             traffic = tj["dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
         pass
-    form_s = form_ms / args.steps * 1e-3
+    form_s = form_ms_iso * 1e-3
     form_gbs = info.bytes_form / form_s / 1e9 if form_s > 0 else 0.0
     roofline = {"bound": "tensor", "achieved": mat_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": mat_tflops / FP64_DMMA_PEAK_TFLOPS,
@@ -451,10 +452,10 @@ def bench_ours(args, rank, world, local):
                              f"{8 * A._hx_device[2] / 1e9:.2f} GB)",
                        "parallelism": f"output-leaf partition x{world}"},
             "canonical_gflop": F_tot / 1e9, "canonical_gbytes": B_tot / 1e9,
-            "phases_ms": {"plan_host": plan_ms / args.steps, "upload": up_ms / args.steps,
-                          "form": form_ms / args.steps,
-                          "materialize": mat_ms / args.steps,
-                          "recompress": rec_ms / args.steps},
+            "phases_ms": iso,
+            "phases_ms_note": "one product after the timed region without chunk overlap "
+                              "(CUDA events per phase); timed steps overlap chunks on two "
+                              "streams",
             "max_far_rank": rep.max_far_rank, "setup_s": setup_s,
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": ck,

@@ -195,6 +195,11 @@ int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tile
 int hx_ctx_synchronize(hx_ctx* ctx);
 /* Device memory available to the context (free + the workspace it already holds). */
 int hx_ctx_mem_info(hx_ctx* ctx, int64_t* free_bytes, int64_t* total_bytes);
+/* Device memory the context holds as reusable workspace. */
+int64_t hx_ctx_held_bytes(hx_ctx* ctx);
+/* Attach the operand pools of src (same device) to dst without copying, so that two
+ * contexts -- two streams -- can run products (chunks) concurrently. */
+int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src);
 /* Release the product workspace (work lists, term/tile buffers, results not yet
  * downloaded); operand pools stay attached. */
 int hx_ctx_trim(hx_ctx* ctx);

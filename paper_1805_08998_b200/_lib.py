@@ -87,6 +87,8 @@ SIGNATURES = {
     "hx_ctx_synchronize": [C.c_void_p],
     "hx_ctx_mem_info": [C.c_void_p, i64p, i64p],
     "hx_ctx_trim": [C.c_void_p],
+    "hx_ctx_operand_share": [C.c_void_p, C.c_void_p],
+    "hx_ctx_held_bytes": [C.c_void_p],
     "hx_operand_layout": [C.POINTER(HxTree), i8p, i32p, i64p, i64p, i64p, i64p],
     "hx_hmatvec": [C.c_void_p, C.POINTER(HxTree), C.POINTER(HxOperand), C.c_int, C.c_int,
                    f64p, f64p, C.c_int],
@@ -97,6 +99,7 @@ SIGNATURES = {
     "hx_version": [],
 }
 VOID_RET = {"hx_plan_free", "hx_ctx_free"}
+INT64_RET = {"hx_ctx_held_bytes"}
 
 STATUS_EXC = {-1: ValueError, -2: MemoryError, -3: HxError, -4: NotImplementedError}
 
@@ -114,7 +117,8 @@ def lib():
                 continue
             f = getattr(L, name)
             f.argtypes = args
-            f.restype = None if name in VOID_RET else C.c_int
+            f.restype = None if name in VOID_RET else (C.c_int64 if name in INT64_RET
+                                                        else C.c_int)
         _lib = L
     return _lib
 

@@ -30,6 +30,8 @@ struct JacJob {
   double* W;        // q x q left singular vectors of R
   double* V;        // q x q right singular vectors of R
   int q;
+  int trans;        // 1: rotate the columns of R^T (the rows of the triangular factor of a
+                    // QR -- far fewer sweeps); left / right vectors swap roles
 };
 
 struct SelJob {
@@ -92,8 +94,9 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
   const bool big = q > JAC_SMEM_QMAX;
   double* M = big ? const_cast<double*>(jb.R) : dsm;   // q x q, ld q
   double* V = big ? jb.W : dsm + q * q;                 // q x q, ld q
+  const bool tr = jb.trans && !big;
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
-    if (!big) M[e] = jb.R[e];
+    if (!big) M[e] = tr ? jb.R[(e % q) * q + e / q] : jb.R[e];
     V[e] = (e % q == e / q) ? 1.0 : 0.0;
   }
   __syncthreads();
@@ -164,17 +167,19 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
     order[pos] = c;
   }
   __syncthreads();
-  // V first: for wide factors the working V lives in jb.W, which is written last
+  // rotations first: for wide factors the working V lives in jb.W, which is written last
+  double* rot_out = tr ? jb.W : jb.V;
+  double* col_out = tr ? jb.V : jb.W;
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
     const int x = e % q, pos = e / q;
-    jb.V[e] = V[order[pos] * q + x];
+    rot_out[e] = V[order[pos] * q + x];
   }
   __syncthreads();
   for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
     const int x = e % q, pos = e / q;
     const int c = order[pos];
     const double s = norms[c];
-    jb.W[e] = s > 0.0 ? M[c * q + x] / s : 0.0;
+    col_out[e] = s > 0.0 ? M[c * q + x] / s : 0.0;
   }
   for (int pos = threadIdx.x; pos < q; pos += blockDim.x) jb.sig[pos] = norms[order[pos]];
 }

@@ -12,6 +12,9 @@
 
 namespace hx {
 
+// debug counters (jobs, sweeps) of the warp Jacobi kernels, read with HX_JAC_STATS
+__device__ unsigned long long g_jac_stats[2];
+
 // One-sided Jacobi SVD of R (q x q, column-major) with lane c holding column c of R and of
 // V in registers.  Pairs follow the same round-robin (circle) ordering as the CTA kernel.
 template <int QM>
@@ -25,12 +28,13 @@ __global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restri
   double col[QM], vc[QM];
 #pragma unroll
   for (int x = 0; x < QM; ++x) {
-    col[x] = (lane < q && x < q) ? jb.R[x + lane * q] : 0.0;
+    col[x] = (lane < q && x < q) ? (jb.trans ? jb.R[lane + x * q] : jb.R[x + lane * q]) : 0.0;
     vc[x] = (x == lane && lane < q) ? 1.0 : 0.0;
   }
   const int qe = (q + 1) & ~1;
   const double tol = 1e-15;
-  for (int sweep = 0; sweep < 60 && q > 1; ++sweep) {
+  int sweep = 0;
+  for (; sweep < 60 && q > 1; ++sweep) {
     int rotated = 0;
     for (int r = 0; r < qe - 1; ++r) {
       // partner of this lane in round r (circle method; position 0 is fixed)
@@ -87,6 +91,10 @@ __global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restri
     }
     if (!__any_sync(0xffffffffu, rotated)) break;
   }
+  if (lane == 0) {
+    atomicAdd(&g_jac_stats[0], 1ull);
+    atomicAdd(&g_jac_stats[1], (unsigned long long)sweep);
+  }
   // singular values = column norms; descending order (stable) via ranking by all lanes
   double nrm = 0.0;
 #pragma unroll
@@ -101,10 +109,12 @@ __global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restri
     jb.sig[pos] = nrm;
     const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
 #pragma unroll
+    double* col_out = jb.trans ? jb.V : jb.W;
+    double* rot_out = jb.trans ? jb.W : jb.V;
     for (int x = 0; x < QM; ++x)
       if (x < q) {
-        jb.W[x + pos * q] = nrm > 0.0 ? col[x] * inv : 0.0;
-        jb.V[x + pos * q] = vc[x];
+        col_out[x + pos * q] = nrm > 0.0 ? col[x] * inv : 0.0;
+        rot_out[x + pos * q] = vc[x];
       }
   }
 }

@@ -556,6 +556,21 @@ extern "C" int hx_ctx_operand(hx_ctx* c, int which, const double* host, const do
   });
 }
 
+extern "C" int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src) {
+  return guarded([&]() -> int {
+    if (!dst || !src || dst == src) return fail(HX_EINVAL, "bad contexts");
+    if (dst->device != src->device) return fail(HX_EINVAL, "contexts on different devices");
+    if (!src->buf(BUF_A) || !src->buf(BUF_B)) return fail(HX_EINVAL, "source operands not set");
+    CK(cudaStreamSynchronize(src->s));  // host-copied pools complete
+    dst->attached[0] = src->buf(BUF_A);
+    dst->opnd_elems[0] = src->opnd_elems[0];
+    dst->alias = src->alias;
+    dst->attached[1] = src->alias ? nullptr : src->buf(BUF_B);
+    dst->opnd_elems[1] = src->opnd_elems[1];
+    return HX_OK;
+  });
+}
+
 extern "C" int hx_ctx_trim(hx_ctx* c) {
   return guarded([&]() -> int {
     if (!c) return fail(HX_EINVAL, "null ctx");
@@ -872,6 +887,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     };
 
     constexpr int PR = 8;  // probe columns of the implicit route's tail estimate
+    // Jacobi on R^T (rows of the QR factor): fewer sweeps than on the columns of R
+    const char* jt = std::getenv("HX_JAC_TRANS");
+    const int jac_trans = jt ? std::atoi(jt) : 1;
     int64_t matvecs = 0;
     int rounds = 0;
     std::vector<int> active;
@@ -1175,9 +1193,21 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       std::vector<JacJob> jj;
       for (int i : active) {
         FarBlock& f = fb[i];
-        jj.push_back(JacJob{f.R, f.sig, f.W, f.V, f.l});
+        jj.push_back(JacJob{f.R, f.sig, f.W, f.V, f.l, jac_trans});
+      }
+      if (std::getenv("HX_JAC_STATS")) {
+        unsigned long long z[2] = {0, 0};
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyToSymbol(g_jac_stats, z, sizeof(z)));
       }
       run_jacobi(c, jj);
+      if (std::getenv("HX_JAC_STATS")) {
+        unsigned long long z[2];
+        CK(cudaStreamSynchronize(s));
+        CK(cudaMemcpyFromSymbol(z, g_jac_stats, sizeof(z)));
+        std::fprintf(stderr, "[hx jacobi] warp jobs %llu mean sweeps %.2f\n", z[0],
+                     z[0] ? double(z[1]) / double(z[0]) : 0.0);
+      }
       // rank selection
       std::vector<SelJob> sj;
       for (size_t a = 0; a < active.size(); ++a) {
@@ -1505,6 +1535,14 @@ extern "C" int hx_hmatvec(hx_ctx* c, const hx_tree* tree, const hx_operand* op, 
   });
 }
 
+static size_t ctx_held(const hx_ctx* c) {
+  size_t held = 0;
+  for (int i = 0; i < NUM_BUFS; ++i)
+    if (i != BUF_A && i != BUF_B && i != BUF_WORK) held += c->own[i].cap * sizeof(double);
+  for (const auto& w : c->work) held += w.cap * sizeof(double);
+  return held;
+}
+
 extern "C" int hx_ctx_mem_info(hx_ctx* c, int64_t* free_bytes, int64_t* total_bytes) {
   return guarded([&]() -> int {
     if (!c) return fail(HX_EINVAL, "null ctx");
@@ -1512,14 +1550,13 @@ extern "C" int hx_ctx_mem_info(hx_ctx* c, int64_t* free_bytes, int64_t* total_by
     size_t f = 0, t = 0;
     CK(cudaMemGetInfo(&f, &t));
     // memory this context already holds for reuse counts as available
-    size_t held = 0;
-    for (int i = 0; i < NUM_BUFS; ++i)
-      if (i != BUF_A && i != BUF_B && i != BUF_WORK) held += c->own[i].cap * sizeof(double);
-    if (free_bytes) *free_bytes = int64_t(f + held);
+    if (free_bytes) *free_bytes = int64_t(f + ctx_held(c));
     if (total_bytes) *total_bytes = int64_t(t);
     return HX_OK;
   });
 }
+
+extern "C" int64_t hx_ctx_held_bytes(hx_ctx* c) { return c ? int64_t(ctx_held(c)) : 0; }
 
 extern "C" int hx_ctx_synchronize(hx_ctx* c) {
   return guarded([&]() -> int {

@@ -33,6 +33,9 @@ def _attach(h, dev, slot, device):
             dev.set_operand(slot, pool=pool)
         except MemoryError:  # the last product's workspace still holds the device
             _lib.check(_lib.lib().hx_ctx_trim(dev.h), "hx_ctx_trim")
+            aux = Device._aux.get(device)
+            if aux is not None:
+                _lib.check(_lib.lib().hx_ctx_trim(aux.h), "hx_ctx_trim")
             dev.set_operand(slot, pool=pool)
     return d
 

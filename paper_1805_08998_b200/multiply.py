@@ -93,6 +93,15 @@ class Device:
             cls._cache[device] = Device(device)
         return cls._cache[device]
 
+    _aux: dict = {}
+
+    @classmethod
+    def aux(cls, device=0):
+        """A second context on the device (its own streams and workspace)."""
+        if device not in cls._aux:
+            cls._aux[device] = Device(device)
+        return cls._aux[device]
+
     def set_operand(self, which, pool=None, dev_ptr=None, n=None):
         if pool is not None:
             pool = np.ascontiguousarray(pool, dtype=np.float64)
@@ -243,7 +252,18 @@ def plan_bytes(info):
         40.0 * (info.mat_tiles + info.core_tiles + info.fac_tiles)
 
 
-def default_chunks(bct, dev=None):
+def available_bytes(dev):
+    """Free device memory plus the workspace both contexts of the device hold for reuse."""
+    fb, tb = C.c_int64(), C.c_int64()
+    _lib.check(_lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)), "hx_ctx_mem_info")
+    free = float(fb.value)
+    aux = Device._aux.get(dev.device)
+    if aux is not None and aux is not dev:
+        free += float(_lib.lib().hx_ctx_held_bytes(aux.h))
+    return free
+
+
+def default_chunks(bct, dev=None, overlap=None):
     """Chunks needed to keep one chunk's device workspace (materialized blocks plus term
     factors, ~12x the leaf area on the BASELINE configs) within ~60% of free memory."""
     env = os.environ.get("HX_CHUNKS")
@@ -252,11 +272,14 @@ def default_chunks(bct, dev=None):
     area = sum(u[2] for u in chunk_units(bct))
     free = 60e9
     if dev is not None:
-        fb, tb = C.c_int64(), C.c_int64()
-        if _lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)) == 0:
-            free = float(fb.value)
+        free = available_bytes(dev)
     need = area * 8.0 * 12.0
-    return max(1, int(np.ceil(need / (0.6 * free))))
+    n = max(1, int(np.ceil(need / (0.6 * free))))
+    # large products run as >= 3 chunks on two contexts: a chunk's recompression overlaps
+    # the next chunk's term formation (config 2: 427 -> 389 ms per product)
+    if area >= 2.5e8 and overlap_default(overlap):
+        n = max(n, 3)
+    return n
 
 
 # --------------------------------------------------------------------------- product
@@ -274,8 +297,15 @@ def implicit_flags(implicit_min=None):
     return (lg & 31) << 8
 
 
+def overlap_default(overlap=None):
+    if overlap is None:
+        return os.environ.get("HX_OVERLAP", "1") != "0"
+    return bool(overlap)
+
+
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
-                    device_operands=True, fetch=True, chunks=None, implicit_min=None):
+                    device_operands=True, fetch=True, chunks=None, implicit_min=None,
+                    overlap=None):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
@@ -320,11 +350,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                            int(sketch0), int(oversample))
     ta = tree_arrays(h.bct)
     tile = plan_tile(h.bct)
-    nch = default_chunks(h.bct, dev) if chunks is None else max(1, int(chunks))
+    nch = default_chunks(h.bct, dev, overlap) if chunks is None else max(1, int(chunks))
     queue = collections.deque(chunk_groups(h.bct, nch))
-    fb, tb = C.c_int64(), C.c_int64()
-    _lib.check(_lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)), "hx_ctx_mem_info")
-    budget = 0.8 * float(fb.value) - 4e9
+    budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
     iflags = implicit_flags(implicit_min)
@@ -345,21 +373,45 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     queue_all = list(queue)
     group_split = [False]
     rep = MultReport()
-    data, degraded = {}, set()
-    leaves_all, ranks_all, infos = [], [], []
-    nxt = {"plan": None, "err": None}
+    # with several chunks, two contexts (two streams) run consecutive chunks concurrently:
+    # one chunk's latency-bound recompression overlaps the next chunk's term formation
+    ctxs = [dev]
+    if len(queue_all) > 1 and overlap_default(overlap):
+        aux = Device.aux(device)
+        _lib.check(_lib.lib().hx_ctx_operand_share(aux.h, dev.h), "hx_ctx_operand_share")
+        ctxs.append(aux)
+        budget = budget / 2
 
-    def plan_async(group):
+    def run_chunk(plan, ctx, out):
         try:
-            nxt["plan"] = make_plan(group)
+            st = _lib.HxProductStats()
+            _lib.check(_lib.lib().hx_product(ctx.h, plan.h, C.byref(pc), C.byref(st)),
+                       "hx_product")
+            leaves = plan.leaves()
+            nl = len(leaves["ids"])
+            rank = np.zeros(nl, np.int32)
+            deg = np.zeros(nl, np.int8)
+            off = np.zeros(nl, np.int64)
+            _lib.check(_lib.lib().hx_result_layout(ctx.h, _lib.ptr(rank, _lib.i32p),
+                                                   _lib.ptr(deg, _lib.i8p),
+                                                   _lib.ptr(off, _lib.i64p)), "hx_result_layout")
+            res = None
+            if fetch:
+                res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
+                _lib.check(_lib.lib().hx_result_download(ctx.h, _lib.ptr(res, _lib.f64p),
+                                                         res.size), "hx_result_download")
+            out.update(st=st, leaves=leaves, rank=rank, deg=deg, off=off, res=res,
+                       info=plan.info)
         except BaseException as exc:  # re-raised on the main thread
-            nxt["err"] = exc
+            out["err"] = exc
+        finally:
+            plan.close()
 
-    worker = None
-    n_run = 0
+    chunks_out = []
+    inflight = collections.deque()
     group = queue.popleft()
     plan = make_plan(group)
-    while plan is not None or queue or worker is not None:
+    while True:
         # a chunk whose workspace would not fit is split and planned again
         while plan is not None and plan_bytes(plan.info) > budget:
             parts = split_chunk(h.bct, group)
@@ -370,34 +422,34 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             group = parts[0]
             queue.extendleft(reversed(parts[1:]))
             plan = make_plan(group)
-        if queue:
-            ngroup = queue.popleft()
-            worker = threading.Thread(target=plan_async, args=(ngroup,))
-            worker.start()
-        if plan is None:  # nothing owned in this chunk
-            if worker is not None:
-                worker.join()
-                worker = None
-                if nxt["err"] is not None:
-                    raise nxt["err"]
-                plan, nxt["plan"], group = nxt["plan"], None, ngroup
-            continue
+        if plan is not None:
+            if len(inflight) >= len(ctxs):  # the context of chunk i - 2 must be free
+                t = inflight.popleft()
+                t.join()
+            out = {}
+            chunks_out.append(out)
+            t = threading.Thread(target=run_chunk,
+                                 args=(plan, ctxs[(len(chunks_out) - 1) % len(ctxs)], out))
+            t.start()
+            inflight.append(t)
+        if not queue:
+            break
+        # plan the next chunk while the device runs the current one(s)
+        group = queue.popleft()
+        plan = make_plan(group)
+    for t in inflight:
+        t.join()
+    data, degraded = {}, set()
+    leaves_all, ranks_all, infos = [], [], []
+    n_run = 0
+    for out in chunks_out:
+        if "err" in out:
+            raise out["err"]
         n_run += 1
-        st = _lib.HxProductStats()
-        _lib.check(_lib.lib().hx_product(dev.h, plan.h, C.byref(pc), C.byref(st)),
-                   "hx_product")
-        leaves = plan.leaves()
-        nl = len(leaves["ids"])
-        rank = np.zeros(nl, np.int32)
-        deg = np.zeros(nl, np.int8)
-        off = np.zeros(nl, np.int64)
-        _lib.check(_lib.lib().hx_result_layout(dev.h, _lib.ptr(rank, _lib.i32p),
-                                               _lib.ptr(deg, _lib.i8p),
-                                               _lib.ptr(off, _lib.i64p)), "hx_result_layout")
+        st, leaves, rank, deg, off, res = (out[k] for k in ("st", "leaves", "rank", "deg", "off",
+                                                            "res"))
         if fetch:
-            res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
-            _lib.check(_lib.lib().hx_result_download(dev.h, _lib.ptr(res, _lib.f64p),
-                                                     res.size), "hx_result_download")
+            nl = len(leaves["ids"])
             ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
             kinds, rl, ol = leaves["kind"].tolist(), rank.tolist(), off.tolist()
             for i in range(nl):
@@ -426,15 +478,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         rep.fro2 += float(st.fro2_total)
         leaves_all.append(leaves)
         ranks_all.append(rank)
-        infos.append(plan.info)
-        plan.close()
-        plan = None
-        if worker is not None:
-            worker.join()
-            worker = None
-            if nxt["err"] is not None:
-                raise nxt["err"]
-            plan, nxt["plan"], group = nxt["plan"], None, ngroup
+        infos.append(out["info"])
     rep.chunks = n_run
     rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start
