@@ -395,7 +395,7 @@ def bench_ours(args, rank, world, local):
     # contention: the kernel durations come from one more product after the timed region,
     # run without overlap (same plan, same kernels), events on the launching stream
     Ci = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask, fetch=False,
-                                  overlap=False)
+                                  chunks=C.report.chunks, overlap=False)
     ri = Ci.report
     iso = {"plan_host": ri.plan_ms, "upload": ri.upload_ms, "form": ri.form_ms,
            "materialize": ri.materialize_ms, "recompress": ri.recompress_ms,

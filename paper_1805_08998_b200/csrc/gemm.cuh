@@ -176,6 +176,30 @@ __device__ __forceinline__ void stage_seg(unsigned sbase, const double* base,
   }
 }
 
+// Stage n slots of a column-gathered operand (Term b_kc == 2): X(idx, kk) =
+// colp[idx][off + kk] -> smem [idx][slot] (LDK); idx valid in [lo, hi).
+template <class C>
+__device__ __forceinline__ void stage_cols(unsigned sbase, const double* const* colp, int64_t off,
+                                           const double* safe, int lo, int hi, int slot0, int n) {
+  constexpr int PK = C::KC / 2, RL = C::THREADS / PK;
+  const int tid = threadIdx.x;
+  const int q = tid % PK, r = tid / PK;
+  const int kk = 2 * q;
+  if (kk >= n) return;
+  const bool pair = kk + 1 < n;
+  for (int i = r; i < C::TM; i += RL) {
+    const bool v = i >= lo && i < hi;
+    const unsigned dst = sbase + 8u * unsigned(i * C::LDK + slot0 + kk);
+    const double* src = v ? colp[i] + off + kk : safe;
+    if (pair && v && ((slot0 & 1) == 0) && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      cp_async16(dst, src, 16);
+    } else {
+      cp_async8(dst, src, v ? 8 : 0);
+      if (pair) cp_async8(dst + 8u, v ? src + 1 : safe, v ? 8 : 0);
+    }
+  }
+}
+
 // Zero slots [a, b) of an operand in either layout (pad up to a multiple of 4).
 template <class C>
 __device__ __forceinline__ void zero_slots(double* s, int kc, int a, int b) {
@@ -192,18 +216,19 @@ template <class C>
 __device__ __forceinline__ Chunk build_chunk(double* sP, double* sQ, Cursor& cur, bool& have,
                                              const Group* __restrict__ groups,
                                              const Term* __restrict__ terms,
-                                             const BufPtrs& bufs, const Tile& tl, int wm, int wn) {
+                                             const BufPtrs& bufs, const Tile& tl, int wm, int wn,
+                                             const double* const* colp) {
   Chunk ch;
   ch.used = 0;
   ch.amask = ch.bmask = 0;
   ch.akc = cur.tm.a_kc;
-  ch.bkc = cur.tm.b_kc;
+  ch.bkc = cur.tm.b_kc ? 1 : 0;  // smem layout: column-gathered operands stage like kc 1
   const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(sP));
   const unsigned sq = static_cast<unsigned>(__cvta_generic_to_shared(sQ));
   int nseg = 0;
   while (have && ch.used < C::KC && nseg < C::MAXSEG) {
     const Term& tm = cur.tm;
-    if (tm.a_kc != ch.akc || tm.b_kc != ch.bkc) break;  // one staging layout per chunk
+    if (tm.a_kc != ch.akc || (tm.b_kc ? 1 : 0) != ch.bkc) break;  // one layout per chunk
     const int n = min(C::KC - ch.used, tm.k - cur.k0);
     const int i0 = tl.row0 - tm.r_lo, j0 = tl.col0 - tm.c_lo;
     const int rlo = max(0, -i0), rhi = min(int(tl.rows), tm.rows - i0);
@@ -216,7 +241,10 @@ __device__ __forceinline__ Chunk build_chunk(double* sP, double* sQ, Cursor& cur
         tm.b_kc ? B + cur.k0 + int64_t(j0) * tm.b_ld : B + j0 + int64_t(cur.k0) * tm.b_ld;
     // masked copies read nothing, but get an in-bounds address (the term's first element)
     stage_seg<C>(sp, pa, A, tm.a_ld, tm.a_kc, rlo, rhi, ch.used, n);
-    stage_seg<C>(sq, pb, B, tm.b_ld, tm.b_kc, clo, chi, ch.used, n);
+    if (tm.b_kc == 2)
+      stage_cols<C>(sq, colp, tm.b_off + cur.k0, bufs.p[BUF_A], clo, chi, ch.used, n);
+    else
+      stage_seg<C>(sq, pb, B, tm.b_ld, tm.b_kc, clo, chi, ch.used, n);
 #pragma unroll
     for (int a = 0; a < C::FR; ++a) {
       const int f0 = wm * C::WT + a * 8;
@@ -293,14 +321,26 @@ template <class C>
 __global__ void __launch_bounds__(C::THREADS) grouped_gemm_kernel(
     const Tile* __restrict__ tiles, const Group* __restrict__ groups,
     const Term* __restrict__ terms, const __grid_constant__ BufPtrs bufs,
-    double* __restrict__ sumsq, int n_tiles) {
+    double* __restrict__ sumsq, int n_tiles, const ColRec* __restrict__ gcols) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red[C::THREADS / 32];
+  __shared__ const double* colp[C::TM];
   const int tile_idx = blockIdx.x;
   if (tile_idx >= n_tiles) return;
   const Tile tl = tiles[tile_idx];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wm = warp >> 1, wn = warp & 1;
+  if (tl.mode == MODE_GCOL) {
+    // column pointers of the tile's slice of the virtual matrix G
+    if (int(threadIdx.x) < tl.cols) {
+      const int j = tl.col0 + threadIdx.x;
+      int idx = tl.aux;
+      ColRec r = gcols[idx];
+      while (j >= r.col + r.k) r = gcols[++idx];
+      colp[threadIdx.x] = bufs.p[r.buf] + r.src_off + int64_t(j - r.col) * r.ld;
+    }
+    __syncthreads();
+  }
 
   double acc[C::FR][C::FR][2];
 #pragma unroll
@@ -315,11 +355,13 @@ __global__ void __launch_bounds__(C::THREADS) grouped_gemm_kernel(
   cur.k0 = 0;
   bool have = next_term(cur, groups, terms);
   int stage = 0;
-  Chunk now = build_chunk<C>(smem, smem + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn);
+  Chunk now =
+      build_chunk<C>(smem, smem + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn, colp);
   cp_async_commit();
   while (now.used > 0) {
     double* ns = smem + (stage ^ 1) * C::STAGE;
-    Chunk nxt = build_chunk<C>(ns, ns + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn);
+    Chunk nxt =
+        build_chunk<C>(ns, ns + C::OPSZ, cur, have, groups, terms, bufs, tl, wm, wn, colp);
     cp_async_commit();
     cp_async_wait<1>();
     __syncthreads();

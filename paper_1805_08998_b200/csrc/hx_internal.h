@@ -133,7 +133,7 @@ struct hx_plan {
   std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
   hx::pvec<hx::OutLeaf> leaves;
   int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
-  hx::hvec<hx::CopyRec> gather;
+  hx::hvec<hx::ColRec> gcols;  // thin factors of each X-group (virtual G)
   // X-groups are processed in batches whose gathered factors and cores fit a bounded
   // workspace (BUF_GATHER / BUF_CORE offsets restart at 0 in every batch)
   struct Batch {

@@ -11,6 +11,8 @@
 //                  a_kc == 1 -> P(i, kk) = buf[a_off + kk + i * a_ld]   (transposed factor)
 //   Q (k x cols):  b_kc == 0 -> Q(kk, j) = buf[b_off + j + kk * b_ld]   (factor used as F^T)
 //                  b_kc == 1 -> Q(kk, j) = buf[b_off + kk + j * b_ld]   (column-major matrix)
+//                  b_kc == 2 -> Q(kk, j) = G(b_off + kk, j), G the tile's column-gathered
+//                               virtual matrix (ColRec, MODE_GCOL tiles)
 //
 // A term only covers rows [r_lo, r_lo + rows) and columns [c_lo, c_lo + cols) of the
 // tile coordinate system; the kernel zero-fills outside, so a term created on a
@@ -41,11 +43,21 @@ struct CopyRec {
   int32_t pad;
 };
 
+// One thin factor of an X-group, seen as columns [col, col + k) of the group's virtual
+// matrix G: column col + c is bufs[buf] + src_off + c * ld (ld = |rho| rows).  Tiles in
+// MODE_GCOL read G through these records instead of a gathered copy (Term b_kc == 2).
+struct ColRec {
+  int64_t src_off;
+  int32_t col, k, ld, buf;
+};
+static_assert(sizeof(ColRec) == 24, "ColRec layout");
+
 enum TileMode : uint8_t {
   MODE_STORE = 0,       // out  = sum
   MODE_ADD = 1,         // out += sum
   MODE_STORE_SUMSQ = 2,  // out  = sum, and sumsq[aux] = sum of squares of the tile
-  MODE_RESID_SUMSQ = 3   // out unchanged, sumsq[aux] = sum of squares of (out - sum)
+  MODE_RESID_SUMSQ = 3,  // out unchanged, sumsq[aux] = sum of squares of (out - sum)
+  MODE_GCOL = 4          // out = sum; aux = first ColRec of the tile's columns (b_kc == 2)
 };
 
 struct Term {

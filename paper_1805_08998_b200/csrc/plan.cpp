@@ -645,9 +645,10 @@ struct Builder {
     return b1 >= b0 ? b1 - b0 + 1 : 0;
   }
 
-  // Tiles of an R x C output (ld R) whose row band i uses group gbase + i.
+  // Tiles of an R x C output (ld R) whose row band i uses group gbase + i; gcol[jt]: first
+  // column record of column tile jt (MODE_GCOL tiles read the X-group's virtual G).
   void write_band_tiles(Tile* tiles, uint8_t out_buf, int64_t out_off, int64_t R, int64_t C,
-                        int64_t row_base, int32_t gbase) const {
+                        int64_t row_base, int32_t gbase, const int32_t* gcol) const {
     int64_t w = 0;
     for (int64_t i = 0, band = 0; i < R; i += T, ++band) {
       const int64_t r1 = std::min<int64_t>(R, i + T);
@@ -662,9 +663,9 @@ struct Builder {
         tl.cols = int16_t(std::min<int64_t>(C, j + T) - j);
         tl.g_begin = gbase + int32_t(band);
         tl.g_end = gbase + int32_t(band) + 1;
-        tl.aux = -1;
+        tl.aux = gcol[j / T];
         tl.out_buf = out_buf;
-        tl.mode = hx::MODE_STORE;
+        tl.mode = hx::MODE_GCOL;
       }
     }
   }
@@ -803,6 +804,7 @@ struct Builder {
       GInfo& g = G[gi_];
       const int64_t gat_need = align16(g.kr * g.ktot);
       const int64_t core_need = align16(g.srows * g.ktot);
+      // the thin factors are read in place (ColRec); gat_cur only bounds a batch's size
       if ((gat_cur + gat_need > budget || core_cur + core_need > budget) &&
           (gat_cur > 0 || core_cur > 0)) {
         close_batch(gi_);
@@ -815,7 +817,6 @@ struct Builder {
       gat_cur += gat_need;
       g.core = core_cur;
       core_cur += core_need;
-      P.gather_elems = std::max(P.gather_elems, gat_cur);
       P.core_elems = std::max(P.core_elems, core_cur);
       g.o_gather = o_gather;
       o_gather += g.b1 - g.b0;
@@ -836,7 +837,7 @@ struct Builder {
       P.info.n_xgroups++;
     }
     close_batch(ng);
-    P.gather.resize(size_t(o_gather));
+    P.gcols.resize(size_t(o_gather));
     P.core_tiles.resize(size_t(o_ct));
     P.core_groups.resize(size_t(o_cg));
     P.core_terms.resize(size_t(o_cm));
@@ -844,21 +845,21 @@ struct Builder {
     P.fac_groups.resize(size_t(o_fg));
     P.fac_terms.resize(size_t(o_fm));
     lap("pass2");
-    // pass 3 (parallel): gather records and the computed-factor offsets of the
-    // materialization terms -- everything the materialization launch needs
+    // pass 3 (parallel): column records of the virtual G and the computed-factor offsets of
+    // the materialization terms -- everything the materialization launch needs
 #pragma omp parallel for schedule(dynamic, 64)
     for (int64_t gi_ = 0; gi_ < ng; ++gi_) {
       const GInfo& g = G[gi_];
-      // gather the thin factors side by side, patch the materialization terms
+      // the thin factors side by side as columns of G; patch the materialization terms
       int64_t col = 0;
       for (int32_t i = g.b0; i < g.b1; ++i) {
         const TRec& r = recs[order[i]];
-        hx::CopyRec& cp = P.gather[size_t(g.o_gather + (i - g.b0))];
-        cp.src_buf = g.side == 0 ? hx::BUF_B : hx::BUF_A;
+        hx::ColRec& cp = P.gcols[size_t(g.o_gather + (i - g.b0))];
+        cp.buf = g.side == 0 ? hx::BUF_B : hx::BUF_A;
         cp.src_off = g.side == 0 ? B.u_off[r.qc] : A.v_off[r.pc];
-        cp.dst_off = g.gat + col * g.kr;
-        cp.n = g.kr * r.k;
-        cp.pad = 0;
+        cp.col = int32_t(col);
+        cp.k = r.k;
+        cp.ld = int32_t(g.kr);
         Term& mt = P.mat_terms[r.mat];
         if (g.side == 0) {
           mt.a_off = g.out + col * g.R;
@@ -882,6 +883,18 @@ struct Builder {
       const GInfo& g = G[gi_];
       const hx_operand& opX = g.side == 0 ? A : B;
       const uint8_t xbuf = g.side == 0 ? hx::BUF_A : hx::BUF_B;
+      const uint8_t gbuf = g.side == 0 ? hx::BUF_B : hx::BUF_A;  // the thin factors
+      // first column record of every 64-column tile of G
+      thread_local std::vector<int32_t> gcol;
+      gcol.assign(size_t(nbands(g.ktot, T)), 0);
+      {
+        int32_t rec = int32_t(g.o_gather);
+        for (size_t jt = 0; jt < gcol.size(); ++jt) {
+          const int64_t j = int64_t(jt) * T;
+          while (P.gcols[size_t(rec)].col + P.gcols[size_t(rec)].k <= j) ++rec;
+          gcol[jt] = rec;
+        }
+      }
       // stacked cores S (srows x ktot, ld srows): rows [off_l, off_l + k_l) = V_l^T G[rho_l]
       // (A side) or U_l^T G[rho_l] (B side)
       const int64_t nbs = nbands(g.srows, T);
@@ -899,9 +912,9 @@ struct Builder {
           const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];
           const int64_t roff = lo(rl) - lo(g.rho);
           const int64_t mid_f = g.side == 0 ? opX.v_off[l] : opX.u_off[l];
-          const Term tm = make_term(xbuf, mid_f, int32_t(sz(rl)), 1, hx::BUF_GATHER,
-                                    g.gat + roff, int32_t(g.kr), 1, int32_t(sz(rl)), cr.row, 0,
-                                    cr.rows, g.ktot);
+          const Term tm = make_term(xbuf, mid_f, int32_t(sz(rl)), 1, gbuf, roff,
+                                    int32_t(g.kr), 2, int32_t(sz(rl)), cr.row, 0, cr.rows,
+                                    g.ktot);
           for (int64_t band = cr.row / T; band <= (cr.row + cr.rows - 1) / T; ++band) {
             while (band_next <= band)
               P.core_groups[size_t(g.o_cg + band_next++)].t_begin = int32_t(w);
@@ -913,7 +926,7 @@ struct Builder {
           P.core_groups[size_t(g.o_cg + band)].t_end =
               band + 1 < nbs ? P.core_groups[size_t(g.o_cg + band + 1)].t_begin : int32_t(w);
         write_band_tiles(&P.core_tiles[size_t(g.o_ct)], hx::BUF_CORE, g.core, g.srows, g.ktot, 0,
-                         int32_t(g.o_cg));
+                         int32_t(g.o_cg), gcol.data());
       }
       // row bands of X G (A side) / X^T G (B side): count per band, then place (leaves in
       // DFS order within a band)
@@ -951,15 +964,15 @@ struct Builder {
                            g.ktot);
           } else {
             tm = make_term(xbuf, opX.d_off[l], int32_t(sz(t.tau[l])),
-                           uint8_t(g.side == 0 ? 0 : 1), hx::BUF_GATHER, g.gat + roff,
-                           int32_t(g.kr), 1, int32_t(sz(rl)), lo(ol), 0, sz(ol), g.ktot);
+                           uint8_t(g.side == 0 ? 0 : 1), gbuf, roff, int32_t(g.kr), 2,
+                           int32_t(sz(rl)), lo(ol), 0, sz(ol), g.ktot);
           }
           for (int64_t band = (lo(ol) - base) / T; band <= (lo(ol) + sz(ol) - 1 - base) / T;
                ++band)
             P.fac_terms[size_t(g.o_fm + pos[size_t(band)]++)] = tm;
         }
         write_band_tiles(&P.fac_tiles[size_t(g.o_ft)], hx::BUF_TERM, g.out, g.R, g.ktot,
-                         lo(g.rows_cl), int32_t(g.o_fg));
+                         lo(g.rows_cl), int32_t(g.o_fg), gcol.data());
       }
     }
   }
@@ -1101,7 +1114,7 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
     I.term_elems = plan->term_elems;
     I.tile_elems = plan->tile_elems;
     I.gather_elems = plan->gather_elems;
-    I.gather_jobs = int64_t(plan->gather.size());
+    I.gather_jobs = int64_t(plan->gcols.size());
     *out = plan;
     return HX_OK;
   });

@@ -91,14 +91,6 @@ __global__ void omega_kernel(double* om, int64_t n, uint64_t seed) {
   om[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
-// Thin factors of each X-group copied side by side into G (BUF_GATHER).
-__global__ void gather_kernel(const CopyRec* __restrict__ recs, BufPtrs bufs) {
-  const CopyRec r = recs[blockIdx.x];
-  const double* __restrict__ src = bufs.p[r.src_buf] + r.src_off;
-  double* __restrict__ dst = bufs.p[BUF_GATHER] + r.dst_off;
-  for (int64_t e = threadIdx.x; e < r.n; e += blockDim.x) dst[e] = src[e];
-}
-
 }  // namespace
 
 // ---- page-locked host memory cache (plan work lists) ----------------------------------
@@ -261,7 +253,7 @@ struct hx_ctx {
   DArr<Group> groups[3];
   DArr<double> sumsq, fro2;
   DArr<int> seg_b, seg_e;
-  DArr<CopyRec> gather_recs;
+  DArr<ColRec> gcols;
   DArr<Term> rterms;
   DArr<Tile> rtiles;
   DArr<Group> rgroups;
@@ -309,7 +301,8 @@ struct hx_ctx {
 namespace {
 
 void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, const Term* terms,
-                 int n_tiles, const BufPtrs& bp, double* sumsq) {
+                 int n_tiles, const BufPtrs& bp, double* sumsq,
+                 const ColRec* gcols = nullptr) {
   if (n_tiles <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -321,10 +314,10 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
   }
   if (tile == 32)
     grouped_gemm_kernel<Gemm32><<<n_tiles, Gemm32::THREADS, Gemm32::SMEM, c->s>>>(
-        tiles, groups, terms, bp, sumsq, n_tiles);
+        tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   else
     grouped_gemm_kernel<Gemm64><<<n_tiles, Gemm64::THREADS, Gemm64::SMEM, c->s>>>(
-        tiles, groups, terms, bp, sumsq, n_tiles);
+        tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   CK(cudaGetLastError());
   c->launches++;
 }
@@ -587,7 +580,7 @@ extern "C" int hx_ctx_trim(hx_ctx* c) {
     c->fro2.release();
     c->seg_b.release();
     c->seg_e.release();
-    c->gather_recs.release();
+    c->gcols.release();
     c->rterms.release();
     c->rtiles.release();
     c->rgroups.release();
@@ -644,7 +637,6 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     c->own[BUF_CORE].ensure(size_t(P->core_elems));
     c->own[BUF_TERM].ensure(size_t(P->term_elems));
     c->own[BUF_TILE].ensure(size_t(P->tile_elems));
-    c->own[BUF_GATHER].ensure(size_t(P->gather_elems));
     c->sumsq.ensure(size_t(P->n_sumsq));
     for (int i = 0; i < 2; ++i) {
       c->terms[i].ensure(i ? P->fac_terms.size() : P->core_terms.size());
@@ -654,13 +646,13 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     c->terms[2].ensure(P->mat_terms.size());
     c->tiles[2].ensure(P->mat_tiles.size());
     c->groups[2].ensure(P->mat_groups.size());
-    c->gather_recs.ensure(P->gather.size());
-    // gather records first on the compute stream; the materialization lists on the copy
+    c->gcols.ensure(P->gcols.size());
+    // column records first on the compute stream; the materialization lists on the copy
     // stream, overlapping the whole formation phase (host arrays are page-locked)
     auto h2d = [](void* d, const void* h, size_t bytes, cudaStream_t st) {
       if (bytes) CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
     };
-    h2d(c->gather_recs.p, P->gather.data(), P->gather.size() * sizeof(CopyRec), s);
+    h2d(c->gcols.p, P->gcols.data(), P->gcols.size() * sizeof(ColRec), s);
     CK(cudaEventRecord(c->ev[6], s));
     CK(cudaStreamWaitEvent(c->s2, c->ev[6], 0));  // buffers allocated before s2 copies
     h2d(c->terms[2].p, P->mat_terms.data(), P->mat_terms.size() * sizeof(Term), c->s2);
@@ -691,16 +683,10 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
           size_t(bt.fg_end - bt.fg_begin) * sizeof(Group), s);
       h2d(c->terms[1].p + bt.fm_begin, P->fac_terms.data() + bt.fm_begin,
           size_t(bt.fm_end - bt.fm_begin) * sizeof(Term), s);
-      const int ng = int(bt.gather_end - bt.gather_begin);
-      if (ng > 0) {
-        gather_kernel<<<ng, 256, 0, s>>>(c->gather_recs.p + bt.gather_begin, bp);
-        CK(cudaGetLastError());
-        c->launches++;
-      }
       launch_gemm(c, P->tile, c->tiles[0].p + bt.core_begin, c->groups[0].p, c->terms[0].p,
-                  int(bt.core_end - bt.core_begin), bp, nullptr);
+                  int(bt.core_end - bt.core_begin), bp, nullptr, c->gcols.p);
       launch_gemm(c, P->tile, c->tiles[1].p + bt.fac_begin, c->groups[1].p, c->terms[1].p,
-                  int(bt.fac_end - bt.fac_begin), bp, nullptr);
+                  int(bt.fac_end - bt.fac_begin), bp, nullptr, c->gcols.p);
     }
     CK(cudaEventRecord(c->ev[1], s));
     // ---- 2. materialization
@@ -1585,7 +1571,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   c->fro2.release();
   c->seg_b.release();
   c->seg_e.release();
-  c->gather_recs.release();
+  c->gcols.release();
   c->rterms.release();
   c->rtiles.release();
   c->rgroups.release();
