@@ -570,7 +570,14 @@ extern "C" int hx_ctx_trim(hx_ctx* c) {
     CK(cudaSetDevice(c->device));
     CK(cudaStreamSynchronize(c->s));
     CK(cudaStreamSynchronize(c->s2));
-    for (int i = BUF_TERM; i < NUM_BUFS; ++i) c->own[i].release();
+    for (int i = BUF_TERM; i < NUM_BUFS; ++i) {
+      if (i == BUF_WORK) {  // points into work[] (released below)
+        c->own[i].p = nullptr;
+        c->own[i].cap = 0;
+        continue;
+      }
+      c->own[i].release();
+    }
     for (int i = 0; i < 3; ++i) {
       c->terms[i].release();
       c->tiles[i].release();
