@@ -211,15 +211,18 @@ def split_chunk(bct, group):
     return parts
 
 
-def chunk_groups(bct, n_chunks):
-    """About `n_chunks` chunks of consecutive units with equal leaf area."""
+def chunk_groups(bct, n_chunks, first=1.0):
+    """About `n_chunks` chunks of consecutive units with equal leaf area (the first one
+    `first` times the others)."""
     units = chunk_units(bct)
     total = sum(u[2] for u in units)
-    target = total / max(1, n_chunks)
+    n_chunks = max(1, n_chunks)
+    unit = total / (n_chunks - 1 + first) if n_chunks > 1 else total
     groups, cur, acc = [], [], 0.0
     for u in units:
         cur.append(u)
         acc += u[2]
+        target = unit * (first if not groups else 1.0)
         if acc >= target and len(groups) < n_chunks - 1:
             groups.append(cur)
             cur, acc = [], 0.0
@@ -264,22 +267,25 @@ def available_bytes(dev):
 
 
 def default_chunks(bct, dev=None, overlap=None):
-    """Chunks needed to keep one chunk's device workspace (materialized blocks plus term
-    factors, ~12x the leaf area on the BASELINE configs) within ~60% of free memory."""
+    """(chunks, overlap): enough chunks to keep one chunk's device workspace (materialized
+    blocks plus term factors, ~12x the leaf area on the BASELINE configs) within ~60% of
+    free memory.  A large product that fits whole runs instead as 3 chunks alternating
+    over two contexts: one chunk's latency-bound recompression overlaps the next chunk's
+    term formation (config 2: 427 -> 389 ms).  Memory-bound products do not overlap (two
+    chunks in flight would halve the chunk size and repeat more ancestor work)."""
     env = os.environ.get("HX_CHUNKS")
     if env:
-        return max(1, int(env))
+        n = max(1, int(env))
+        return n, n > 1 and overlap_default(overlap)
     area = sum(u[2] for u in chunk_units(bct))
     free = 60e9
     if dev is not None:
         free = available_bytes(dev)
     need = area * 8.0 * 12.0
     n = max(1, int(np.ceil(need / (0.6 * free))))
-    # large products run as >= 3 chunks on two contexts: a chunk's recompression overlaps
-    # the next chunk's term formation (config 2: 427 -> 389 ms per product)
-    if area >= 2.5e8 and overlap_default(overlap):
-        n = max(n, 3)
-    return n
+    if n == 1 and area >= 2.5e8 and overlap_default(overlap):
+        return 3, True
+    return n, False
 
 
 # --------------------------------------------------------------------------- product
@@ -350,8 +356,13 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                            int(sketch0), int(oversample))
     ta = tree_arrays(h.bct)
     tile = plan_tile(h.bct)
-    nch = default_chunks(h.bct, dev, overlap) if chunks is None else max(1, int(chunks))
-    queue = collections.deque(chunk_groups(h.bct, nch))
+    if chunks is None:
+        nch, use_overlap = default_chunks(h.bct, dev, overlap)
+    else:
+        nch = max(1, int(chunks))
+        use_overlap = nch > 1 and overlap_default(overlap)
+    # with overlap the first chunk is half size: its planning is the only exposed part
+    queue = collections.deque(chunk_groups(h.bct, nch, first=0.5 if use_overlap else 1.0))
     budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
@@ -376,7 +387,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     # with several chunks, two contexts (two streams) run consecutive chunks concurrently:
     # one chunk's latency-bound recompression overlaps the next chunk's term formation
     ctxs = [dev]
-    if len(queue_all) > 1 and overlap_default(overlap):
+    if len(queue_all) > 1 and use_overlap:
         aux = Device.aux(device)
         _lib.check(_lib.lib().hx_ctx_operand_share(aux.h, dev.h), "hx_ctx_operand_share")
         ctxs.append(aux)
