@@ -49,10 +49,11 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-template <int TM_>
+template <int TM_, int KC_ = 32, int MINB_ = 1>
 struct GemmCfg {
   static constexpr int TM = TM_;
-  static constexpr int KC = 32;                // slots per chunk
+  static constexpr int KC = KC_;               // slots per chunk
+  static constexpr int MINB = MINB_;           // resident CTAs per SM to budget registers for
   static constexpr int LDI = TM + 4;           // [slot][i] row (doubles), 16B aligned
   static constexpr int LDK = KC + 4;           // [i][slot] row (doubles), 16B aligned
   static constexpr int OPSZ = (KC * LDI > TM * LDK) ? KC * LDI : TM * LDK;
@@ -64,8 +65,11 @@ struct GemmCfg {
   static constexpr int MAXSEG = 8;
 };
 
-using Gemm64 = GemmCfg<64>;
+using Gemm64 = GemmCfg<64, 32, 3>;
 using Gemm32 = GemmCfg<32>;
+// short-K batches (stacked cores, X G bands: K ~ 70): half-size chunks, 41 KB of smem and
+// <= 128 registers, so four CTAs share an SM and hide each other's tile prologues
+using Gemm64s = GemmCfg<64, 16, 4>;
 
 // Cursor over (group, term, k offset) of one tile.
 struct Cursor {
@@ -318,7 +322,7 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[C::FR][C::FR][2], const 
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::THREADS) grouped_gemm_kernel(
+__global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_kernel(
     const Tile* __restrict__ tiles, const Group* __restrict__ groups,
     const Term* __restrict__ terms, const __grid_constant__ BufPtrs bufs,
     double* __restrict__ sumsq, int n_tiles, const ColRec* __restrict__ gcols) {

@@ -244,6 +244,9 @@ struct hx_ctx {
   int device = 0;
   cudaStream_t s = nullptr;
   cudaStream_t s2 = nullptr;  // copy stream (materialization work lists)
+  // high-priority stream for the latency-bound recompression: when two contexts run
+  // consecutive chunks, its small launches get SMs ahead of the other chunk's formation
+  cudaStream_t s_hi = nullptr;
   DArr<double> own[NUM_BUFS];
   double* attached[2] = {nullptr, nullptr};
   int64_t opnd_elems[2] = {0, 0};
@@ -302,7 +305,7 @@ namespace {
 
 void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, const Term* terms,
                  int n_tiles, const BufPtrs& bp, double* sumsq,
-                 const ColRec* gcols = nullptr) {
+                 const ColRec* gcols = nullptr, bool short_k = false) {
   if (n_tiles <= 0) return;
   static bool attr = false;
   if (!attr) {
@@ -310,9 +313,15 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
                             cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm64::SMEM));
     CK(cudaFuncSetAttribute(grouped_gemm_kernel<Gemm32>,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm32::SMEM));
+    CK(cudaFuncSetAttribute(grouped_gemm_kernel<Gemm64s>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm64s::SMEM));
     attr = true;
   }
-  if (tile == 32)
+  static const bool use_short = !std::getenv("HX_NO_SHORTK");
+  if (tile == 64 && short_k && use_short)
+    grouped_gemm_kernel<Gemm64s><<<n_tiles, Gemm64s::THREADS, Gemm64s::SMEM, c->s>>>(
+        tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+  else if (tile == 32)
     grouped_gemm_kernel<Gemm32><<<n_tiles, Gemm32::THREADS, Gemm32::SMEM, c->s>>>(
         tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   else
@@ -522,6 +531,9 @@ extern "C" int hx_ctx_create(int device, hx_ctx** out) {
     c->device = device;
     CK(cudaStreamCreateWithFlags(&c->s, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s2, cudaStreamNonBlocking));
+    int lo_prio = 0, hi_prio = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    CK(cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi_prio));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     *out = c;
     return HX_OK;
@@ -691,9 +703,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       h2d(c->terms[1].p + bt.fm_begin, P->fac_terms.data() + bt.fm_begin,
           size_t(bt.fm_end - bt.fm_begin) * sizeof(Term), s);
       launch_gemm(c, P->tile, c->tiles[0].p + bt.core_begin, c->groups[0].p, c->terms[0].p,
-                  int(bt.core_end - bt.core_begin), bp, nullptr, c->gcols.p);
+                  int(bt.core_end - bt.core_begin), bp, nullptr, c->gcols.p, true);
       launch_gemm(c, P->tile, c->tiles[1].p + bt.fac_begin, c->groups[1].p, c->terms[1].p,
-                  int(bt.fac_end - bt.fac_begin), bp, nullptr, c->gcols.p);
+                  int(bt.fac_end - bt.fac_begin), bp, nullptr, c->gcols.p, true);
     }
     CK(cudaEventRecord(c->ev[1], s));
     // ---- 2. materialization
@@ -719,7 +731,17 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->launches++;
     }
 
-    // ---- 3. recompression of far leaves
+    // ---- 3. recompression of far leaves, on the high-priority stream
+    const cudaStream_t s_main = s;
+    CK(cudaEventRecord(c->ev[6], s));
+    CK(cudaStreamWaitEvent(c->s_hi, c->ev[6], 0));
+    s = c->s_hi;
+    c->s = s;
+    struct RestoreStream {
+      hx_ctx* c;
+      cudaStream_t s;
+      ~RestoreStream() { c->s = s; }
+    } restore_stream{c, s_main};
     std::vector<FarBlock> fb;
     int mu_max = 0;
     for (int i = 0; i < nl; ++i) {
@@ -1591,6 +1613,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   for (auto& e : c->ev) cudaEventDestroy(e);
   cudaStreamDestroy(c->s);
   cudaStreamDestroy(c->s2);
+  cudaStreamDestroy(c->s_hi);
   delete c;
 }
 
