@@ -366,6 +366,10 @@ def bench_ours(args, rank, world, local):
         pa, _ = multiply._host_directory(A)
         pb = pa if B is A else multiply._host_directory(B)[0]
         h2d = 8 * (pa.size + (0 if B is A else pb.size))
+        for _ in range(2):  # warm-up: page-locked result buffers enter the reuse cache
+            del_me = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
+                                              device_operands=False)
+            del del_me
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -374,8 +378,9 @@ def bench_ours(args, rank, world, local):
         for _ in range(max(1, args.steps // 2)):
             Ce = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
                                           device_operands=False)
-            d2h = 8 * sum((p.left.size + p.right.size) if hasattr(p, "left") else p.size
-                          for p in Ce.data.values())
+            # bytes of the result buffers copied back (every far factor and near block);
+            # the HMatrix builds its leaf views over them on access
+            d2h = 8 * int(Ce.report.out_elems)
         torch.cuda.synchronize()
         te = (time.perf_counter() - t0) / max(1, args.steps // 2)
         tt = torch.tensor([te], dtype=torch.float64, device="cuda")

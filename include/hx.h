@@ -200,6 +200,12 @@ int64_t hx_ctx_held_bytes(hx_ctx* ctx);
 /* Attach the operand pools of src (same device) to dst without copying, so that two
  * contexts -- two streams -- can run products (chunks) concurrently. */
 int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src);
+/* Page-locked host memory for the caller's result blocks (from the library's reuse cache;
+ * hx_host_free returns it) and registration of caller-owned pools for fast uploads. */
+void* hx_host_alloc(int64_t bytes);
+void hx_host_free(void* p, int64_t bytes);
+int hx_host_register(void* p, int64_t bytes);
+int hx_host_unregister(void* p);
 /* Release the product workspace (work lists, term/tile buffers, results not yet
  * downloaded); operand pools stay attached. */
 int hx_ctx_trim(hx_ctx* ctx);

@@ -89,6 +89,10 @@ SIGNATURES = {
     "hx_ctx_trim": [C.c_void_p],
     "hx_ctx_operand_share": [C.c_void_p, C.c_void_p],
     "hx_ctx_held_bytes": [C.c_void_p],
+    "hx_host_alloc": [C.c_int64],
+    "hx_host_free": [C.c_void_p, C.c_int64],
+    "hx_host_register": [C.c_void_p, C.c_int64],
+    "hx_host_unregister": [C.c_void_p],
     "hx_operand_layout": [C.POINTER(HxTree), i8p, i32p, i64p, i64p, i64p, i64p],
     "hx_hmatvec": [C.c_void_p, C.POINTER(HxTree), C.POINTER(HxOperand), C.c_int, C.c_int,
                    f64p, f64p, C.c_int],
@@ -98,8 +102,9 @@ SIGNATURES = {
     "hx_last_error": [C.c_char_p, C.c_size_t],
     "hx_version": [],
 }
-VOID_RET = {"hx_plan_free", "hx_ctx_free"}
+VOID_RET = {"hx_plan_free", "hx_ctx_free", "hx_host_free"}
 INT64_RET = {"hx_ctx_held_bytes"}
+PTR_RET = {"hx_host_alloc"}
 
 STATUS_EXC = {-1: ValueError, -2: MemoryError, -3: HxError, -4: NotImplementedError}
 
@@ -117,8 +122,8 @@ def lib():
                 continue
             f = getattr(L, name)
             f.argtypes = args
-            f.restype = None if name in VOID_RET else (C.c_int64 if name in INT64_RET
-                                                        else C.c_int)
+            f.restype = None if name in VOID_RET else (
+                C.c_int64 if name in INT64_RET else (C.c_void_p if name in PTR_RET else C.c_int))
         _lib = L
     return _lib
 
@@ -212,3 +217,28 @@ class Plan:
             self.close()
         except Exception:  # pragma: no cover
             pass
+
+
+def pinned_empty(n, dtype=np.float64):
+    """numpy array of n elements in page-locked memory from the library's cache (returned to
+    the cache when the array and every view of it are gone)."""
+    import weakref
+    itemsize = np.dtype(dtype).itemsize
+    nbytes = max(int(n), 1) * itemsize
+    p = lib().hx_host_alloc(nbytes)
+    if not p:
+        raise MemoryError("hx_host_alloc failed")
+    buf = (C.c_char * nbytes).from_address(p)
+    arr = np.frombuffer(buf, dtype=dtype, count=max(int(n), 1))
+    weakref.finalize(buf, lib().hx_host_free, p, nbytes)
+    return arr
+
+
+def pin_host_array(a):
+    """Page-lock a caller-owned array in place (uploads become DMA); undone when it dies."""
+    import weakref
+    if a.nbytes == 0 or getattr(a, "_hx_pinned", False):
+        return
+    p = a.ctypes.data
+    if lib().hx_host_register(C.c_void_p(p), a.nbytes) == 0:
+        weakref.finalize(a, lib().hx_host_unregister, C.c_void_p(p))

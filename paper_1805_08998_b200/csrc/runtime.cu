@@ -1618,3 +1618,31 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
 }
 
 #include "assemble.cuh"
+
+// ---- page-locked host memory for the Python layer (result blocks, operand pools)
+extern "C" void* hx_host_alloc(int64_t bytes) {
+  try {
+    return hx::pinned_alloc(size_t(std::max<int64_t>(bytes, 1)));
+  } catch (...) {
+    return nullptr;
+  }
+}
+
+extern "C" void hx_host_free(void* p, int64_t bytes) {
+  hx::pinned_free(p, size_t(std::max<int64_t>(bytes, 1)));
+}
+
+extern "C" int hx_host_register(void* p, int64_t bytes) {
+  if (!p || bytes <= 0) return fail(HX_EINVAL, "bad host range");
+  const cudaError_t e = cudaHostRegister(p, size_t(bytes), cudaHostRegisterPortable);
+  if (e == cudaSuccess) return HX_OK;
+  cudaGetLastError();
+  if (e == cudaErrorHostMemoryAlreadyRegistered) return HX_OK;
+  return fail(HX_ECUDA, std::string("cudaHostRegister: ") + cudaGetErrorString(e));
+}
+
+extern "C" int hx_host_unregister(void* p) {
+  if (!p) return HX_OK;
+  if (cudaHostUnregister(p) != cudaSuccess) cudaGetLastError();
+  return HX_OK;
+}

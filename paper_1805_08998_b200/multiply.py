@@ -150,7 +150,83 @@ def _host_directory(h):
     if pool is None:  # assembled on the device: one download of the packed pool
         pool = h._hx_pool.download()
         h._hx_packed = (pool, d)
+    if pool.nbytes >= (64 << 20) and not getattr(h, "_hx_pool_pinned", False):
+        # page-locked once: every later upload of this operand is a full-speed DMA
+        _lib.pin_host_array(pool)
+        try:
+            h._hx_pool_pinned = True
+        except AttributeError:  # pragma: no cover
+            pass
     return pool, d
+
+
+class _ProductLeaves(dict):
+    """Leaf payloads of a product, built on first access from the downloaded result
+    buffers (zero-copy views: far leaves LowRank(U*S, V), near leaves m x n arrays)."""
+
+    def __init__(self, chunks):
+        super().__init__()
+        self._chunks = chunks  # (leaves dict, rank, deg, off, res) per chunk
+        self._where = None
+        self._filled = False
+
+    def _index(self):
+        if self._where is None:
+            self._where = {}
+            for ci, (lv, rank, deg, off, res) in enumerate(self._chunks):
+                for i, b in enumerate(lv["ids"].tolist()):
+                    self._where[b] = (ci, i)
+        return self._where
+
+    def _make(self, ci, i):
+        lv, rank, deg, off, res = self._chunks[ci]
+        m, n, o = int(lv["m"][i]), int(lv["n"][i]), int(off[i])
+        if lv["kind"][i] == 1:
+            r = int(rank[i])
+            left = np.ndarray((m, r), np.float64, buffer=res, offset=8 * o, order="F")
+            right = np.ndarray((n, r), np.float64, buffer=res, offset=8 * (o + m * r),
+                               order="F")
+            return LowRank(left, right, degraded=bool(deg[i]))
+        return np.ndarray((m, n), np.float64, buffer=res, offset=8 * o, order="F")
+
+    def __missing__(self, key):
+        w = self._index().get(key)
+        if w is None:
+            raise KeyError(key)
+        v = self._make(*w)
+        super().__setitem__(key, v)
+        return v
+
+    def __contains__(self, key):
+        return key in self._index()
+
+    def _fill(self):
+        if self._filled:
+            return
+        for ci, (lv, *_rest) in enumerate(self._chunks):
+            for i, b in enumerate(lv["ids"].tolist()):
+                if not super().__contains__(b):
+                    super().__setitem__(b, self._make(ci, i))
+        self._filled = True
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __len__(self):
+        return len(self._index())
+
+    def keys(self):
+        self._fill()
+        return super().keys()
+
+    def values(self):
+        self._fill()
+        return super().values()
+
+    def items(self):
+        self._fill()
+        return super().items()
 
 
 # --------------------------------------------------------------------------- chunks
@@ -338,6 +414,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
+    marks = [("start", time.perf_counter())]
     dev_a = resident(h)
     if dev_a is not None:
         dev.set_operand(0, dev_ptr=dev_a[1], n=dev_a[2])
@@ -351,6 +428,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             dev.set_operand(1, dev_ptr=dev_b[1], n=dev_b[2])
         else:
             dev.set_operand(1, pool=pool_b)
+    marks.append(("operands", time.perf_counter()))
     comp = cfg.compressor
     pc = _lib.HxProductCfg(kind, eps, kmax, TAG_CODES[comp.tag], int(comp.seed) & (2**64 - 1),
                            int(sketch0), int(oversample))
@@ -408,7 +486,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                                                    _lib.ptr(off, _lib.i64p)), "hx_result_layout")
             res = None
             if fetch:
-                res = np.empty(max(int(st.out_elems), 1), dtype=np.float64)
+                res = _lib.pinned_empty(max(int(st.out_elems), 1))
                 _lib.check(_lib.lib().hx_result_download(ctx.h, _lib.ptr(res, _lib.f64p),
                                                          res.size), "hx_result_download")
             out.update(st=st, leaves=leaves, rank=rank, deg=deg, off=off, res=res,
@@ -450,8 +528,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         plan = make_plan(group)
     for t in inflight:
         t.join()
-    data, degraded = {}, set()
-    leaves_all, ranks_all, infos = [], [], []
+    marks.append(("products", time.perf_counter()))
+    degraded = set()
+    leaves_all, ranks_all, infos, fetched = [], [], [], []
     n_run = 0
     for out in chunks_out:
         if "err" in out:
@@ -460,19 +539,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         st, leaves, rank, deg, off, res = (out[k] for k in ("st", "leaves", "rank", "deg", "off",
                                                             "res"))
         if fetch:
-            nl = len(leaves["ids"])
-            ids, ms, ns = leaves["ids"].tolist(), leaves["m"].tolist(), leaves["n"].tolist()
-            kinds, rl, ol = leaves["kind"].tolist(), rank.tolist(), off.tolist()
-            for i in range(nl):
-                m, n, o = ms[i], ns[i], ol[i]
-                if kinds[i] == 1:
-                    r = rl[i]
-                    data[ids[i]] = LowRank(res[o:o + m * r].reshape(r, m).T,
-                                           res[o + m * r:o + (m + n) * r].reshape(r, n).T)
-                    if deg[i]:
-                        degraded.add(ids[i])
-                else:
-                    data[ids[i]] = res[o:o + m * n].reshape(n, m).T
+            fetched.append((leaves, rank, deg, off, res))
+            far_deg = (leaves["kind"] == 1) & (deg != 0)
+            degraded.update(leaves["ids"][far_deg].tolist())
         rep.degraded_blocks += int(st.degraded_blocks)
         rep.max_far_rank = max(rep.max_far_rank, int(st.max_far_rank))
         rep.matvec_count += int(st.matvec_count)
@@ -490,10 +559,14 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         leaves_all.append(leaves)
         ranks_all.append(rank)
         infos.append(out["info"])
+    marks.append(("unpack", time.perf_counter()))
+    if os.environ.get("HX_TIMING"):
+        print("[hx timing] " + " ".join(f"{b[0]} {1e3 * (b[1] - a[1]):.1f}ms"
+                                        for a, b in zip(marks, marks[1:])), flush=True)
     rep.chunks = n_run
     rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start
-    out = HMatrix(h.bct, data, degraded)
+    out = HMatrix(h.bct, _ProductLeaves(fetched) if fetch else {}, degraded)
     out.report = rep
     out.plan_info = _sum_info(infos)
     out.plan_leaves = ({key: np.concatenate([lv[key] for lv in leaves_all]) for key in
