@@ -183,11 +183,13 @@ class _ProductLeaves(dict):
         m, n, o = int(lv["m"][i]), int(lv["n"][i]), int(off[i])
         if lv["kind"][i] == 1:
             r = int(rank[i])
-            left = np.ndarray((m, r), np.float64, buffer=res, offset=8 * o, order="F")
-            right = np.ndarray((n, r), np.float64, buffer=res, offset=8 * (o + m * r),
-                               order="F")
-            return LowRank(left, right, degraded=bool(deg[i]))
-        return np.ndarray((m, n), np.float64, buffer=res, offset=8 * o, order="F")
+            # column-major views; shapes are the plan's, so LowRank's checks are skipped
+            x = object.__new__(LowRank)
+            object.__setattr__(x, "left", res[o:o + m * r].reshape(r, m).T)
+            object.__setattr__(x, "right", res[o + m * r:o + (m + n) * r].reshape(r, n).T)
+            object.__setattr__(x, "degraded", bool(deg[i]))
+            return x
+        return res[o:o + m * n].reshape(n, m).T
 
     def __missing__(self, key):
         w = self._index().get(key)
