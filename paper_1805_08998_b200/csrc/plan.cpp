@@ -229,17 +229,27 @@ struct Builder {
     return k;
   }
 
+  // Dense x dense pair evaluated on block tc x sc: the rows tc of D_pc times the columns sc
+  // of D_qc.  On ragged trees (leaves at different depths) a dense pair stays pending below
+  // its own blocks and arrives here as sub-views (HBlock.subview, hmatrix.py:257-258;
+  // _split_pair's dense branch, sumexpr.py:130-133): the views are column-major slices.
   void create_dxd(Walk& w, int tc, int sc, int pc, int qc) const {
     const int rho = t.sigma[pc];
     const int64_t m = sz(tc), n = sz(sc), kr = sz(rho);
     if (!isD(A, pc) || !isD(B, qc))
       throw hx::Unsupported("pending pair that is neither inner x inner nor dense x dense");
-    if (t.tau[pc] != tc || t.sigma[qc] != sc)
-      throw hx::Unsupported("dense sub-views (ragged cluster trees)");
-    w.o.terms.push_back(make_term(hx::BUF_A, A.d_off[pc], int32_t(m), 0, hx::BUF_B, B.d_off[qc],
+    const int tp = t.tau[pc], sq = t.sigma[qc];
+    if (lo(tc) < lo(tp) || lo(tc) + m > lo(tp) + sz(tp) || lo(sc) < lo(sq) ||
+        lo(sc) + n > lo(sq) + sz(sq) || t.tau[qc] != rho)
+      throw std::runtime_error("dense pair does not cover the block");
+    const int64_t a_off = A.d_off[pc] + (lo(tc) - lo(tp));
+    const int64_t b_off = B.d_off[qc] + (lo(sc) - lo(sq)) * kr;
+    w.o.terms.push_back(make_term(hx::BUF_A, a_off, int32_t(sz(tp)), 0, hx::BUF_B, b_off,
                                   int32_t(kr), 1, int32_t(kr), lo(tc), lo(sc), m, n));
     w.o.n_dxd++;
   }
+
+  bool dense_pair(int p, int q) const { return isD(A, p) && isD(B, q); }
 
   // --------------------------------------------------------------- the descent
   // Pending pairs of (virtual) block tc x sc split onto child (ti, si):
@@ -249,8 +259,14 @@ struct Builder {
     const int tcc = t.c_child[2 * tc + ti], scc = t.c_child[2 * sc + si];
     for (const auto& pq : pend) {
       const int p = pq.first, q = pq.second;
+      if (dense_pair(p, q)) {
+        // the middle cluster is a leaf and never splits: the pair goes down as is, its
+        // views narrowing with the output block (sumexpr.py:130-133)
+        sub.emplace_back(p, q);
+        continue;
+      }
       if (kind(p) != INNER || kind(q) != INNER)
-        throw hx::Unsupported("pending pair with a dense side above the leaf level");
+        throw hx::Unsupported("pending pair that is neither inner x inner nor dense x dense");
       for (int ri = 0; ri < 2; ++ri) {
         const int pc = child_of(p, ti, ri), qc = child_of(q, ri, si);
         if (pc < 0 || qc < 0) throw std::runtime_error("block tree is not level-conserving");
@@ -269,7 +285,7 @@ struct Builder {
               int64_t& K, double& fdd, double& edd) const {
     if (pend.empty()) return;
     if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0)
-      throw std::runtime_error("expand reached leaf clusters");
+      throw hx::Unsupported("H-block x dense pending pair at a leaf (ragged cluster trees)");
     Out& o = w.o;
     for (int ti = 0; ti < 2; ++ti)
       for (int si = 0; si < 2; ++si) {
@@ -392,13 +408,16 @@ struct Builder {
       int64_t Kc = 0;
       split_pairs(w, tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
       o.n_terms_real += int64_t(o.terms.size()) - gb;
-      // DxD pairs of a leaf at the leaf level join the leaf's own group
-      const bool leaf_level = kind(c) != INNER &&
-                              (t.c_child[2 * t.tau[c]] < 0 || t.c_child[2 * t.sigma[c]] < 0);
+      // DxD pairs of a leaf join the leaf's own group (on ragged trees as sub-views);
+      // inner x inner pairs of a leaf are expanded below
       double fdd = 0, edd = 0;
       PairList rest;
-      if (leaf_level) {
+      if (kind(c) != INNER) {
         for (const auto& pq : sub) {
+          if (!dense_pair(pq.first, pq.second)) {
+            rest.push_back(pq);
+            continue;
+          }
           create_dxd(w, t.tau[c], t.sigma[c], pq.first, pq.second);
           const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c])),
                        kk = double(sz(t.sigma[pq.first]));
@@ -426,8 +445,9 @@ struct Builder {
       } else {
         std::vector<VGroup> vg;
         int64_t K = w.path_K;
-        if (kind(c) == FAR) expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
-        else if (!rest.empty()) throw hx::Unsupported("near leaf above the leaf level");
+        // inner x inner pairs pending at a leaf (far, or near above the leaf level on a
+        // ragged tree) are expanded exactly over virtual sub-blocks
+        expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
         const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
         if (kind(c) == NEAR) {
           o.flops_near += fdd + 2.0 * mm * nn * double(K);

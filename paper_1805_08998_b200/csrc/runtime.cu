@@ -1162,8 +1162,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->est.ensure(size_t(std::max(na, 1)));
       auto gemm_batch = [&](int b, double* sums) {
         const size_t n = gm.count(b);
+        static const bool rshort = std::getenv("HX_RSHORT") != nullptr;
         if (n) launch_gemm(c, 64, c->xtiles.p + gm.cuts[size_t(b)], c->xgroups.p, c->xterms.p,
-                           int(n), bp, sums);
+                           int(n), bp, sums, nullptr, rshort);
       };
       auto gather_batch = [&](int b) {
         const size_t n = ga.count(b);

@@ -79,3 +79,4 @@ def test_plan_rejects_bad_arguments():
     rc = _lib.lib().hx_plan_create(None, None, None, None, 64, 0, C.byref(h))
     assert rc == -1
     assert "null" in _lib.last_error()
+
