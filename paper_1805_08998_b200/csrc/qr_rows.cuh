@@ -11,7 +11,7 @@
 // replaces q^2 reductions by q^2/32 transpose-reductions per panel.
 //
 //   qr_rows_warp_kernel  one warp per panel, panel in its shared-memory slice
-//   qr_rows_cta_kernel   one CTA (LA_THREADS) per panel, in shared memory when it fits,
+//   qr_rows_cta_kernel   one CTA (256-1024 threads) per panel, in shared memory when it fits,
 //                        else in place in HBM (coalesced: consecutive threads, consecutive rows)
 #pragma once
 #include <cstdint>
@@ -153,13 +153,15 @@ __global__ void qr_rows_warp_kernel(const QrJob* __restrict__ jobs, int n_jobs, 
   for (int64_t e = lane; e < n; e += 32) jb.X[e] = M[e];
 }
 
-// One CTA per panel; use_smem: stage the panel (p * q doubles) in dynamic shared memory.
-__global__ void __launch_bounds__(LA_THREADS, 2)
+// One CTA of NT threads per panel; use_smem: stage the panel (p * q doubles) in dynamic
+// shared memory.  Taller panels get more threads (one or two rows each).
+template <int NT>
+__global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1))
     qr_rows_cta_kernel(const QrJob* __restrict__ jobs, int use_smem) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ double tau_s[JAC_QMAX];
   __shared__ double wsum[32];
-  __shared__ double red[LA_THREADS];
+  __shared__ double red[NT];
   const QrJob jb = jobs[blockIdx.x];
   const int p = jb.p, q = jb.q;
   const int64_t n = int64_t(p) * q;
@@ -208,7 +210,7 @@ __device__ __forceinline__ double reg_pick(const double (&row)[QM], int j) {
 }
 
 template <int NW, int QM, int RPT>
-__global__ void __launch_bounds__(NW * 32) qr_reg_kernel(const QrJob* __restrict__ jobs) {
+__global__ void __launch_bounds__(NW * 32, NW == 1 ? 8 : 16 / NW) qr_reg_kernel(const QrJob* __restrict__ jobs) {
   constexpr int NT = NW * 32;
   __shared__ double red[NW][QM];
   __shared__ double wsum[QM];

@@ -429,7 +429,9 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
   if (!attr) {
     CK(cudaFuncSetAttribute(qr_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(SMEM_CAP)));
-    CK(cudaFuncSetAttribute(qr_rows_cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CK(cudaFuncSetAttribute(qr_rows_cta_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(SMEM_CAP)));
+    CK(cudaFuncSetAttribute(qr_rows_cta_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(SMEM_CAP)));
     attr = true;
   }
@@ -460,9 +462,12 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
       qr_rows_warp_kernel<<<(n + wpc - 1) / wpc, 32 * wpc, per * size_t(wpc), c->s>>>(
           c->qr_jobs.p + a, n, int(need));
     } else if (kind == 1) {
-      qr_rows_cta_kernel<<<n, LA_THREADS, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
+      if (all[a].p > 256)
+        qr_rows_cta_kernel<512><<<n, 512, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
+      else
+        qr_rows_cta_kernel<256><<<n, 256, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
     } else {
-      qr_rows_cta_kernel<<<n, LA_THREADS, 0, c->s>>>(c->qr_jobs.p + a, 0);
+      qr_rows_cta_kernel<512><<<n, 512, 0, c->s>>>(c->qr_jobs.p + a, 0);
     }
     CK(cudaGetLastError());
     c->launches++;
