@@ -289,21 +289,26 @@ def split_chunk(bct, group):
     return parts
 
 
-def chunk_groups(bct, n_chunks, first=1.0):
-    """About `n_chunks` chunks of consecutive units with equal leaf area (the first one
-    `first` times the others)."""
+def chunk_groups(bct, n_chunks, first=1.0, weights=None):
+    """About `n_chunks` chunks of consecutive units; chunk i gets a share of the leaf area
+    proportional to weights[i] (default: the first one `first`, the others 1)."""
     units = chunk_units(bct)
     total = sum(u[2] for u in units)
     n_chunks = max(1, n_chunks)
-    unit = total / (n_chunks - 1 + first) if n_chunks > 1 else total
+    if weights is None:
+        env = os.environ.get("HX_CHUNK_WEIGHTS")
+        if env and len(env.split(",")) == n_chunks:
+            weights = [float(x) for x in env.split(",")]
+        else:
+            weights = [first] + [1.0] * (n_chunks - 1)
+    bounds = np.cumsum(weights) / sum(weights) * total
     groups, cur, acc = [], [], 0.0
     for u in units:
         cur.append(u)
         acc += u[2]
-        target = unit * (first if not groups else 1.0)
-        if acc >= target and len(groups) < n_chunks - 1:
+        if len(groups) < n_chunks - 1 and acc >= bounds[len(groups)]:
             groups.append(cur)
-            cur, acc = [], 0.0
+            cur = []
     if cur:
         groups.append(cur)
     return groups
@@ -446,6 +451,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
+    timeline = []  # (what, host start, host end) for HX_TIMING
     iflags = implicit_flags(implicit_min)
 
     def make_plan(group):
@@ -458,7 +464,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         # device runs the previous batch
         p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile,
                       flags=_lib.Plan.DEFER | iflags)
-        plan_ms[0] += (time.perf_counter() - t0) * 1e3
+        t1 = time.perf_counter()
+        plan_ms[0] += (t1 - t0) * 1e3
+        timeline.append(("plan", t0, t1))
         return p
 
     queue_all = list(queue)
@@ -476,8 +484,10 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     def run_chunk(plan, ctx, out):
         try:
             st = _lib.HxProductStats()
+            t0 = time.perf_counter()
             _lib.check(_lib.lib().hx_product(ctx.h, plan.h, C.byref(pc), C.byref(st)),
                        "hx_product")
+            timeline.append(("product", t0, time.perf_counter()))
             leaves = plan.leaves()
             nl = len(leaves["ids"])
             rank = np.zeros(nl, np.int32)
@@ -565,6 +575,10 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     if os.environ.get("HX_TIMING"):
         print("[hx timing] " + " ".join(f"{b[0]} {1e3 * (b[1] - a[1]):.1f}ms"
                                         for a, b in zip(marks, marks[1:])), flush=True)
+        t00 = marks[0][1]
+        print("[hx timeline] " + " ".join(f"{w}:{1e3 * (a - t00):.0f}-{1e3 * (b - t00):.0f}"
+                                          for w, a, b in sorted(timeline, key=lambda x: x[1])),
+              flush=True)
     rep.chunks = n_run
     rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start
