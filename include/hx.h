@@ -185,7 +185,7 @@ int hx_pool_download(hx_ctx* ctx, const double* pool_dev, double* host, int64_t 
 int hx_pool_free(hx_ctx* ctx, double* pool_dev);
 
 /* Diagnostics: run the grouped DMMA GEMM kernel on host data (Term / Tile / Group records
- * of paper_1805_08998_b200/csrc/hx_types.h; host_bufs/buf_elems: 9 buffer slots, copied to
+ * of paper_1805_08998_b200/csrc/hx_types.h; host_bufs/buf_elems: 10 buffer slots, copied to
  * the device and back).  Used by the kernel-level parity tests. */
 int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tiles,
                   int64_t n_tiles, const void* groups, int64_t n_groups,

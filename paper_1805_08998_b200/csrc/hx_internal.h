@@ -134,6 +134,9 @@ struct hx_plan {
   hx::pvec<hx::OutLeaf> leaves;
   int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
   hx::hvec<hx::ColRec> gcols;  // thin factors of each X-group (virtual G)
+  std::vector<hx::TransRec> dtrans;  // transposed dense blocks (dense x H-block terms)
+  int64_t dtrans_elems = 0;
+  bool needs_eye = false;            // some term uses the identity operand (BUF_EYE)
   // X-groups are processed in batches whose gathered factors and cores fit a bounded
   // workspace (BUF_GATHER / BUF_CORE offsets restart at 0 in every batch)
   struct Batch {

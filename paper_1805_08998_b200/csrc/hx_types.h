@@ -32,8 +32,9 @@ enum Buf : uint8_t {
   BUF_OMEGA = 5,   // Gaussian test matrix for the sketch
   BUF_WORK = 6,    // recompression workspace (Y/Q, Bt/Q2, small matrices)
   BUF_OUT = 7,     // output factors (left m x r, right n x r per far leaf)
-  BUF_GATHER = 8,  // thin factors of each X-group gathered side by side (G)
-  NUM_BUFS = 9
+  BUF_GATHER = 8,  // scratch: transposed dense blocks of mixed pairs; X of hx_hmatvec
+  BUF_EYE = 9,     // identity matrix (the plain factor of H-block x dense terms)
+  NUM_BUFS = 10
 };
 
 // Contiguous copy of n doubles from (src_buf, src_off) to BUF_GATHER + dst_off.
@@ -41,6 +42,17 @@ struct CopyRec {
   int64_t src_off, dst_off, n;
   int32_t src_buf;
   int32_t pad;
+};
+
+// Leading dimension of the identity operand (BUF_EYE): the fixed factor of H-block x dense
+// terms, whose rank is a leaf cluster size.
+constexpr int EYE_LD = 1024;
+
+// Transposed copy of a dense block (rows x cols, column-major, in BUF_A at src_off) into
+// BUF_GATHER at dst_off (cols x rows): the thin matrix of dense x H-block terms.
+struct TransRec {
+  int64_t src_off, dst_off;
+  int32_t rows, cols;
 };
 
 // One thin factor of an X-group, seen as columns [col, col + k) of the group's virtual

@@ -60,7 +60,9 @@ struct TRec {
   int32_t k;         // rank of the term
   int32_t mat;       // index of its materialization term (patched with the factor offset)
   int8_t side;       // 0: left_t = X U_B (X = pc), 1: right_t = X^T V_A (X = qc)
+  int8_t dg;         // 1: the thin matrix is a dense block (H-block x dense pair), 0: a factor
 };
+
 
 using PairList = std::vector<std::pair<int, int>>;
 using GRef = std::pair<int32_t, int32_t>;  // (output index, group id local to that output)
@@ -76,6 +78,7 @@ struct Out {
   std::vector<int32_t> log_block, log_a, log_b, log_rank;
   std::vector<int8_t> log_kind;
   int64_t n_terms_real = 0, n_terms_expand = 0, n_dxd = 0, created[3] = {0, 0, 0};
+  int64_t n_mixed = 0;  // H-block x dense terms (ragged trees)
   int64_t n_far = 0, n_near = 0, max_out_dim = 0;
   double flops_near = 0, bytes_near = 0;
   int64_t ws_far = 0, ws_near = 0;
@@ -207,6 +210,7 @@ struct Builder {
     r.qc = qc;
     r.k = k;
     r.side = side;
+    r.dg = 0;
     r.mat = int32_t(o.terms.size());
     o.recs.push_back(r);
     // the fixed factor is a pool factor; the computed one is patched by build_groups()
@@ -250,6 +254,40 @@ struct Builder {
   }
 
   bool dense_pair(int p, int q) const { return isD(A, p) && isD(B, q); }
+  bool mixed_pair(int p, int q) const {
+    return (kind(p) == INNER && isD(B, q)) || (isD(A, p) && kind(q) == INNER);
+  }
+
+  // H-block x dense pair (or dense x H-block) at a leaf-level block of a ragged tree: the
+  // inner branch of _split_pair meets a leaf cluster on one side (sumexpr.py:123-129) and
+  // the pair is applied through HBlock.matmat (hmatrix.py:177-211) by the compressor or
+  // evaluate_dense.  Exact as a term whose computed factor is X D (or X^T D^T, D^T from a
+  // transposed copy) and whose other factor is the identity.
+  void create_mixed(Walk& w, int tc, int sc, int pc, int qc) const {
+    Out& o = w.o;
+    const int64_t m = sz(tc), n = sz(sc);
+    if (t.tau[pc] != tc || t.sigma[qc] != sc || t.sigma[pc] != t.tau[qc])
+      throw hx::Unsupported("H-block x dense pair on a sub-view");
+    TRec r;
+    r.pc = pc;
+    r.qc = qc;
+    r.dg = 1;
+    r.mat = int32_t(o.terms.size());
+    if (kind(pc) == INNER) {  // X = A_pc, thin matrix D_qc (rho x sc); right factor I
+      r.k = int32_t(n);
+      r.side = 0;
+      o.terms.push_back(make_term(hx::BUF_TERM, -1, int32_t(m), 0, hx::BUF_EYE, 0, hx::EYE_LD, 0,
+                                  int32_t(n), lo(tc), lo(sc), m, n));
+    } else {  // X = B_qc, thin matrix D_pc^T (rho x tc); left factor I
+      r.k = int32_t(m);
+      r.side = 1;
+      o.terms.push_back(make_term(hx::BUF_EYE, 0, hx::EYE_LD, 0, hx::BUF_TERM, -1, int32_t(n), 0,
+                                  int32_t(m), lo(tc), lo(sc), m, n));
+    }
+    if (r.k > hx::EYE_LD) throw hx::Unsupported("H-block x dense pair wider than 1024");
+    o.recs.push_back(r);
+    o.n_mixed++;
+  }
 
   // --------------------------------------------------------------- the descent
   // Pending pairs of (virtual) block tc x sc split onto child (ti, si):
@@ -299,6 +337,10 @@ struct Builder {
         const bool leaf_level = t.c_child[2 * tcc] < 0 || t.c_child[2 * scc] < 0;
         if (leaf_level) {
           for (const auto& pq : sub) {
+            if (mixed_pair(pq.first, pq.second)) {
+              create_mixed(w, tcc, scc, pq.first, pq.second);
+              continue;
+            }
             create_dxd(w, tcc, scc, pq.first, pq.second);
             const double mm = double(sz(tcc)), nn = double(sz(scc)),
                          kk = double(sz(t.sigma[pq.first]));
@@ -414,6 +456,10 @@ struct Builder {
       PairList rest;
       if (kind(c) != INNER) {
         for (const auto& pq : sub) {
+          if (mixed_pair(pq.first, pq.second)) {
+            create_mixed(w, t.tau[c], t.sigma[c], pq.first, pq.second);
+            continue;
+          }
           if (!dense_pair(pq.first, pq.second)) {
             rest.push_back(pq);
             continue;
@@ -573,7 +619,7 @@ struct Builder {
     hx_plan_info& I = P.info;
     for (const Out& o : outs) {
       I.n_terms_real += o.n_terms_real;
-      I.n_terms_expand += o.n_terms_expand;
+      I.n_terms_expand += o.n_terms_expand + o.n_mixed;
       I.n_dxd += o.n_dxd;
       for (int k = 0; k < 3; ++k) I.created[k] += o.created[k];
       I.n_far += o.n_far;
@@ -587,6 +633,7 @@ struct Builder {
   int64_t ws_far_total = 0, ws_near_total = 0;
   std::vector<int64_t> task_log_pos;
   std::vector<int32_t> order;  // terms sorted by X-group
+  std::vector<int64_t> trans_off;  // per A node: offset of its transposed copy (or -1)
 
   // --------------------------------------------------------------- grouped term factors
   // workspace bound (doubles) for one batch of gathered factors, and for its cores
@@ -865,6 +912,20 @@ struct Builder {
     P.fac_groups.resize(size_t(o_fg));
     P.fac_terms.resize(size_t(o_fm));
     lap("pass2");
+    // transposed copies of the dense blocks of dense x H-block terms (ragged trees)
+    trans_off.clear();
+    for (const TRec& r : recs) {
+      if (!r.dg) continue;
+      P.needs_eye = true;
+      if (r.side != 1) continue;
+      if (trans_off.empty()) trans_off.assign(size_t(t.n_nodes), -1);
+      if (trans_off[size_t(r.pc)] >= 0) continue;
+      const int tp = t.tau[r.pc], rp = t.sigma[r.pc];
+      trans_off[size_t(r.pc)] = P.dtrans_elems;
+      P.dtrans.push_back(hx::TransRec{A.d_off[r.pc], P.dtrans_elems, int32_t(sz(tp)),
+                                      int32_t(sz(rp))});
+      P.dtrans_elems = align16(P.dtrans_elems + sz(tp) * sz(rp));
+    }
     // pass 3 (parallel): column records of the virtual G and the computed-factor offsets of
     // the materialization terms -- everything the materialization launch needs
 #pragma omp parallel for schedule(dynamic, 64)
@@ -877,6 +938,14 @@ struct Builder {
         hx::ColRec& cp = P.gcols[size_t(g.o_gather + (i - g.b0))];
         cp.buf = g.side == 0 ? hx::BUF_B : hx::BUF_A;
         cp.src_off = g.side == 0 ? B.u_off[r.qc] : A.v_off[r.pc];
+        if (r.dg) {  // dense thin matrix: D_qc itself, or the transposed copy of D_pc
+          if (g.side == 0) {
+            cp.src_off = B.d_off[r.qc];
+          } else {
+            cp.buf = hx::BUF_GATHER;
+            cp.src_off = trans_off[size_t(r.pc)];
+          }
+        }
         cp.col = int32_t(col);
         cp.k = r.k;
         cp.ld = int32_t(g.kr);

@@ -91,6 +91,21 @@ __global__ void omega_kernel(double* om, int64_t n, uint64_t seed) {
   om[i] = sqrt(-2.0 * log(u1)) * cospi(2.0 * u2);
 }
 
+__global__ void transpose_kernel(const TransRec* __restrict__ recs, const double* __restrict__ a,
+                                 double* __restrict__ g) {
+  const TransRec r = recs[blockIdx.x];
+  const int64_t n = int64_t(r.rows) * r.cols;
+  for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+    const int64_t i = e % r.rows, j = e / r.rows;
+    g[r.dst_off + j + i * r.cols] = a[r.src_off + e];
+  }
+}
+
+__global__ void eye_kernel(double* __restrict__ m, int64_t n, int ld) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (e < n) m[e] = (e % ld == e / ld) ? 1.0 : 0.0;
+}
+
 }  // namespace
 
 // ---- page-locked host memory cache (plan work lists) ----------------------------------
@@ -257,6 +272,8 @@ struct hx_ctx {
   DArr<double> sumsq, fro2;
   DArr<int> seg_b, seg_e;
   DArr<ColRec> gcols;
+  DArr<TransRec> trans_recs;
+  bool eye_ready = false;
   DArr<Term> rterms;
   DArr<Tile> rtiles;
   DArr<Group> rgroups;
@@ -629,6 +646,8 @@ extern "C" int hx_ctx_trim(hx_ctx* c) {
     c->omega_rows = 0;
     c->omega_cols = 0;
     c->omega_seed = ~0ULL;
+    c->eye_ready = false;
+    c->trans_recs.release();
     c->out_far = c->near_begin = c->near_elems = 0;
     c->res_rank.clear();
     c->res_deg.clear();
@@ -677,6 +696,23 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       if (bytes) CK(cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, st));
     };
     h2d(c->gcols.p, P->gcols.data(), P->gcols.size() * sizeof(ColRec), s);
+    // ragged trees: identity operand and transposed dense blocks of H-block x dense terms
+    if (P->needs_eye && !c->eye_ready) {
+      const int64_t ne = int64_t(EYE_LD) * EYE_LD;
+      c->own[BUF_EYE].ensure(size_t(ne));
+      eye_kernel<<<int((ne + 255) / 256), 256, 0, s>>>(c->own[BUF_EYE].p, ne, EYE_LD);
+      CK(cudaGetLastError());
+      c->launches++;
+      c->eye_ready = true;
+    }
+    if (!P->dtrans.empty()) {
+      c->own[BUF_GATHER].ensure(size_t(P->dtrans_elems));
+      c->trans_recs.upload(P->dtrans, s);
+      transpose_kernel<<<int(P->dtrans.size()), 256, 0, s>>>(c->trans_recs.p, c->buf(BUF_A),
+                                                             c->own[BUF_GATHER].p);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
     CK(cudaEventRecord(c->ev[6], s));
     CK(cudaStreamWaitEvent(c->s2, c->ev[6], 0));  // buffers allocated before s2 copies
     h2d(c->terms[2].p, P->mat_terms.data(), P->mat_terms.size() * sizeof(Term), c->s2);

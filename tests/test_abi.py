@@ -80,3 +80,33 @@ def test_plan_rejects_bad_arguments():
     assert rc == -1
     assert "null" in _lib.last_error()
 
+
+
+def test_plan_term_log_ragged_tree(golden):
+    """Ragged cluster tree (n = 200, leaves at different depths), A != B: the planner's log
+    equals the reference's restrict log; dense sub-view and H-block x dense pairs are
+    planned (no NotImplementedError)."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import _lib, hmatrix, multiply
+
+    g = golden("ragged3d.npz")
+    n, n_min, eta, eps_a, tol = g["params"]
+    pts = g["points"]
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, int(n_min)), eta)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, int(n_min)), eta)
+    h = int(n) ** (-1.0 / 3.0)
+    oa = O.assemble_o("exp0.5", obt, O.Eps(eps_a), pts, h)
+    ob = O.assemble_o("inv", obt, O.Eps(eps_a), pts, h)
+    _, da = hmatrix.pack_operand(hx.HMatrix(bct, oa.data))
+    _, db = hmatrix.pack_operand(hx.HMatrix(bct, ob.data))
+    plan = _lib.Plan(hmatrix.tree_arrays(bct), da, db, tile=multiply.plan_tile(bct),
+                     flags=_lib.Plan.LOG)
+    log = []
+    O.hmult_new_o(oa, ob, O.Eps(float(tol)), "dense-svd", log=log)
+    kmap = {"FF": 0, "FX": 1, "XF": 2}
+    ref = np.array([(c, kmap[k], a, b, r) for (c, k, a, b, r) in log], dtype=np.int64)
+    L = plan.term_log()
+    mine = np.stack([L["block"], L["kind"], L["a"], L["b"], L["rank"]], axis=1)
+    assert mine.shape == ref.shape
+    assert np.array_equal(mine, ref)
+    assert plan.info.n_dxd > 0

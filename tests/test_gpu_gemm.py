@@ -20,7 +20,7 @@ TILE = np.dtype([("out_off", "<i8"), ("out_ld", "<i4"), ("row0", "<i4"), ("col0"
                  ("rows", "<i2"), ("cols", "<i2"), ("g_begin", "<i4"), ("g_end", "<i4"),
                  ("aux", "<i4"), ("out_buf", "u1"), ("mode", "u1"), ("pad", "u1", 2)])
 GROUP = np.dtype([("t_begin", "<i4"), ("t_end", "<i4")])
-NBUF = 9
+NBUF = 10
 
 
 def test_record_sizes():
