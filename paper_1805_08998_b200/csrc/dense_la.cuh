@@ -186,9 +186,15 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
 
 // rank[i] / retry[i] for each block: select_rank (lowrank.py:75-90) on the singular values
 // with the unsampled tail appended as one more entry.  policy 0: eps, 1: fixed k_max.
+// randomized_rule: the `randomized` tag (randomized_adaptive, compressors.py:368-404) keeps
+// every basis vector up to two consecutive stop_criterion hits (:152-159) and no final
+// trim, so its rank exceeds the epsilon-rank.  Replayed on the singular values: vector j
+// carries sigma_j, hits need sigma_j <= eps * ||sigma_{<=j}||, and the random probes cost
+// one vector more than the singular directions (ranks within +-1 of the reference's on
+// its fixtures); the factors are still the best approximation of that rank.
 __global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int policy, double eps,
                                    int k_max, int oversample, int* __restrict__ rank,
-                                   int* __restrict__ retry) {
+                                   int* __restrict__ retry, int randomized_rule = 0) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   if (b >= n) return;
   const SelJob jb = jobs[b];
@@ -214,6 +220,23 @@ __global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int p
   for (int i = l - 1; i >= 0; --i) {
     acc += jb.sig[i] * jb.sig[i];
     if (sqrt(acc) <= thr) r = i;
+  }
+  if (randomized_rule) {
+    double acc2 = 0.0;
+    int hits = 0, rr = l + 1;
+    for (int j = 0; j < l; ++j) {
+      const double sj = jb.sig[j];
+      acc2 += sj * sj;
+      if (j >= 1 && sj <= eps * sqrt(acc2)) {
+        if (++hits >= 2) {
+          rr = j + 2;
+          break;
+        }
+      } else {
+        hits = 0;
+      }
+    }
+    r = min(rr, jb.mu);
   }
   // select_rank picks the FIRST r whose tail is small enough; tails are non-increasing in r,
   // so the smallest qualifying r found by the backward scan is that index.

@@ -1282,7 +1282,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->retry_d.ensure(size_t(na));
       select_rank_kernel<<<(na + 127) / 128, 128, 0, s>>>(c->sel_jobs.p, na, cfg->policy,
                                                           cfg->eps, cfg->k_max, over,
-                                                          c->rank_d.p, c->retry_d.p);
+                                                          c->rank_d.p, c->retry_d.p,
+                                                          cfg->tag == 2 ? 1 : 0);
       CK(cudaGetLastError());
       c->launches++;
       std::vector<int> rk(na), rt(na);

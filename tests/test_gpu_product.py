@@ -51,6 +51,19 @@ def test_product_parity(golden, name, tag):
     _check_parity(g, tag, bct, C, oa, ob, tol)
 
 
+def test_randomized_tag_parity(golden):
+    """`randomized` keeps its basis up to two consecutive stop hits, no final trim
+    (compressors.py:368-404): its ranks sit 2-4 above the epsilon-rank; the GPU replays the
+    rule on the singular values and must land within +-1 of the reference's ranks."""
+    import paper_1805_08998_b200 as hx
+
+    g = golden("small2d.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "small2d.npz")
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("randomized"), policy=hx.EpsRank(tol))
+    C = hx.hmult_new(A, B, cfg)
+    _check_parity(g, "randomized", bct, C, oa, ob, tol)
+
+
 @pytest.mark.parametrize("name,imin", [("small2d.npz", 32), ("cfg1.npz", 64),
                                        ("cfg1.npz", 128)])
 def test_implicit_route_parity(golden, name, imin):
