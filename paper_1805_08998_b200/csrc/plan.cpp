@@ -116,6 +116,10 @@ struct Builder {
   hx::pvec<TRec> recs;
   bool logging = false;  // HX_PLAN_LOG: keep the restrict log (parity tests)
   int64_t implicit_min = 0;  // far leaves with min(m, n) >= this take the implicit route
+  // sketch width assumed by the implicit route's per-term choice (HX_SKETCH_COLS; 0 sketches
+  // every sub-block term, the fully implicit route)
+  double sketch_cols = std::getenv("HX_SKETCH_COLS") ? std::atof(std::getenv("HX_SKETCH_COLS"))
+                                                     : 56.0;
 
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
@@ -380,14 +384,34 @@ struct Builder {
     L.tile_begin = int32_t(o.tiles.size());
     L.sumsq_begin = o.n_sumsq;
     // implicit route: the terms inherited from the root path (full-leaf extent, most of the
-    // stacked rank of a large leaf) are only sketched; the tiles materialize the sub-block
-    // terms of the leaf (pending-pair expansions, small extents) into T_sub
+    // stacked rank of a large leaf) and the sub-block terms on large sub-blocks are only
+    // sketched -- a term on an h x w extent costs ~4 (h + w) L flops per unit of rank to
+    // sketch (range and co-range passes, L ~ 56 columns) against 2 h w to materialize; the
+    // tiles materialize the remaining small sub-block terms into T_sub (none: no T_sub)
     const bool impl = far && implicit_min > 0 && std::min(m, n) >= implicit_min;
+    auto sketched = [this](const VGroup& v) {
+      const double h = double(v.r1 - v.r0), wd = double(v.c1 - v.c0);
+      return h * wd >= 4.0 * sketch_cols * (h + wd);
+    };
+    bool tsub = !impl;
     if (impl) {
       L.implicit = 1;
       L.g_begin = int32_t(o.tile_groups.size());
       o.tile_groups.insert(o.tile_groups.end(), w.path.begin(), w.path.end());
+      for (const VGroup& v : vg) {
+        if (sketched(v))
+          o.tile_groups.push_back(v.g);
+        else
+          tsub = true;
+      }
       L.g_end = int32_t(o.tile_groups.size());
+    }
+    if (!tsub) {  // everything is sketched: no tiles, no m x n workspace
+      L.tile_end = L.tile_begin;
+      L.sumsq_end = L.sumsq_begin;
+      o.max_out_dim = std::max<int64_t>(o.max_out_dim, std::max(m, n));
+      o.leaves.push_back(L);
+      return;
     }
     ws = align16(ws + m * n);
     int32_t prev_gb = -1, prev_ge = -1;
@@ -401,7 +425,8 @@ struct Builder {
         else
           cur.assign(w.path.begin(), w.path.end());
         for (const VGroup& v : vg)
-          if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0) cur.push_back(v.g);
+          if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0 && !(impl && sketched(v)))
+            cur.push_back(v.g);
         int32_t gb, ge;
         if (cur == prev) {
           gb = prev_gb;

@@ -1070,11 +1070,12 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             y.r_lo = x.t.r_lo;
             ts.push_back(y);
           }
-          // + T_sub Omega (the materialized sub-block terms)
-          Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1, f.n,
-                      f.m, l + PR);
-          y.r_lo = int32_t(L.row0);
-          ts.push_back(y);
+          if (L.tile_end > L.tile_begin) {  // + T_sub Omega (the materialized sub-blocks)
+            Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
+                        f.n, f.m, l + PR);
+            y.r_lo = int32_t(L.row0);
+            ts.push_back(y);
+          }
           const int32_t g = gm.group(ts.data(), ts.size());
           gm.cover(g, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0);
         } else {
@@ -1160,10 +1161,11 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             y.r_lo = x.t.c_lo;
             ts.push_back(y);
           }
-          // + T_sub^T Q
-          Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
-          y.r_lo = int32_t(L.col0);
-          ts.push_back(y);
+          if (L.tile_end > L.tile_begin) {  // + T_sub^T Q
+            Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
+            y.r_lo = int32_t(L.col0);
+            ts.push_back(y);
+          }
           const int32_t g = gm.group(ts.data(), ts.size());
           gm.cover(g, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0);
         } else {

@@ -83,6 +83,22 @@ def test_implicit_route_parity(golden, name, imin):
     _check_parity(g, "dense-svd", bct, C, oa, ob, tol)
 
 
+@pytest.mark.parametrize("name,imin", [("small2d.npz", 32), ("cfg1.npz", 64),
+                                       ("ragged3d.npz", 32)])
+def test_fully_implicit_route_parity(golden, monkeypatch, name, imin):
+    """Every term of the implicit leaves sketched, sub-block terms included (partial K
+    ranges in the gathered rows, dense pieces as plain tiles): no T_sub at all."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import multiply
+
+    monkeypatch.setenv("HX_SKETCH_COLS", "0")
+    g = golden(name)
+    bct, A, B, oa, ob, tol = _operands(g, name)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    C = multiply.multiply_device(A, B, cfg, implicit_min=imin)
+    _check_parity(g, "dense-svd", bct, C, oa, ob, tol)
+
+
 def _check_parity(g, tag, bct, C, oa, ob, tol):
     import paper_1805_08998_b200 as hx
 
