@@ -119,7 +119,7 @@ std::unordered_set<void*>& g_unpinned() {
   return s;
 }
 constexpr size_t PIN_MIN = size_t(1) << 20;        // below: ordinary heap
-constexpr size_t PIN_CACHE_MAX = size_t(8) << 30;  // cached bytes kept for reuse
+constexpr size_t PIN_CACHE_MAX = size_t(32) << 30;  // cached bytes kept for reuse (pinning GBs costs ~1 s)
 size_t pin_cap(size_t bytes) {
   size_t c = PIN_MIN;
   while (c < bytes) c <<= 1;
