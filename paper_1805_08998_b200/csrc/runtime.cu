@@ -262,6 +262,7 @@ struct hx_ctx {
   // high-priority stream for the latency-bound recompression: when two contexts run
   // consecutive chunks, its small launches get SMs ahead of the other chunk's formation
   cudaStream_t s_hi = nullptr;
+  cudaStream_t s3 = nullptr;  // second formation stream (odd batches)
   DArr<double> own[NUM_BUFS];
   double* attached[2] = {nullptr, nullptr};
   int64_t opnd_elems[2] = {0, 0};
@@ -322,8 +323,10 @@ namespace {
 
 void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, const Term* terms,
                  int n_tiles, const BufPtrs& bp, double* sumsq,
-                 const ColRec* gcols = nullptr, bool short_k = false) {
+                 const ColRec* gcols = nullptr, bool short_k = false,
+                 cudaStream_t stream = nullptr) {
   if (n_tiles <= 0) return;
+  cudaStream_t st = stream ? stream : c->s;
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(grouped_gemm_kernel<Gemm64>,
@@ -336,13 +339,13 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
   }
   static const bool use_short = !std::getenv("HX_NO_SHORTK");
   if (tile == 64 && short_k && use_short)
-    grouped_gemm_kernel<Gemm64s><<<n_tiles, Gemm64s::THREADS, Gemm64s::SMEM, c->s>>>(
+    grouped_gemm_kernel<Gemm64s><<<n_tiles, Gemm64s::THREADS, Gemm64s::SMEM, st>>>(
         tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   else if (tile == 32)
-    grouped_gemm_kernel<Gemm32><<<n_tiles, Gemm32::THREADS, Gemm32::SMEM, c->s>>>(
+    grouped_gemm_kernel<Gemm32><<<n_tiles, Gemm32::THREADS, Gemm32::SMEM, st>>>(
         tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   else
-    grouped_gemm_kernel<Gemm64><<<n_tiles, Gemm64::THREADS, Gemm64::SMEM, c->s>>>(
+    grouped_gemm_kernel<Gemm64><<<n_tiles, Gemm64::THREADS, Gemm64::SMEM, st>>>(
         tiles, groups, terms, bp, sumsq, n_tiles, gcols);
   CK(cudaGetLastError());
   c->launches++;
@@ -556,6 +559,7 @@ extern "C" int hx_ctx_create(int device, hx_ctx** out) {
     int lo_prio = 0, hi_prio = 0;
     CK(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
     CK(cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi_prio));
+    CK(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
     *out = c;
     return HX_OK;
@@ -725,28 +729,48 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     // ---- 1. term formation: gather thin factors per X-group, cores, X G products.
     // Deferred plans fill each batch's work lists here, on the host, while the device
     // runs the previous batch.
+    // Consecutive batches are independent (different X-groups): odd batches run on a
+    // second stream with their own copy of the core workspace, so one batch's X G bands
+    // overlap the next batch's cores.
+    const bool two = P->batches.size() > 1 && !std::getenv("HX_ONE_FORM_STREAM");
+    BufPtrs bp_odd = bp;
+    if (two) {
+      c->own[BUF_CORE].ensure(size_t(2 * P->core_elems));
+      bp = c->ptrs();
+      bp_odd = bp;
+      bp_odd.p[BUF_CORE] = bp.p[BUF_CORE] + P->core_elems;
+      CK(cudaEventRecord(c->ev[6], s));
+      CK(cudaStreamWaitEvent(c->s3, c->ev[6], 0));
+    }
     for (size_t bi = 0; bi < P->batches.size(); ++bi) {
       if (!P->batch_ready[bi]) {
         P->fill_batch(int64_t(bi));
         P->batch_ready[bi] = 1;
       }
       const hx_plan::Batch& bt = P->batches[bi];
+      const bool odd = two && (bi & 1);
+      const cudaStream_t fs = odd ? c->s3 : s;
+      const BufPtrs& fbp = odd ? bp_odd : bp;
       h2d(c->tiles[0].p + bt.core_begin, P->core_tiles.data() + bt.core_begin,
-          size_t(bt.core_end - bt.core_begin) * sizeof(Tile), s);
+          size_t(bt.core_end - bt.core_begin) * sizeof(Tile), fs);
       h2d(c->groups[0].p + bt.cg_begin, P->core_groups.data() + bt.cg_begin,
-          size_t(bt.cg_end - bt.cg_begin) * sizeof(Group), s);
+          size_t(bt.cg_end - bt.cg_begin) * sizeof(Group), fs);
       h2d(c->terms[0].p + bt.cm_begin, P->core_terms.data() + bt.cm_begin,
-          size_t(bt.cm_end - bt.cm_begin) * sizeof(Term), s);
+          size_t(bt.cm_end - bt.cm_begin) * sizeof(Term), fs);
       h2d(c->tiles[1].p + bt.fac_begin, P->fac_tiles.data() + bt.fac_begin,
-          size_t(bt.fac_end - bt.fac_begin) * sizeof(Tile), s);
+          size_t(bt.fac_end - bt.fac_begin) * sizeof(Tile), fs);
       h2d(c->groups[1].p + bt.fg_begin, P->fac_groups.data() + bt.fg_begin,
-          size_t(bt.fg_end - bt.fg_begin) * sizeof(Group), s);
+          size_t(bt.fg_end - bt.fg_begin) * sizeof(Group), fs);
       h2d(c->terms[1].p + bt.fm_begin, P->fac_terms.data() + bt.fm_begin,
-          size_t(bt.fm_end - bt.fm_begin) * sizeof(Term), s);
+          size_t(bt.fm_end - bt.fm_begin) * sizeof(Term), fs);
       launch_gemm(c, P->tile, c->tiles[0].p + bt.core_begin, c->groups[0].p, c->terms[0].p,
-                  int(bt.core_end - bt.core_begin), bp, nullptr, c->gcols.p, true);
+                  int(bt.core_end - bt.core_begin), fbp, nullptr, c->gcols.p, true, fs);
       launch_gemm(c, P->tile, c->tiles[1].p + bt.fac_begin, c->groups[1].p, c->terms[1].p,
-                  int(bt.fac_end - bt.fac_begin), bp, nullptr, c->gcols.p, true);
+                  int(bt.fac_end - bt.fac_begin), fbp, nullptr, c->gcols.p, true, fs);
+    }
+    if (two) {
+      CK(cudaEventRecord(c->ev[6], c->s3));
+      CK(cudaStreamWaitEvent(s, c->ev[6], 0));
     }
     CK(cudaEventRecord(c->ev[1], s));
     // ---- 2. materialization
@@ -1659,6 +1683,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   cudaStreamDestroy(c->s);
   cudaStreamDestroy(c->s2);
   cudaStreamDestroy(c->s_hi);
+  cudaStreamDestroy(c->s3);
   delete c;
 }
 
