@@ -157,7 +157,12 @@ typedef struct hx_product_stats {
   double fro2_total;     /* sum of squared Frobenius norms of all output blocks     */
   double dom_kernel_ms;  /* summed device time of the materialization launches      */
   double ms_upload;      /* H2D of the plan's work lists (inside ms_total)          */
+  double t_marks[4];     /* start, formation end, materialization end, end: ms after the
+                          * device epoch (hx_timeline_epoch), -1 without an epoch    */
 } hx_product_stats;
+
+/* Records the device epoch the t_marks of later products are measured from. */
+int hx_timeline_epoch(void);
 
 int hx_product(hx_ctx* ctx, hx_plan* plan, const hx_product_cfg* cfg,
                hx_product_stats* stats);

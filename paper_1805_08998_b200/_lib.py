@@ -56,7 +56,8 @@ class HxProductStats(C.Structure):
         (name, C.c_int64) for name in ("far_leaves", "near_leaves", "degraded_blocks",
                                        "max_far_rank", "matvec_count", "sketch_rounds",
                                        "launches", "out_elems")] + [
-        ("fro2_total", C.c_double), ("dom_kernel_ms", C.c_double), ("ms_upload", C.c_double)]
+        ("fro2_total", C.c_double), ("dom_kernel_ms", C.c_double), ("ms_upload", C.c_double),
+        ("t_marks", C.c_double * 4)]
 
 
 class HxError(RuntimeError):
@@ -89,6 +90,7 @@ SIGNATURES = {
     "hx_ctx_trim": [C.c_void_p],
     "hx_ctx_operand_share": [C.c_void_p, C.c_void_p],
     "hx_ctx_held_bytes": [C.c_void_p],
+    "hx_timeline_epoch": [],
     "hx_host_alloc": [C.c_int64],
     "hx_host_free": [C.c_void_p, C.c_int64],
     "hx_host_register": [C.c_void_p, C.c_int64],

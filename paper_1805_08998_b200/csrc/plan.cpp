@@ -535,14 +535,15 @@ struct Builder {
   }
 
   int choose_cut() const {
-    // first block level holding enough inner blocks to keep every thread busy
+    // first block level holding enough owned inner blocks to keep every thread busy (a
+    // masked plan -- one chunk, one rank -- owns only part of each level)
     const int want = 8 * std::max(1, omp_get_max_threads());
     std::vector<int> level_nodes{0}, next;
     for (int level = 0; level < 64 && !level_nodes.empty(); ++level) {
       int inner = 0;
       next.clear();
       for (int b : level_nodes)
-        if (kind(b) == INNER) {
+        if (kind(b) == INNER && owned_sub[size_t(b)]) {
           ++inner;
           for (int c = 0; c < 4; ++c)
             if (t.child[4 * b + c] >= 0) next.push_back(t.child[4 * b + c]);
@@ -784,33 +785,42 @@ struct Builder {
     const int nk = 2 * nn;
     const int nth = std::max(1, std::min(omp_get_max_threads(), int(nr / 65536) + 1));
     std::vector<int32_t> hist(size_t(nth) * size_t(nk), 0);
+    std::vector<int32_t> block_sum(size_t(nth), 0);
     order.resize(nr);
 #pragma omp parallel num_threads(nth)
     {
+      const int nth = omp_get_num_threads();  // the team actually granted
       const int th = omp_get_thread_num();
       const size_t a = nr * size_t(th) / size_t(nth), e = nr * size_t(th + 1) / size_t(nth);
       int32_t* h = &hist[size_t(th) * size_t(nk)];
       for (size_t i = a; i < e; ++i) h[key(recs[i])]++;
 #pragma omp barrier
-#pragma omp single
-      {
-        int32_t run = 0;
-        for (int k = 0; k < nk; ++k) {
-          cnt[size_t(k)] = run;
-          for (int q = 0; q < nth; ++q) {
-            int32_t& x = hist[size_t(q) * size_t(nk) + size_t(k)];
-            const int32_t c = x;
-            x = run;
-            run += c;
-          }
+      // (key, thread)-ordered exclusive prefix, in parallel over key blocks
+      const int kb0 = int(int64_t(nk) * th / nth), kb1 = int(int64_t(nk) * (th + 1) / nth);
+      int32_t bsum = 0;
+      for (int k = kb0; k < kb1; ++k)
+        for (int q = 0; q < nth; ++q) bsum += hist[size_t(q) * size_t(nk) + size_t(k)];
+      block_sum[size_t(th)] = bsum;
+#pragma omp barrier
+      int32_t run = 0;
+      for (int q = 0; q < th; ++q) run += block_sum[size_t(q)];
+      for (int k = kb0; k < kb1; ++k) {
+        cnt[size_t(k)] = run;
+        for (int q = 0; q < nth; ++q) {
+          int32_t& x = hist[size_t(q) * size_t(nk) + size_t(k)];
+          const int32_t c = x;
+          x = run;
+          run += c;
         }
-        cnt[size_t(nk)] = run;
       }
+      if (th == nth - 1) cnt[size_t(nk)] = run;
+#pragma omp barrier
       for (size_t i = a; i < e; ++i) order[size_t(h[key(recs[i])]++)] = int32_t(i);
     }
     lap("order");
     std::vector<int32_t> gpos(size_t(nk) + 1, 0);
     for (int g = 0; g < nk; ++g) gpos[size_t(g) + 1] = gpos[size_t(g)] + (cnt[g] != cnt[g + 1]);
+    // (a sequential pass of nk adds: cheap next to the histogram work)
     G.clear();
     G.resize(size_t(gpos[size_t(nk)]));
 #pragma omp parallel for schedule(static)

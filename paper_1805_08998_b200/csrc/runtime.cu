@@ -106,7 +106,19 @@ __global__ void eye_kernel(double* __restrict__ m, int64_t n, int ld) {
   if (e < n) m[e] = (e % ld == e / ld) ? 1.0 : 0.0;
 }
 
+cudaEvent_t g_epoch;
+bool g_epoch_set = false;
+
 }  // namespace
+
+extern "C" int hx_timeline_epoch(void) {
+  return guarded([&]() -> int {
+    if (!g_epoch_set) CK(cudaEventCreate(&g_epoch));
+    g_epoch_set = true;
+    CK(cudaEventRecord(g_epoch, 0));
+    return HX_OK;
+  });
+}
 
 // ---- page-locked host memory cache (plan work lists) ----------------------------------
 namespace hx {
@@ -1406,6 +1418,17 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       double tot = 0;
       for (double v : f2) tot += v;
       st->fro2_total = tot;
+      const int marks[4] = {0, 1, 2, 4};
+      for (int k = 0; k < 4; ++k) {
+        st->t_marks[k] = -1.0;
+        if (g_epoch_set) {
+          float t = 0;
+          if (cudaEventElapsedTime(&t, g_epoch, c->ev[marks[k]]) == cudaSuccess)
+            st->t_marks[k] = t;
+          else
+            cudaGetLastError();
+        }
+      }
     }
     return HX_OK;
   });

@@ -421,6 +421,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
+    if os.environ.get("HX_TIMING"):
+        _lib.lib().hx_timeline_epoch()
     marks = [("start", time.perf_counter())]
     dev_a = resident(h)
     if dev_a is not None:
@@ -488,6 +490,10 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             _lib.check(_lib.lib().hx_product(ctx.h, plan.h, C.byref(pc), C.byref(st)),
                        "hx_product")
             timeline.append(("product", t0, time.perf_counter()))
+            if os.environ.get("HX_TIMING"):
+                tm = list(st.t_marks)
+                print(f"[hx device] ctx {ctxs.index(ctx)}: start {tm[0]:.1f} form-end "
+                      f"{tm[1]:.1f} mat-end {tm[2]:.1f} end {tm[3]:.1f} ms", flush=True)
             leaves = plan.leaves()
             nl = len(leaves["ids"])
             rank = np.zeros(nl, np.int32)

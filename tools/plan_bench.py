@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fill", action="store_true", help="also fill every batch")
     ap.add_argument("--sizes", action="store_true", help="materialization flops by leaf size")
+    ap.add_argument("--chunk", type=int, default=-1, help="plan only this chunk of 3")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     t0 = time.time()
@@ -52,9 +53,14 @@ def main():
     bct = build_block_cluster_tree(build_cluster_tree(pts, c["n_min"]), c["eta"])
     ta, d = synthetic_directory(bct)
     print(f"tree {time.time() - t0:.1f}s nodes {bct.n_nodes}", flush=True)
+    mask = None
+    if a.chunk >= 0:
+        from paper_1805_08998_b200 import multiply
+        groups = multiply.chunk_groups(bct, 3, first=0.5)
+        mask = multiply.group_mask(bct, groups[a.chunk])
     for _ in range(a.reps):
         t0 = time.perf_counter()
-        p = _lib.Plan(ta, d, d, None, 64, flags=_lib.Plan.DEFER)
+        p = _lib.Plan(ta, d, d, mask, 64, flags=_lib.Plan.DEFER)
         t1 = time.perf_counter()
         msg = f"plan {1e3 * (t1 - t0):.1f} ms"
         if a.fill:
