@@ -448,8 +448,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         nch = max(1, int(chunks))
         use_overlap = nch > 1 and overlap_default(overlap)
-    # with overlap the first chunk is half size: its planning is the only exposed part
-    queue = collections.deque(chunk_groups(h.bct, nch, first=0.5 if use_overlap else 1.0))
+    # with overlap the first chunk is small: its planning is the only exposed part
+    queue = collections.deque(chunk_groups(h.bct, nch, first=0.2 if use_overlap else 1.0))
     budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
