@@ -192,17 +192,14 @@ __global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __
 // carries sigma_j, hits need sigma_j <= eps * ||sigma_{<=j}||, and the random probes cost
 // one vector more than the singular directions (ranks within +-1 of the reference's on
 // its fixtures); the factors are still the best approximation of that rank.
-__global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int policy, double eps,
-                                   int k_max, int oversample, int* __restrict__ rank,
-                                   int* __restrict__ retry, int randomized_rule = 0) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= n) return;
-  const SelJob jb = jobs[b];
+__device__ __forceinline__ void select_one(const SelJob& jb, int policy, double eps, int k_max,
+                                           int oversample, int randomized_rule, int& rank_out,
+                                           int& retry_out) {
   const int l = jb.l;
   if (policy == 1) {
     const int r = min(k_max, jb.mu);
-    rank[b] = min(r, l);
-    retry[b] = (r > l) ? 1 : 0;
+    rank_out = min(r, l);
+    retry_out = (r > l) ? 1 : 0;
     return;
   }
   double s2 = 0.0;
@@ -241,12 +238,21 @@ __global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int p
   // select_rank picks the FIRST r whose tail is small enough; tails are non-increasing in r,
   // so the smallest qualifying r found by the backward scan is that index.
   if (jb.exact) {
-    rank[b] = min(r, l);
-    retry[b] = 0;
+    rank_out = min(r, l);
+    retry_out = 0;
   } else {
-    retry[b] = (r > l - oversample && l < jb.mu) ? 1 : 0;
-    rank[b] = min(r, l);
+    retry_out = (r > l - oversample && l < jb.mu) ? 1 : 0;
+    rank_out = min(r, l);
   }
+}
+
+__global__ void select_rank_kernel(const SelJob* __restrict__ jobs, int n, int policy, double eps,
+                                   int k_max, int oversample, int* __restrict__ rank,
+                                   int* __restrict__ retry, int randomized_rule = 0) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= n) return;
+  const SelJob jb = jobs[b];
+  select_one(jb, policy, eps, k_max, oversample, randomized_rule, rank[b], retry[b]);
 }
 
 // out(rows x r) = P(rows x q) * C(:, :r) * diag(scale); grid (job, row chunk of 128).

@@ -17,13 +17,9 @@ __device__ unsigned long long g_jac_stats[2];
 
 // One-sided Jacobi SVD of R (q x q, column-major) with lane c holding column c of R and of
 // V in registers.  Pairs follow the same round-robin (circle) ordering as the CTA kernel.
+// One warp: one-sided Jacobi SVD of jb (any address space for the job's arrays).
 template <int QM>
-__global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restrict__ jobs,
-                                                          int n_jobs) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int jid = blockIdx.x * (blockDim.x >> 5) + warp;
-  if (jid >= n_jobs) return;
-  const JacJob jb = jobs[jid];
+__device__ __forceinline__ void warp_jacobi_run(const JacJob& jb, int lane) {
   const int q = jb.q;
   double col[QM], vc[QM];
 #pragma unroll
@@ -108,15 +104,24 @@ __global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restri
   if (lane < q) {
     jb.sig[pos] = nrm;
     const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
-#pragma unroll
     double* col_out = jb.trans ? jb.V : jb.W;
     double* rot_out = jb.trans ? jb.W : jb.V;
+#pragma unroll
     for (int x = 0; x < QM; ++x)
       if (x < q) {
         col_out[x + pos * q] = nrm > 0.0 ? col[x] * inv : 0.0;
         rot_out[x + pos * q] = vc[x];
       }
   }
+}
+
+template <int QM>
+__global__ void __launch_bounds__(128) warp_jacobi_kernel(const JacJob* __restrict__ jobs,
+                                                          int n_jobs) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jid = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (jid >= n_jobs) return;
+  warp_jacobi_run<QM>(jobs[jid], lane);
 }
 
 }  // namespace hx
