@@ -46,10 +46,18 @@ struct DArr {
   size_t cap = 0;
   void ensure(size_t n) {
     if (n <= cap && p) return;
+    // growing: 25% slack (at most 2 GB) against regrowth by the next chunk or round
+    const size_t grown = cap ? cap + std::min(cap / 4, (size_t(2) << 30) / sizeof(T)) : 0;
     if (p) cudaFree(p);
     p = nullptr;
     cap = 0;
     const size_t want = std::max<size_t>(n, 1);
+    const size_t ask = std::max(want, grown);
+    if (ask > want && cudaMalloc(&p, ask * sizeof(T)) == cudaSuccess) {
+      cap = ask;
+      return;
+    }
+    cudaGetLastError();
     if (cudaMalloc(&p, want * sizeof(T)) != cudaSuccess) {
       cudaGetLastError();
       throw hx::OutOfMemory("cudaMalloc of " + std::to_string(want * sizeof(T)) + " bytes");
