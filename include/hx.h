@@ -72,6 +72,24 @@ typedef struct hx_operand {
 int hx_operand_layout(const hx_tree* tree, const int8_t* payload, const int32_t* rank,
                       int64_t* u_off, int64_t* v_off, int64_t* d_off, int64_t* pool_elems);
 
+/* HMX1 operator files (reference format pkg/src/hmat/hmatrix.py:9-24), read and written
+ * straight from / into a packed pool with the directory above.
+ * hx_hmx1_write replaces save_hmatrix (hmatrix.py:338-361): records in ascending node id,
+ * row-major payloads; `fingerprint` = sha256 of the block-tree dump (tree_fingerprint,
+ * hmatrix.py:334-335); `degraded` [n_nodes] may be NULL.
+ * hx_hmx1_scan + hx_hmx1_read replace load_hmatrix (hmatrix.py:364-388): the scan checks
+ * the header (HX_EINVAL with the reference's messages: "not an H-matrix file",
+ * "unsupported version V", "dimension mismatch: file N, tree M", "block tree does not match
+ * the stored operator"), every record against the tree, and returns per node the payload
+ * kind (1 low rank, 2 dense), rank, degraded flag and payload file position; the caller
+ * lays the pool out (hx_operand_layout) and hx_hmx1_read fills it. */
+int hx_hmx1_write(const char* path, const hx_tree* tree, int64_t n, const uint8_t* fingerprint,
+                  const hx_operand* op, const int8_t* degraded, const double* pool);
+int hx_hmx1_scan(const char* path, const hx_tree* tree, int64_t n, const uint8_t* fingerprint,
+                 int8_t* payload, int32_t* rank, int8_t* degraded, int64_t* pos);
+int hx_hmx1_read(const char* path, const hx_tree* tree, const hx_operand* op,
+                 const int64_t* pos, double* pool);
+
 typedef struct hx_plan hx_plan;
 typedef struct hx_ctx hx_ctx;
 

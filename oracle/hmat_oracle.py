@@ -21,7 +21,9 @@ What it restates (all citations are ``file:line`` in the reference tree
   Golub-Kahan-Lanczos (``:271-365``), randomized adaptive / fixed (``:368-428``), dense SVD
   (``:431-438``) and the shared epsilon-rank rule (``lowrank.py:75-90``);
 * the product driver ``hmult_new`` (``multiply.py:207-256``) with per-block seeds
-  (``multiply.py:61-63``) and the report counters (``multiply.py:50-58``).
+  (``multiply.py:61-63``) and the report counters (``multiply.py:50-58``);
+* the HMX1 operator file format (``hmatrix.py:9-24``, ``save_hmatrix`` / ``load_hmatrix``
+  ``:334-388``).
 
 Parity of this restatement is pinned against the reference itself: ``tests/golden`` holds
 fixtures produced by importing the reference in the build container
@@ -957,3 +959,62 @@ def make_points(cfg, seed=0):
         g = rng.standard_normal((n, 3))
         return g / np.linalg.norm(g, axis=1, keepdims=True)
     raise ValueError(geom)
+
+
+# ------------------------------------------------------------------ HMX1 files
+def fingerprint_o(bt: BlockTreeO):
+    """``tree_fingerprint`` (``hmatrix.py:334-335``): sha256 of the block-tree dump."""
+    import hashlib
+    return hashlib.sha256(bt.dump().encode()).digest()
+
+
+def save_hmatrix_o(H: HMatO, path):
+    """``save_hmatrix`` (``hmatrix.py:338-361``): header, then leaf records in ascending id
+    with row-major payloads."""
+    import struct
+    with open(path, "wb") as f:
+        f.write(b"HMX1")
+        f.write(struct.pack("<IQ", 1, H.bt.n))
+        f.write(fingerprint_o(H.bt))
+        f.write(struct.pack("<Q", len(H.data)))
+        for b in sorted(H.data):
+            p = H.data[b]
+            flag = 1 if b in H.degraded else 0
+            if isinstance(p, LR):
+                f.write(struct.pack("<QBBIII", b, 1, flag, p.left.shape[0], p.right.shape[0],
+                                    p.rank))
+                f.write(np.ascontiguousarray(p.left).tobytes())
+                f.write(np.ascontiguousarray(p.right).tobytes())
+            else:
+                f.write(struct.pack("<QBBII", b, 0, flag, p.shape[0], p.shape[1]))
+                f.write(np.ascontiguousarray(p).tobytes())
+
+
+def load_hmatrix_o(path, bt: BlockTreeO):
+    """``load_hmatrix`` (``hmatrix.py:364-388``) with its header checks and messages."""
+    import struct
+    with open(path, "rb") as f:
+        if f.read(4) != b"HMX1":
+            raise ValueError("not an H-matrix file")
+        version, n = struct.unpack("<IQ", f.read(12))
+        if version != 1:
+            raise ValueError(f"unsupported version {version}")
+        if n != bt.n:
+            raise ValueError(f"dimension mismatch: file {n}, tree {bt.n}")
+        if f.read(32) != fingerprint_o(bt):
+            raise ValueError("block tree does not match the stored operator")
+        (count,) = struct.unpack("<Q", f.read(8))
+        data, degraded = {}, set()
+        for _ in range(count):
+            b, kind, flag = struct.unpack("<QBB", f.read(10))
+            if flag:
+                degraded.add(b)
+            if kind == 1:
+                m, nn, k = struct.unpack("<III", f.read(12))
+                left = np.frombuffer(f.read(8 * m * k)).reshape(m, k).copy()
+                right = np.frombuffer(f.read(8 * nn * k)).reshape(nn, k).copy()
+                data[b] = LR(left, right)
+            else:
+                m, nn = struct.unpack("<II", f.read(8))
+                data[b] = np.frombuffer(f.read(8 * m * nn)).reshape(m, nn).copy()
+    return HMatO(bt, data, degraded)

@@ -11,7 +11,8 @@ from .clustering import (FAR, INNER, NEAR, BlockClusterTree, BlockNode, Cluster,
                          ClusterTree, admissible, build_block_cluster_tree,
                          build_cluster_tree, dump_tree, sparsity_constant)
 from .compressors import CompressorKind
-from .hmatrix import HMatrix, frobenius_norm, to_dense
+from .hmatrix import (HMatrix, frobenius_norm, load_hmatrix, save_hmatrix, to_dense,
+                      tree_fingerprint)
 from .lowrank import EpsRank, FixedRank, LowRank, select_rank, zero_lowrank
 from .multiply import MultiplyConfig, MultReport, hmult_new
 from .assembly import KERNELS, assemble_hmatrix

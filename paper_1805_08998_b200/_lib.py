@@ -96,6 +96,10 @@ SIGNATURES = {
     "hx_host_register": [C.c_void_p, C.c_int64],
     "hx_host_unregister": [C.c_void_p],
     "hx_operand_layout": [C.POINTER(HxTree), i8p, i32p, i64p, i64p, i64p, i64p],
+    "hx_hmx1_write": [C.c_char_p, C.POINTER(HxTree), C.c_int64, u8p, C.POINTER(HxOperand),
+                      i8p, f64p],
+    "hx_hmx1_scan": [C.c_char_p, C.POINTER(HxTree), C.c_int64, u8p, i8p, i32p, i8p, i64p],
+    "hx_hmx1_read": [C.c_char_p, C.POINTER(HxTree), C.POINTER(HxOperand), i64p, f64p],
     "hx_hmatvec": [C.c_void_p, C.POINTER(HxTree), C.POINTER(HxOperand), C.c_int, C.c_int,
                    f64p, f64p, C.c_int],
     "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,

@@ -9,6 +9,7 @@
 //      -> select_rank with the exact unsampled tail -> factors (U S, V)
 //      blocks whose selected rank leaves less than `oversample` spare sketch columns are
 //      redone with a doubled sketch; a sketch that spans the block is exact.
+#include <chrono>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -687,6 +688,28 @@ extern "C" int hx_ctx_operand_alias(hx_ctx* c) {
   return HX_OK;
 }
 
+// HX_RECOMP_TIMING: synchronizing wall-clock marks through the recompression phase (a
+// diagnostic: it serializes host list building and device work)
+struct PhaseMarks {
+  bool on = std::getenv("HX_RECOMP_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  std::vector<std::pair<std::string, double>> acc;
+  void mark(const char* what, cudaStream_t s) {
+    if (!on) return;
+    CK(cudaStreamSynchronize(s));
+    const auto now = std::chrono::steady_clock::now();
+    const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+    t = now;
+    for (auto& a : acc)
+      if (a.first == what) { a.second += ms; return; }
+    acc.emplace_back(what, ms);
+  }
+  ~PhaseMarks() {
+    if (!on) return;
+    for (auto& a : acc) std::fprintf(stderr, "[hx recomp] %-14s %9.1f ms\n", a.first.c_str(), a.second);
+  }
+};
+
 extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
                           hx_product_stats* st) {
   return guarded([&]() -> int {
@@ -827,6 +850,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       cudaStream_t s;
       ~RestoreStream() { c->s = s; }
     } restore_stream{c, s_main};
+    PhaseMarks pm;
+    pm.mark("materialize", s);
     std::vector<FarBlock> fb;
     int mu_max = 0;
     for (int i = 0; i < nl; ++i) {
@@ -986,6 +1011,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       flush();
     };
 
+    pm.mark("impl-lists", s);
     constexpr int PR = 8;  // probe columns of the implicit route's tail estimate
     // Jacobi on R^T (rows of the QR factor): fewer sweeps than on the columns of R
     const char* jt = std::getenv("HX_JAC_TRANS");
@@ -1234,6 +1260,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         tail_e.push_back(tail_slots);
       }
       gm.cut();  // gemm batch 6
+      pm.mark("host-lists", s);
       // upload and run
       const int na = int(active.size());
       c->xterms.upload(gm.terms, s);
@@ -1278,12 +1305,14 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       gather_batch(0);
       gemm_batch(0, nullptr);
       gemm_batch(1, nullptr);
+      pm.mark("sketch-Y", s);
       run_qr(c, qy);
       if (est_slots) {
         gemm_batch(2, nullptr);
         gemm_batch(3, c->esum.p);
         seg_sums(est_b, est_e, c->eb, c->ee, c->esum.p, c->est.p, 1.0 / PR);
       }
+      pm.mark("qr-Y+est", s);
       gather_batch(1);
       gemm_batch(4, nullptr);
       gemm_batch(5, nullptr);
@@ -1291,6 +1320,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         gemm_batch(6, c->rsum.p);
         seg_sums(tail_b, tail_e, c->tb, c->te, c->rsum.p, c->resid.p, 1.0);
       }
+      pm.mark("sketch-Bt", s);
       run_qr(c, qb);
       // SVD of the small factor
       std::vector<JacJob> jj;
@@ -1311,6 +1341,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         std::fprintf(stderr, "[hx jacobi] warp jobs %llu mean sweeps %.2f\n", z[0],
                      z[0] ? double(z[1]) / double(z[0]) : 0.0);
       }
+      pm.mark("qr-Bt+jacobi", s);
       // rank selection
       std::vector<SelJob> sj;
       for (size_t a = 0; a < active.size(); ++a) {
@@ -1336,6 +1367,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaMemcpyAsync(rt.data(), c->retry_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
+      pm.mark("select", s);
       std::vector<int> next;
       for (int a = 0; a < na; ++a) {
         FarBlock& f = fb[active[a]];
@@ -1388,6 +1420,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaGetLastError());
       c->launches++;
     }
+    pm.mark("output", s);
     // near leaves: payload stays in BUF_TILE after the far blocks
     c->near_begin = P->near_ws_begin;
     c->near_elems = P->tile_elems - P->near_ws_begin;

@@ -13,6 +13,8 @@ kind, rank, offsets) -- the ``hx_operand`` of ``include/hx.h``.
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
+import os
 
 import numpy as np
 
@@ -167,3 +169,125 @@ def frobenius_norm(h):
         else:
             total += float(np.sum(p * p))
     return float(np.sqrt(total))
+
+
+# ------------------------------------------------------------------ HMX1 operator files
+class _PoolLeaves(dict):
+    """Leaf payloads unpacked on first access from a packed host pool (loaded operands)."""
+
+    def __init__(self, owner):
+        super().__init__()
+        self._owner = owner
+        self._filled = False
+
+    def _fill(self):
+        if self._filled:
+            return
+        self._filled = True
+        from .assembly import unpack_leaves
+        h = self._owner
+        pool, d = h._hx_packed
+        super().update(unpack_leaves(h.bct, pool, d))
+
+    def __missing__(self, key):
+        self._fill()
+        return super().__getitem__(key)
+
+    def __contains__(self, key):
+        self._fill()
+        return super().__contains__(key)
+
+    def __iter__(self):
+        self._fill()
+        return super().__iter__()
+
+    def __len__(self):
+        self._fill()
+        return super().__len__()
+
+    def keys(self):
+        self._fill()
+        return super().keys()
+
+    def values(self):
+        self._fill()
+        return super().values()
+
+    def items(self):
+        self._fill()
+        return super().items()
+
+
+def tree_fingerprint(bct):
+    """sha256 of the block-tree dump (reference ``tree_fingerprint``, hmatrix.py:334-335)."""
+    return hashlib.sha256(clustering.dump_tree(block_arrays(bct)).encode()).digest()
+
+
+def _packed(h):
+    cached = getattr(h, "_hx_packed", None)
+    if cached is None:
+        return pack_operand(h)
+    pool, d = cached
+    if pool is None:  # assembled on the device: one download
+        from .assembly import host_pool
+        pool, d = host_pool(h)
+    return pool, d
+
+
+def save_hmatrix(h, path):
+    """Write the leaf payloads in the HMX1 layout (reference ``save_hmatrix``,
+    hmatrix.py:338-361), straight from the packed operand pool (``hx_hmx1_write``)."""
+    from . import _lib
+    arr = block_arrays(h.bct)
+    pool, d = _packed(h)
+    tb = _lib.TreeBuf(tree_arrays(h.bct))
+    ob = _lib.OperandBuf(d)
+    deg = np.zeros(arr.n_nodes, np.int8)
+    if h.degraded:
+        deg[np.fromiter(h.degraded, dtype=np.int64)] = 1
+    fp = np.frombuffer(tree_fingerprint(h.bct), dtype=np.uint8).copy()
+    pool = np.ascontiguousarray(pool, dtype=np.float64)
+    _lib.check(_lib.lib().hx_hmx1_write(os.fsencode(path), C.byref(tb.st), int(h.n),
+                                        _lib.ptr(fp, _lib.u8p), C.byref(ob.st),
+                                        _lib.ptr(deg, _lib.i8p), _lib.ptr(pool, _lib.f64p)),
+               "save_hmatrix")
+
+
+def load_hmatrix(path, bct):
+    """Read an HMX1 file back (reference ``load_hmatrix``, hmatrix.py:364-388): the header
+    checks raise ``ValueError`` with the reference's messages; the payloads land directly in
+    a packed pool in panel order (``hx_hmx1_scan`` / ``hx_hmx1_read``), ready for upload;
+    ``data`` unpacks lazily into ``LowRank`` / ndarray leaves."""
+    from . import _lib
+    with open(path, "rb"):  # FileNotFoundError / PermissionError as the reference raises
+        pass
+    arr = block_arrays(bct)
+    nn = arr.n_nodes
+    tb = _lib.TreeBuf(tree_arrays(bct))
+    payload = np.zeros(nn, np.int8)
+    rank = np.zeros(nn, np.int32)
+    deg = np.zeros(nn, np.int8)
+    pos = np.zeros(nn, np.int64)
+    fp = np.frombuffer(tree_fingerprint(bct), dtype=np.uint8).copy()
+    _lib.check(_lib.lib().hx_hmx1_scan(os.fsencode(path), C.byref(tb.st), int(bct.n),
+                                       _lib.ptr(fp, _lib.u8p), _lib.ptr(payload, _lib.i8p),
+                                       _lib.ptr(rank, _lib.i32p), _lib.ptr(deg, _lib.i8p),
+                                       _lib.ptr(pos, _lib.i64p)), "load_hmatrix")
+    u_off = np.zeros(nn, np.int64)
+    v_off = np.zeros(nn, np.int64)
+    d_off = np.zeros(nn, np.int64)
+    total = np.zeros(1, np.int64)
+    _lib.check(_lib.lib().hx_operand_layout(
+        C.byref(tb.st), _lib.ptr(payload, _lib.i8p), _lib.ptr(rank, _lib.i32p),
+        _lib.ptr(u_off, _lib.i64p), _lib.ptr(v_off, _lib.i64p), _lib.ptr(d_off, _lib.i64p),
+        _lib.ptr(total, _lib.i64p)), "hx_operand_layout")
+    pool = np.zeros(max(int(total[0]), 16), dtype=np.float64)
+    d = dict(payload=payload, rank=rank, u_off=u_off, v_off=v_off, d_off=d_off)
+    ob = _lib.OperandBuf(d)
+    _lib.check(_lib.lib().hx_hmx1_read(os.fsencode(path), C.byref(tb.st), C.byref(ob.st),
+                                       _lib.ptr(pos, _lib.i64p), _lib.ptr(pool, _lib.f64p)),
+               "load_hmatrix")
+    H = HMatrix(bct, {}, set(np.flatnonzero(deg).tolist()))
+    H._hx_packed = (pool, d)
+    H.data = _PoolLeaves(H)
+    return H
