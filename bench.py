@@ -9,7 +9,7 @@ value  = canonical FP64 work of the product (SURVEY 8(d) min-route model) / step
          in GFLOP/s, whole job.
 e2e    = the same through the public API with host operands: pack/H2D of the operand pool,
          the product, D2H of every output block and construction of the HMatrix.
-Multi-GPU (torchrun): output leaves are LPT-partitioned over ranks by estimated cost,
+Multi-GPU (torchrun): output subtrees are LPT-partitioned over ranks by estimated cost,
 operand pools replicated from rank 0 by an NCCL broadcast; no reduction (strong scaling).
 
 --impl reference: the reference algorithm (the NumPy restatement in oracle/, the
@@ -297,9 +297,9 @@ def bench_ours(args, rank, world, local):
         full = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, None,
                          multiply.plan_tile(bct))
         lv = full.leaves()
-        owner, load = lpt_partition(leaf_costs(lv), world)
-        mask = np.zeros(bct.n_nodes, np.uint8)
-        mask[lv["ids"][owner == rank]] = 1
+        cost = np.zeros(bct.n_nodes)
+        cost[lv["ids"]] = leaf_costs(lv)
+        mask = multiply.subtree_partition(bct, cost, world)[3][rank]
         full.close()
     setup_s = time.time() - t_setup
     # tensor-core work of this rank's plan (outside the timed region)
@@ -456,7 +456,7 @@ def bench_ours(args, rank, world, local):
             "config": {"workload": configs.NAMES[args.config], "compressor": args.tag,
                        "l2": "inputs larger than L2 (operand pools "
                              f"{8 * A._hx_device[2] / 1e9:.2f} GB)",
-                       "parallelism": f"output-leaf partition x{world}"},
+                       "parallelism": f"output-subtree partition x{world}"},
             "canonical_gflop": F_tot / 1e9, "canonical_gbytes": B_tot / 1e9,
             "phases_ms": iso,
             "phases_ms_note": "one product after the timed region without chunk overlap "

@@ -207,6 +207,10 @@ int hx_assemble(hx_ctx* ctx, const hx_tree* tree, const double* points, int dim,
 int hx_pool_download(hx_ctx* ctx, const double* pool_dev, double* host, int64_t n_elems);
 int hx_pool_free(hx_ctx* ctx, double* pool_dev);
 
+/* Diagnostics: batched Householder QR of n_jobs column-major panels (p[i] x q[i], q <= p,
+ * concatenated in X, overwritten by the explicit Q; R gets the q x q factors), through the
+ * same dispatch as the recompression (register / warp / CTA kernels, TSQR for tall panels). */
+int hx_debug_qr(int n_jobs, const int32_t* p, const int32_t* q, double* X, double* R);
 /* Diagnostics: run the grouped DMMA GEMM kernel on host data (Term / Tile / Group records
  * of paper_1805_08998_b200/csrc/hx_types.h; host_bufs/buf_elems: 10 buffer slots, copied to
  * the device and back).  Used by the kernel-level parity tests. */
@@ -232,6 +236,9 @@ int hx_host_unregister(void* p);
 /* Release the product workspace (work lists, term/tile buffers, results not yet
  * downloaded); operand pools stay attached. */
 int hx_ctx_trim(hx_ctx* ctx);
+/* Forget the per-size-class rank hints that narrow the first sketch of later chunks of
+ * one product (called at the start of every product). */
+int hx_ctx_reset_hints(hx_ctx* ctx);
 
 /* Y = M X (transpose = 0) or M^T X (transpose = 1) for the H-matrix attached in operand
  * slot `which` (0 or 1) of the context: X and Y are host n x s column-major blocks in

@@ -88,6 +88,7 @@ SIGNATURES = {
     "hx_ctx_synchronize": [C.c_void_p],
     "hx_ctx_mem_info": [C.c_void_p, i64p, i64p],
     "hx_ctx_trim": [C.c_void_p],
+    "hx_ctx_reset_hints": [C.c_void_p],
     "hx_ctx_operand_share": [C.c_void_p, C.c_void_p],
     "hx_ctx_held_bytes": [C.c_void_p],
     "hx_timeline_epoch": [],
@@ -104,6 +105,7 @@ SIGNATURES = {
                    f64p, f64p, C.c_int],
     "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                       C.c_int64, C.POINTER(f64p), i64p, f64p, C.c_int64],
+    "hx_debug_qr": [C.c_int, i32p, i32p, f64p, f64p],
     "hx_ctx_free": [C.c_void_p],
     "hx_last_error": [C.c_char_p, C.c_size_t],
     "hx_version": [],

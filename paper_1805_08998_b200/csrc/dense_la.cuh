@@ -19,9 +19,13 @@ constexpr int JAC_QMAX = 512;      // widest sketch / SVD factor
 constexpr int JAC_SMEM_QMAX = 96;  // above: the Jacobi CTA works in place in HBM/L2
 
 struct QrJob {
-  double* X;   // p x q column-major, ld = p; overwritten by explicit Q
-  double* R;   // q x q column-major output (upper triangular)
+  double* X;   // p x q column-major (ld ldx); overwritten by explicit Q
+  double* R;   // q x q column-major output (upper triangular, ld ldr)
   int p, q;
+  int ldx = 0;  // 0: p
+  int ldr = 0;  // 0: q
+  __host__ __device__ int lx() const { return ldx ? ldx : p; }
+  __host__ __device__ int lr() const { return ldr ? ldr : q; }
 };
 
 struct JacJob {

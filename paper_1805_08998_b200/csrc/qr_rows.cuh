@@ -88,10 +88,10 @@ __device__ void rows_apply(double* M, int ld, int p, int q, int j, double tau, d
   }
 }
 
-// In-place QR of M (p x q, ld): R (q x q, ld q) to Rout, M overwritten by the explicit Q.
+// In-place QR of M (p x q, ld): R (q x q, ld ldr) to Rout, M overwritten by the explicit Q.
 // tau_s: q doubles, wsum: 32, red: 32 per warp (CTA).
 template <bool CTA>
-__device__ void rows_householder_qr(double* M, int ld, int p, int q, double* Rout,
+__device__ void rows_householder_qr(double* M, int ld, int p, int q, double* Rout, int ldr,
                                     double* tau_s, double* wsum, double* red) {
   const int t = CTA ? int(threadIdx.x) : int(threadIdx.x & 31);
   const int nt = CTA ? int(blockDim.x) : 32;
@@ -121,7 +121,7 @@ __device__ void rows_householder_qr(double* M, int ld, int p, int q, double* Rou
   }
   for (int e = t; e < q * q; e += nt) {
     const int i = e % q, c = e / q;
-    Rout[e] = (i <= c && i < p) ? M[i + int64_t(c) * ld] : 0.0;
+    Rout[i + int64_t(c) * ldr] = (i <= c && i < p) ? M[i + int64_t(c) * ld] : 0.0;
   }
   grp_sync<CTA>();
   for (int j = q - 1; j >= 0; --j) {
@@ -147,10 +147,11 @@ __global__ void qr_rows_warp_kernel(const QrJob* __restrict__ jobs, int n_jobs, 
   double* tau_s = M + int64_t(p) * q;
   double* wsum = tau_s + q;
   const int64_t n = int64_t(p) * q;
-  for (int64_t e = lane; e < n; e += 32) M[e] = jb.X[e];
+  const int64_t lx = jb.lx();
+  for (int64_t e = lane; e < n; e += 32) M[e] = jb.X[e % p + (e / p) * lx];
   __syncwarp();
-  rows_householder_qr<false>(M, p, p, q, jb.R, tau_s, wsum, nullptr);
-  for (int64_t e = lane; e < n; e += 32) jb.X[e] = M[e];
+  rows_householder_qr<false>(M, p, p, q, jb.R, jb.lr(), tau_s, wsum, nullptr);
+  for (int64_t e = lane; e < n; e += 32) jb.X[e % p + (e / p) * lx] = M[e];
 }
 
 // One CTA of NT threads per panel; use_smem: stage the panel (p * q doubles) in dynamic
@@ -165,14 +166,15 @@ __global__ void __launch_bounds__(NT, (NT <= 256 ? 2 : 1))
   const QrJob jb = jobs[blockIdx.x];
   const int p = jb.p, q = jb.q;
   const int64_t n = int64_t(p) * q;
+  const int64_t lx = jb.lx();
   if (use_smem) {
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dsm[e] = jb.X[e];
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dsm[e] = jb.X[e % p + (e / p) * lx];
     __syncthreads();
-    rows_householder_qr<true>(dsm, p, p, q, jb.R, tau_s, wsum, red);
+    rows_householder_qr<true>(dsm, p, p, q, jb.R, jb.lr(), tau_s, wsum, red);
     __syncthreads();
-    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) jb.X[e] = dsm[e];
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) jb.X[e % p + (e / p) * lx] = dsm[e];
   } else {
-    rows_householder_qr<true>(jb.X, p, p, q, jb.R, tau_s, wsum, red);
+    rows_householder_qr<true>(jb.X, int(lx), p, q, jb.R, jb.lr(), tau_s, wsum, red);
   }
 }
 
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 1 ? 8 : 16 / NW) qr_reg_kernel(
     ii[r] = t + r * NT;
 #pragma unroll
     for (int x = 0; x < QM; ++x)
-      a[r][x] = (x < q && ii[r] < p) ? jb.X[ii[r] + int64_t(x) * p] : 0.0;
+      a[r][x] = (x < q && ii[r] < p) ? jb.X[ii[r] + int64_t(x) * jb.lx()] : 0.0;
   }
   // group sum of a scalar
   auto gsum = [&](double v) {
@@ -326,7 +328,7 @@ __global__ void __launch_bounds__(NW * 32, NW == 1 ? 8 : 16 / NW) qr_reg_kernel(
     if (ii[r] < q) {
 #pragma unroll
       for (int x = 0; x < QM; ++x)
-        if (x < q) jb.R[ii[r] + x * q] = (ii[r] <= x) ? a[r][x] : 0.0;
+        if (x < q) jb.R[ii[r] + int64_t(x) * jb.lr()] = (ii[r] <= x) ? a[r][x] : 0.0;
     }
   // explicit Q (dorg2r)
   for (int j = q - 1; j >= 0; --j) {
@@ -349,8 +351,50 @@ __global__ void __launch_bounds__(NW * 32, NW == 1 ? 8 : 16 / NW) qr_reg_kernel(
     if (ii[r] < p) {
 #pragma unroll
       for (int x = 0; x < QM; ++x)
-        if (x < q) jb.X[ii[r] + int64_t(x) * p] = a[r][x];
+        if (x < q) jb.X[ii[r] + int64_t(x) * jb.lx()] = a[r][x];
     }
+}
+
+}  // namespace hx
+
+namespace hx {
+
+// ---------------------------------------------------------------------------------------
+// TSQR of tall panels (p > 256 rows, q <= 64): the panel is cut into row blocks of
+// 128..255 rows, each block is factored in place by the kernels above (explicit Q_i,
+// R_i stacked into S), S is factored the same way until one block remains, and the
+// explicit Q is assembled top-down: every block's Q_i is multiplied in place by its q x q
+// slice of the explicit Q of the level above.  One CTA per 64-row slab of a block.
+struct TsMul {
+  double* X;         // slab (rows x q, ld ldx), overwritten by X * Qs
+  const double* Qs;  // q x q slice (ld ldq)
+  int ldx, ldq, rows, q;
+};
+
+constexpr int TS_SLAB = 64;
+constexpr int TS_QMAX = 64;
+
+__global__ void __launch_bounds__(256) tsqr_apply_kernel(const TsMul* __restrict__ jobs) {
+  extern __shared__ __align__(16) double tsm[];
+  double* xs = tsm;                      // TS_SLAB x q, ld TS_SLAB
+  double* qs = tsm + TS_SLAB * TS_QMAX;  // q x q, ld TS_QMAX
+  const TsMul jb = jobs[blockIdx.x];
+  const int rows = jb.rows, q = jb.q;
+  for (int e = threadIdx.x; e < TS_SLAB * q; e += blockDim.x) {
+    const int i = e & (TS_SLAB - 1), c = e / TS_SLAB;
+    xs[e] = i < rows ? jb.X[i + int64_t(c) * jb.ldx] : 0.0;
+  }
+  for (int e = threadIdx.x; e < q * q; e += blockDim.x) {
+    const int i = e % q, c = e / q;
+    qs[i + c * TS_QMAX] = jb.Qs[i + int64_t(c) * jb.ldq];
+  }
+  __syncthreads();
+  const int i = threadIdx.x & (TS_SLAB - 1);
+  for (int c = threadIdx.x / TS_SLAB; c < q; c += blockDim.x / TS_SLAB) {
+    double acc = 0.0;
+    for (int k = 0; k < q; ++k) acc = fma(xs[i + k * TS_SLAB], qs[k + c * TS_QMAX], acc);
+    if (i < rows) jb.X[i + int64_t(c) * jb.ldx] = acc;
+  }
 }
 
 }  // namespace hx

@@ -300,6 +300,8 @@ struct hx_ctx {
   DArr<Tile> rtiles;
   DArr<Group> rgroups;
   DArr<QrJob> qr_jobs;
+  DArr<TsMul> ts_jobs;     // TSQR down-sweep slabs
+  DArr<double> tsqr_ws;    // TSQR stacked R factors
   DArr<JacJob> jac_jobs;
   DArr<SelJob> sel_jobs;
   DArr<SmallJob> small_jobs;
@@ -314,6 +316,10 @@ struct hx_ctx {
   DArr<GSeg> gsegs;
   std::vector<DArr<double>> work;  // one workspace per sketch round
   std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
+  // sketch-width hints: the largest rank seen per log2(min(m, n)) class by earlier chunks
+  // of the same product (hx_ctx_reset_hints between products), for the same policy
+  int rank_hint[32];
+  double hint_key[4] = {-1, -1, -1, -1};
   int64_t omega_rows = 0;
   int omega_cols = 0;
   uint64_t omega_seed = ~0ULL;
@@ -433,39 +439,143 @@ void run_gemm_batch(hx_ctx* c, std::vector<Term>& terms, std::vector<Tile>& tile
 // (bucketed by height so that each launch sizes its smem slices tightly), taller ones one
 // CTA each, in shared memory when the panel fits.
 constexpr int QR_WARP_ROWS = 128;
+constexpr int TS_BLOCK = 128;  // TSQR row blocks of 128..255 rows (panels taller than 256)
 
 // Shared memory bounds occupancy here, so jobs are bucketed by their smem need (powers of
 // two) and every launch sizes its slices for its own bucket.
+// Bucket, sort and launch one set of independent QR jobs (already uploaded at dev).
+void launch_qr_set(hx_ctx* c, const QrJob* dev, const std::vector<QrJob>& all,
+                   const std::vector<int>& keys, size_t a0, size_t a1);
+
+int qr_bucket(const QrJob& j);
+
 void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
   if (jobs.empty()) return;
-  auto slice_of = [](const QrJob& j) { return size_t(j.p) * j.q + j.q + 32; };  // doubles
-  auto warp_job = [&](const QrJob& j) {
-    return j.p <= QR_WARP_ROWS && slice_of(j) * sizeof(double) <= size_t(SMEM_CAP);
-  };
-  // register-resident kernel: q <= 32, p <= 256; key 192 + 4 (QM == 32) + log2(NW) with
-  // two rows per thread for QM = 16 and one for QM = 32
-  auto reg_job = [](const QrJob& j) { return j.q <= 32 && j.q <= j.p && j.p <= 256; };
+  // TSQR decomposition of the tall panels (qr_rows.cuh): up-sweep levels of QR jobs and
+  // down-sweep slab products; offsets into one workspace, sized before any pointer is taken
+  static const bool no_tsqr = std::getenv("HX_NO_TSQR") != nullptr;
+  auto tall = [](const QrJob& j) { return !no_tsqr && j.q <= TS_QMAX && j.p > 2 * TS_BLOCK; };
+  int64_t ws = 0;
+  for (const QrJob& j : jobs) {
+    if (!tall(j)) continue;
+    int64_t p = j.p;
+    while (p > 2 * TS_BLOCK) {
+      const int64_t nb = p / TS_BLOCK;
+      ws += nb * j.q * j.q;
+      p = nb * j.q;
+    }
+  }
+  if (ws) c->tsqr_ws.ensure(size_t(ws));
+  std::vector<std::vector<QrJob>> lev(1);
+  std::vector<std::vector<TsMul>> down;
+  int64_t pos = 0;
+  for (const QrJob& j : jobs) {
+    if (!tall(j)) {
+      lev[0].push_back(j);
+      continue;
+    }
+    double* X = j.X;
+    int ld = j.lx();
+    int p = j.p;
+    const int q = j.q;
+    for (size_t L = 0;; ++L) {
+      if (lev.size() <= L) lev.resize(L + 1);
+      if (p <= 2 * TS_BLOCK) {
+        QrJob t{X, j.R, p, q};
+        t.ldx = ld;
+        t.ldr = j.lr();
+        lev[L].push_back(t);
+        break;
+      }
+      if (down.size() <= L) down.resize(L + 1);
+      const int nb = p / TS_BLOCK;
+      const int ls = nb * q;  // rows (and ld) of the stacked R factors
+      double* S = c->tsqr_ws.p + pos;
+      pos += int64_t(ls) * q;
+      const int base = p / nb, extra = p % nb;
+      int r0 = 0;
+      for (int i = 0; i < nb; ++i) {
+        const int rows = base + (i < extra ? 1 : 0);
+        QrJob t{X + r0, S + int64_t(i) * q, rows, q};
+        t.ldx = ld;
+        t.ldr = ls;
+        lev[L].push_back(t);
+        for (int s0 = 0; s0 < rows; s0 += TS_SLAB)
+          down[L].push_back(TsMul{X + r0 + s0, S + int64_t(i) * q, ld, ls,
+                                  std::min(TS_SLAB, rows - s0), q});
+        r0 += rows;
+      }
+      X = S;
+      ld = ls;
+      p = ls;
+    }
+  }
+  std::vector<QrJob> all;
+  std::vector<int> keys;
+  std::vector<size_t> lb;
+  for (auto& L : lev) {
+    lb.push_back(all.size());
+    std::vector<std::pair<int, int>> keyed(L.size());
+    for (size_t i = 0; i < L.size(); ++i) keyed[i] = {qr_bucket(L[i]), int(i)};
+    std::sort(keyed.begin(), keyed.end());
+    for (auto& kv : keyed) {
+      all.push_back(L[size_t(kv.second)]);
+      keys.push_back(kv.first);
+    }
+  }
+  lb.push_back(all.size());
+  c->qr_jobs.upload(all, c->s);
+  std::vector<TsMul> dm;
+  std::vector<size_t> db;
+  for (auto& D : down) {
+    db.push_back(dm.size());
+    dm.insert(dm.end(), D.begin(), D.end());
+  }
+  db.push_back(dm.size());
+  if (!dm.empty()) c->ts_jobs.upload(dm, c->s);
+  for (size_t L = 0; L + 1 < lb.size(); ++L) launch_qr_set(c, c->qr_jobs.p, all, keys, lb[L], lb[L + 1]);
+  static bool tattr = false;
+  if (!dm.empty() && !tattr) {
+    CK(cudaFuncSetAttribute(tsqr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            int(2 * TS_SLAB * TS_QMAX * sizeof(double))));
+    tattr = true;
+  }
+  for (size_t L = down.size(); L-- > 0;) {
+    const size_t n = db[L + 1] - db[L];
+    if (!n) continue;
+    tsqr_apply_kernel<<<int(n), 256, 2 * TS_SLAB * TS_QMAX * sizeof(double), c->s>>>(
+        c->ts_jobs.p + db[L]);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+}
+
+// register-resident kernel: q <= 32, p <= 256; key 192 + 4 (QM == 32) + log2(NW) with
+// two rows per thread for QM = 16 and one for QM = 32
+bool qr_reg_job(const QrJob& j) { return j.q <= 32 && j.q <= j.p && j.p <= 256; }
+size_t qr_slice(const QrJob& j) { return size_t(j.p) * j.q + j.q + 32; }  // doubles
+bool qr_warp_job(const QrJob& j) {
+  return j.p <= QR_WARP_ROWS && qr_slice(j) * sizeof(double) <= size_t(SMEM_CAP);
+}
+
+// bucket key: kind (0 warp, 1 CTA smem, 2 CTA global, 3 register) and log2 of the smem bytes
+int qr_bucket(const QrJob& j) {
   auto lg_nw = [](int rows_per_warp, int p) {
     int l = 0;
     while ((rows_per_warp << l) < p) ++l;
     return l;
   };
-  // bucket key: kind (0 warp, 1 CTA smem, 2 CTA global) and log2 of the smem bytes
-  auto bucket = [&](const QrJob& j) {
-    if (reg_job(j)) return j.q > 16 ? 196 + lg_nw(32, j.p) : 192 + lg_nw(64, j.p);
-    const size_t need = warp_job(j) ? slice_of(j) * sizeof(double)
-                                    : size_t(j.p) * j.q * sizeof(double);
-    const int kind = warp_job(j) ? 0 : (need <= size_t(SMEM_CAP) ? 1 : 2);
-    int lg = 0;
-    while ((size_t(1) << lg) < need && lg < 40) ++lg;
-    return kind == 2 ? 2 * 64 : kind * 64 + lg;
-  };
-  std::vector<std::pair<int, int>> keyed(jobs.size());
-  for (size_t i = 0; i < jobs.size(); ++i) keyed[i] = {bucket(jobs[i]), int(i)};
-  std::sort(keyed.begin(), keyed.end());
-  std::vector<QrJob> all(jobs.size());
-  for (size_t i = 0; i < jobs.size(); ++i) all[i] = jobs[size_t(keyed[i].second)];
-  c->qr_jobs.upload(all, c->s);
+  if (qr_reg_job(j)) return j.q > 16 ? 196 + lg_nw(32, j.p) : 192 + lg_nw(64, j.p);
+  const size_t need = qr_warp_job(j) ? qr_slice(j) * sizeof(double)
+                                     : size_t(j.p) * j.q * sizeof(double);
+  const int kind = qr_warp_job(j) ? 0 : (need <= size_t(SMEM_CAP) ? 1 : 2);
+  int lg = 0;
+  while ((size_t(1) << lg) < need && lg < 40) ++lg;
+  return kind == 2 ? 2 * 64 : kind * 64 + lg;
+}
+
+void launch_qr_set(hx_ctx* c, const QrJob* dev, const std::vector<QrJob>& all,
+                   const std::vector<int>& keys, size_t a0, size_t a1) {
   static bool attr = false;
   if (!attr) {
     CK(cudaFuncSetAttribute(qr_rows_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -476,19 +586,19 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
                             int(SMEM_CAP)));
     attr = true;
   }
-  for (size_t a = 0; a < all.size();) {
+  for (size_t a = a0; a < a1;) {
     size_t e = a;
     size_t need = 0;
-    while (e < all.size() && keyed[e].first == keyed[a].first) {
-      need = std::max(need, warp_job(all[e]) ? slice_of(all[e])
-                                             : size_t(all[e].p) * all[e].q);
+    while (e < a1 && keys[e] == keys[a]) {
+      need = std::max(need, qr_warp_job(all[e]) ? qr_slice(all[e])
+                                                : size_t(all[e].p) * all[e].q);
       ++e;
     }
     const int n = int(e - a);
-    const int kind = keyed[a].first / 64;
+    const int kind = keys[a] / 64;
+    const QrJob* jp = dev + a;
     if (kind == 3) {
-      const QrJob* jp = c->qr_jobs.p + a;
-      switch (keyed[a].first - 192) {
+      switch (keys[a] - 192) {
         case 0: qr_reg_kernel<1, 16, 2><<<n, 32, 0, c->s>>>(jp); break;
         case 1: qr_reg_kernel<2, 16, 2><<<n, 64, 0, c->s>>>(jp); break;
         case 2: qr_reg_kernel<4, 16, 2><<<n, 128, 0, c->s>>>(jp); break;
@@ -501,14 +611,14 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
       const size_t per = need * sizeof(double);
       const int wpc = int(std::max<size_t>(1, std::min<size_t>(4, size_t(SMEM_CAP) / per)));
       qr_rows_warp_kernel<<<(n + wpc - 1) / wpc, 32 * wpc, per * size_t(wpc), c->s>>>(
-          c->qr_jobs.p + a, n, int(need));
+          jp, n, int(need));
     } else if (kind == 1) {
       if (all[a].p > 256)
-        qr_rows_cta_kernel<512><<<n, 512, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
+        qr_rows_cta_kernel<512><<<n, 512, need * sizeof(double), c->s>>>(jp, 1);
       else
-        qr_rows_cta_kernel<256><<<n, 256, need * sizeof(double), c->s>>>(c->qr_jobs.p + a, 1);
+        qr_rows_cta_kernel<256><<<n, 256, need * sizeof(double), c->s>>>(jp, 1);
     } else {
-      qr_rows_cta_kernel<512><<<n, 512, 0, c->s>>>(c->qr_jobs.p + a, 0);
+      qr_rows_cta_kernel<512><<<n, 512, 0, c->s>>>(jp, 0);
     }
     CK(cudaGetLastError());
     c->launches++;
@@ -554,6 +664,12 @@ void run_jacobi(hx_ctx* c, const std::vector<JacJob>& jobs) {
     CK(cudaGetLastError());
     c->launches++;
   }
+}
+
+int ilog2(int x) {
+  int l = 0;
+  while ((1 << (l + 1)) <= x && l < 31) ++l;
+  return l;
 }
 
 int default_sketch(int mu) {
@@ -621,6 +737,12 @@ extern "C" int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src) {
     dst->opnd_elems[1] = src->opnd_elems[1];
     return HX_OK;
   });
+}
+
+extern "C" int hx_ctx_reset_hints(hx_ctx* c) {
+  if (!c) return fail(HX_EINVAL, "null context");
+  std::fill(c->rank_hint, c->rank_hint + 32, -1);
+  return HX_OK;
 }
 
 extern "C" int hx_ctx_trim(hx_ctx* c) {
@@ -720,6 +842,14 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     CK(cudaSetDevice(c->device));
     const int over = cfg->oversample > 0 ? cfg->oversample : 6;
     c->launches = 0;
+    {
+      const double key[4] = {double(cfg->policy), cfg->eps, double(cfg->k_max), double(cfg->tag)};
+      if (!std::equal(key, key + 4, c->hint_key)) {
+        std::copy(key, key + 4, c->hint_key);
+        std::fill(c->rank_hint, c->rank_hint + 32, -1);
+      }
+    }
+    static const bool use_hints = std::getenv("HX_NO_RANK_HINT") == nullptr;
     cudaStream_t s = c->s;
     CK(cudaEventRecord(c->ev[0], s));
 
@@ -1033,6 +1163,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
           l = std::min(f.mu, cfg->k_max + over);
         } else if (f.l == 0) {
           l = cfg->sketch0 > 0 ? cfg->sketch0 : default_sketch(f.mu);
+          const int h = c->rank_hint[ilog2(f.mu)];
+          if (cfg->sketch0 <= 0 && h >= 0 && use_hints)
+            l = std::min(l, std::max(16, (h + over + 4 + 7) & ~7));
         } else {
           l = 2 * f.l;
         }
@@ -1379,6 +1512,10 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       ++rounds;
     }
     CK(cudaEventRecord(c->ev[3], s));
+    for (const FarBlock& f : fb) {
+      int& h = c->rank_hint[ilog2(f.mu)];
+      h = std::max(h, f.rank);
+    }
 
     // ---- 4. output factors
     const int nf = int(fb.size());
@@ -1541,6 +1678,42 @@ extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const
     dg.release();
     ds.release();
     tmp.s = nullptr;
+    return HX_OK;
+  });
+}
+
+extern "C" int hx_debug_qr(int n_jobs, const int32_t* p, const int32_t* q, double* X,
+                           double* R) {
+  return guarded([&]() -> int {
+    if (n_jobs < 0 || (n_jobs && (!p || !q || !X || !R))) return fail(HX_EINVAL, "bad arguments");
+    int64_t nx = 0, nr = 0;
+    for (int i = 0; i < n_jobs; ++i) {
+      if (p[i] < 1 || q[i] < 1 || q[i] > JAC_QMAX || q[i] > p[i])
+        return fail(HX_EINVAL, "bad panel shape");
+      nx += int64_t(p[i]) * q[i];
+      nr += int64_t(q[i]) * q[i];
+    }
+    hx_ctx tmp;
+    tmp.s = nullptr;
+    DArr<double> dx, dr;
+    dx.upload(X, size_t(nx), nullptr);
+    dr.ensure(size_t(std::max<int64_t>(nr, 1)));
+    std::vector<QrJob> jobs;
+    int64_t ox = 0, orr = 0;
+    for (int i = 0; i < n_jobs; ++i) {
+      jobs.push_back(QrJob{dx.p + ox, dr.p + orr, p[i], q[i]});
+      ox += int64_t(p[i]) * q[i];
+      orr += int64_t(q[i]) * q[i];
+    }
+    run_qr(&tmp, jobs);
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(X, dx.p, size_t(nx) * 8, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(R, dr.p, size_t(nr) * 8, cudaMemcpyDeviceToHost));
+    dx.release();
+    dr.release();
+    tmp.qr_jobs.release();
+    tmp.ts_jobs.release();
+    tmp.tsqr_ws.release();
     return HX_OK;
   });
 }

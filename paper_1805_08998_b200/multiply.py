@@ -331,6 +331,56 @@ def chunk_masks(bct, n_chunks, base_mask=None):
     return [m for m in out if m.any()]
 
 
+def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8):
+    """Multi-GPU partition of the output leaves: whole subtrees (the chunk
+    units: subtrees at the first block level holding a far leaf, split further while
+    there are fewer than ``min_units_per_rank`` per rank or one unit outweighs a quarter of
+    a rank's share) go to ranks by longest-processing-time greedy on their summed leaf
+    cost.  A rank then forms only the terms of its own subtrees (plus the few created at
+    the split points), so no term formation is repeated across ranks the way a leaf-wise
+    partition would repeat it at every shared ancestor.  ``leaf_cost`` is indexed by node
+    id.  Returns (owner rank per unit, the units, per-rank load, per-rank leaf masks)."""
+    arr = block_arrays(bct)
+    leaf = arr.kind_code != 0
+    cc = np.concatenate([[0.0], np.cumsum(np.where(leaf, leaf_cost, 0.0))])
+
+    def cost(u):
+        return float(cc[u[1]] - cc[u[0]])
+
+    units = [(u[0], u[1]) for u in chunk_units(bct)]
+    total = cost((0, arr.n_nodes))
+    frozen = set()  # leaf units (nothing to split)
+    for _ in range(64 * world):
+        cand = [j for j in range(len(units)) if units[j] not in frozen]
+        if not cand:
+            break
+        i = max(cand, key=lambda j: cost(units[j]))
+        if len(units) >= min_units_per_rank * world and \
+                max(cost(u) for u in units) <= total / (4.0 * world):
+            break
+        parts = split_chunk(bct, [(units[i][0], units[i][1], 0.0)])
+        if len(parts) == 1:
+            frozen.add(units[i])
+            continue
+        # the unit root is an inner block without payload: its children's subtrees cover it
+        units[i:i + 1] = [(p[0][0], p[0][1]) for p in parts]
+    ucost = np.array([cost(u) for u in units])
+    owner = np.zeros(len(units), dtype=np.int64)
+    load = np.zeros(world)
+    for i in np.argsort(-ucost, kind="stable"):
+        r = int(np.argmin(load))
+        owner[i] = r
+        load[r] += ucost[i]
+    masks = []
+    for r in range(world):
+        m = np.zeros(arr.n_nodes, dtype=np.uint8)
+        for (b0, b1), o in zip(units, owner):
+            if o == r:
+                m[b0:b1] = leaf[b0:b1]
+        masks.append(m)
+    return owner, units, load, masks
+
+
 def plan_bytes(info):
     """Device workspace a plan needs (the buffers hx_product sizes from it)."""
     return 8.0 * (info.term_elems + info.tile_elems + info.core_elems + info.gather_elems) + \
@@ -421,6 +471,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
+    for d in (dev, Device._aux.get(device)):
+        if d is not None:
+            _lib.check(_lib.lib().hx_ctx_reset_hints(d.h), "hx_ctx_reset_hints")
     if os.environ.get("HX_TIMING"):
         _lib.lib().hx_timeline_epoch()
     marks = [("start", time.perf_counter())]

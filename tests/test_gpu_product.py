@@ -179,8 +179,10 @@ def test_chunked_product_matches_single(golden, chunks):
         q = many.data[b]
         if hasattr(p, "left"):
             assert p.rank == q.rank
+            # later chunks start from sketch widths narrowed by the earlier chunks' ranks
+            # (rank hints), so the factors differ at the truncation level, not beyond it
             d = np.linalg.norm(p.to_dense() - q.to_dense())
-            assert d <= 1e-12 * max(np.linalg.norm(p.to_dense()), 1e-300)
+            assert d <= 1e-2 * tol * max(np.linalg.norm(p.to_dense()), 1e-300)
         else:
             assert np.array_equal(p, q)
     assert many.report.far_leaves == one.report.far_leaves

@@ -1,4 +1,4 @@
-"""Multi-GPU host logic on CPU: LPT partition of output leaves over ranks and the masked
+"""Multi-GPU host logic on CPU: LPT partition of output subtrees over ranks and the masked
 per-rank plans (world size 2, gloo)."""
 
 import os
@@ -46,16 +46,18 @@ def _worker(rank, world, port, out):
     bct, d = _cfg1_plan_inputs()
     full = _lib.Plan(hmatrix.tree_arrays(bct), d, d, None, multiply.plan_tile(bct))
     lv = full.leaves()
-    owner, _ = bench.lpt_partition(bench.leaf_costs(lv), world)
-    mask = np.zeros(bct.n_nodes, np.uint8)
-    mask[lv["ids"][owner == rank]] = 1
+    cost = np.zeros(bct.n_nodes)
+    cost[lv["ids"]] = bench.leaf_costs(lv)
+    mask = multiply.subtree_partition(bct, cost, world)[3][rank]
     mine = _lib.Plan(hmatrix.tree_arrays(bct), d, d, mask, multiply.plan_tile(bct))
     ml = mine.leaves()
     got = [None] * world
     dist.all_gather_object(got, {"ids": ml["ids"].tolist(), "K": ml["K"].tolist(),
-                                 "flops_near": mine.info.flops_near})
+                                 "flops_near": mine.info.flops_near,
+                                 "flops_form": mine.info.flops_form})
     if rank == 0:
-        out.put((lv["ids"].tolist(), lv["K"].tolist(), full.info.flops_near, got))
+        out.put((lv["ids"].tolist(), lv["K"].tolist(), full.info.flops_near, got,
+                 full.info.flops_form))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -77,7 +79,7 @@ def test_masked_plans_cover_all_leaves_world2():
     procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
     for p in procs:
         p.start()
-    ids, K, fnear, got = q.get(timeout=300)
+    ids, K, fnear, got, fform = q.get(timeout=300)
     for p in procs:
         p.join(timeout=300)
         assert p.exitcode == 0
@@ -89,3 +91,27 @@ def test_masked_plans_cover_all_leaves_world2():
         for i, k in zip(g["ids"], g["K"]):
             assert kfull[i] == k
     assert np.isclose(sum(g["flops_near"] for g in got), fnear)
+    # whole subtrees per rank: term formation is (almost) not repeated across ranks
+    assert sum(g["flops_form"] for g in got) <= 1.05 * fform
+
+
+def test_subtree_partition_covers_and_balances():
+    import bench
+    from paper_1805_08998_b200 import _lib, hmatrix, multiply
+
+    bct, d = _cfg1_plan_inputs()
+    full = _lib.Plan(hmatrix.tree_arrays(bct), d, d, None, multiply.plan_tile(bct))
+    lv = full.leaves()
+    cost = np.zeros(bct.n_nodes)
+    cost[lv["ids"]] = bench.leaf_costs(lv)
+    for world in (1, 2, 3, 8):
+        owner, units, load, masks = multiply.subtree_partition(bct, cost, world)
+        tot = np.sum(masks, axis=0)
+        leaf = bct.kind_code != 0
+        assert np.array_equal(tot, leaf.astype(tot.dtype))   # every leaf exactly once
+        assert np.isclose(load.sum(), cost[leaf].sum())
+        # units are disjoint subtrees in pre-order
+        spans = sorted(units)
+        assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
+        ucost = [cost[u0:u1].sum() for u0, u1 in units]
+        assert load.max() <= load.mean() + max(ucost) + 1e-9

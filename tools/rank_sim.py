@@ -1,0 +1,78 @@
+"""Per-rank product time of a multi-GPU partition, measured one rank at a time on ONE GPU.
+
+Each rank's masked product (its output subtrees; operands resident) runs alone on the
+device, so its time is what that rank would take on its own B200 (no rank waits on
+another).  The predicted N-GPU step is the max over ranks; speed-up = t(1) / max.
+The NCCL operand broadcast is not part of the product step (it happens once, at setup).
+
+usage: python tools/rank_sim.py CFG [--worlds 2,4,8] [--steps 3] [--leafwise]
+"""
+import argparse
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import bench  # noqa: E402
+import paper_1805_08998_b200 as hx  # noqa: E402
+from paper_1805_08998_b200 import _lib, configs, hmatrix, multiply  # noqa: E402
+
+
+def timed(A, B, cfg, mask, steps):
+    import torch
+    for _ in range(2):
+        multiply.multiply_device(A, B, cfg, leaf_mask=mask, fetch=False)
+    ts = []
+    for _ in range(steps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        C = multiply.multiply_device(A, B, cfg, leaf_mask=mask, fetch=False)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+    return float(np.median(ts)) * 1e3, C.report
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg", type=int)
+    ap.add_argument("--worlds", default="2,4,8")
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--leafwise", action="store_true", help="old leaf-wise LPT partition")
+    a = ap.parse_args()
+    c = configs.CONFIGS[a.cfg]
+    bct, A, B = configs.build_operands(c)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(c["tol"]))
+    _, dA = multiply.operand_directory(A)
+    _, dB = multiply.operand_directory(B)
+    full = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, None,
+                     multiply.plan_tile(bct))
+    lv = full.leaves()
+    cost = np.zeros(bct.n_nodes)
+    cost[lv["ids"]] = bench.leaf_costs(lv)
+    t1, r1 = timed(A, B, cfg, None, a.steps)
+    print(f"cfg{a.cfg} world 1: {t1:.1f} ms (form {r1.form_ms:.1f} mat {r1.materialize_ms:.1f} "
+          f"recomp {r1.recompress_ms:.1f})", flush=True)
+    for w in [int(x) for x in a.worlds.split(",")]:
+        if a.leafwise:
+            owner, load = bench.lpt_partition(bench.leaf_costs(lv), w)
+            masks = []
+            for r in range(w):
+                m = np.zeros(bct.n_nodes, np.uint8)
+                m[lv["ids"][owner == r]] = 1
+                masks.append(m)
+        else:
+            _, units, load, masks = multiply.subtree_partition(bct, cost, w)
+        per = []
+        for r in range(w):
+            t, rep = timed(A, B, cfg, masks[r], a.steps)
+            per.append(t)
+            print(f"  world {w} rank {r}: {t:.1f} ms (form {rep.form_ms:.1f} "
+                  f"mat {rep.materialize_ms:.1f} recomp {rep.recompress_ms:.1f}) "
+                  f"load {load[r] / load.sum():.3f}", flush=True)
+        print(f"world {w}: max {max(per):.1f} ms mean {np.mean(per):.1f} ms "
+              f"speed-up {t1 / max(per):.2f}x (efficiency {t1 / max(per) / w:.2f})", flush=True)
+
+
+if __name__ == "__main__":
+    main()
