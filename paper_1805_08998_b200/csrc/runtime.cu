@@ -453,8 +453,14 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
   if (jobs.empty()) return;
   // TSQR decomposition of the tall panels (qr_rows.cuh): up-sweep levels of QR jobs and
   // down-sweep slab products; offsets into one workspace, sized before any pointer is taken
+  // panels up to ~2k rows are many (config 2: the 512- and 1024-blocks) and one CTA each
+  // is faster there; TSQR pays for the few very tall panels of the largest blocks
+  static const int ts_min = std::getenv("HX_TSQR_MIN") ? std::atoi(std::getenv("HX_TSQR_MIN"))
+                                                       : 2048;
   static const bool no_tsqr = std::getenv("HX_NO_TSQR") != nullptr;
-  auto tall = [](const QrJob& j) { return !no_tsqr && j.q <= TS_QMAX && j.p > 2 * TS_BLOCK; };
+  auto tall = [](const QrJob& j) {
+    return !no_tsqr && j.q <= TS_QMAX && j.p > std::max(ts_min, 2 * TS_BLOCK);
+  };
   int64_t ws = 0;
   for (const QrJob& j : jobs) {
     if (!tall(j)) continue;
@@ -1164,8 +1170,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         } else if (f.l == 0) {
           l = cfg->sketch0 > 0 ? cfg->sketch0 : default_sketch(f.mu);
           const int h = c->rank_hint[ilog2(f.mu)];
-          if (cfg->sketch0 <= 0 && h >= 0 && use_hints)
-            l = std::min(l, std::max(16, (h + over + 4 + 7) & ~7));
+          // narrowed only when the saving is large: a hint that undershoots costs a retry
+          const int lh = std::max(16, (h + over + 8 + 7) & ~7);
+          if (cfg->sketch0 <= 0 && h >= 0 && use_hints && 4 * lh <= 3 * l) l = lh;
         } else {
           l = 2 * f.l;
         }

@@ -399,26 +399,53 @@ def available_bytes(dev):
     return free
 
 
-def default_chunks(bct, dev=None, overlap=None):
+def default_chunks(bct, dev=None, overlap=None, leaf_mask=None):
     """(chunks, overlap): enough chunks to keep one chunk's device workspace (materialized
     blocks plus term factors, ~12x the leaf area on the BASELINE configs) within ~60% of
     free memory.  A large product that fits whole runs instead as 3 chunks alternating
     over two contexts: one chunk's latency-bound recompression overlaps the next chunk's
-    term formation (config 2: 427 -> 389 ms).  Memory-bound products do not overlap (two
-    chunks in flight would halve the chunk size and repeat more ancestor work)."""
+    term formation (config 2: 427 -> 389 ms).  Memory-bound products overlap too, and
+    their chunk sizes adapt (``adaptive``): the first chunk's plan gives the workspace per
+    unit of leaf area, and the remaining subtrees are regrouped into chunks that fill the
+    per-context budget (config 4: 256 -> ~40 chunks).  Returns (chunks, overlap, adaptive)."""
     env = os.environ.get("HX_CHUNKS")
     if env:
         n = max(1, int(env))
-        return n, n > 1 and overlap_default(overlap)
-    area = sum(u[2] for u in chunk_units(bct))
+        return n, n > 1 and overlap_default(overlap), False
+    if leaf_mask is None:
+        area = sum(u[2] for u in chunk_units(bct))
+    else:  # a rank's share of a multi-GPU partition
+        arr = block_arrays(bct)
+        lo, hi = arr.tree.lo, arr.tree.hi
+        own = np.flatnonzero(np.asarray(leaf_mask) != 0)
+        area = float(np.sum((hi[arr.tau[own]] - lo[arr.tau[own]]) *
+                            (hi[arr.sigma[own]] - lo[arr.sigma[own]])))
     free = 60e9
     if dev is not None:
         free = available_bytes(dev)
     need = area * 8.0 * 12.0
     n = max(1, int(np.ceil(need / (0.6 * free))))
-    if n == 1 and area >= 2.5e8 and overlap_default(overlap):
-        return 3, True
-    return n, False
+    if n == 1:
+        if area >= float(os.environ.get("HX_OVERLAP_AREA", 2.5e8)) and overlap_default(overlap):
+            return 3, True, False
+        return 1, False, False
+    return n, overlap_default(overlap), os.environ.get("HX_ADAPTIVE_CHUNKS", "1") != "0"
+
+
+def regroup_units(groups, rate, target):
+    """Consecutive units of the remaining chunks merged into chunks whose estimated
+    workspace (rate x leaf area) stays within target bytes."""
+    out, cur, acc = [], [], 0.0
+    for u in (u for g in groups for u in g):
+        est = rate * u[2]
+        if cur and acc + est > target:
+            out.append(cur)
+            cur, acc = [], 0.0
+        cur.append(u)
+        acc += est
+    if cur:
+        out.append(cur)
+    return out
 
 
 # --------------------------------------------------------------------------- product
@@ -496,8 +523,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                            int(sketch0), int(oversample))
     ta = tree_arrays(h.bct)
     tile = plan_tile(h.bct)
+    adaptive = False
     if chunks is None:
-        nch, use_overlap = default_chunks(h.bct, dev, overlap)
+        nch, use_overlap, adaptive = default_chunks(h.bct, dev, overlap, leaf_mask)
     else:
         nch = max(1, int(chunks))
         use_overlap = nch > 1 and overlap_default(overlap)
@@ -568,6 +596,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             plan.close()
 
     chunks_out = []
+    seen = [0.0, 0.0]  # planned workspace bytes and leaf area (adaptive chunking)
     inflight = collections.deque()
     group = queue.popleft()
     plan = make_plan(group)
@@ -582,6 +611,14 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             group = parts[0]
             queue.extendleft(reversed(parts[1:]))
             plan = make_plan(group)
+        if adaptive and plan is not None and queue:
+            # workspace per unit of leaf area over the plans so far (self-correcting: the
+            # first subtrees hold the dense diagonal); the rest is regrouped to fill budget
+            seen[0] += plan_bytes(plan.info)
+            seen[1] += sum(u[2] for u in group)
+            if seen[1] > 0:
+                queue = collections.deque(regroup_units(list(queue), seen[0] / seen[1],
+                                                        0.7 * budget))
         if plan is not None:
             if len(inflight) >= len(ctxs):  # the context of chunk i - 2 must be free
                 t = inflight.popleft()

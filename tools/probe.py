@@ -56,7 +56,8 @@ def main():
         info = C.plan_info
         print(f"wall {time.time()-t0:.3f}s plan {r.plan_ms:.0f}ms dev {r.device_ms:.1f}ms "
               f"form {r.form_ms:.1f} mat {r.materialize_ms:.1f} recomp {r.recompress_ms:.1f} "
-              f"rounds {r.sketch_rounds} launches {r.launches} maxr {r.max_far_rank}", flush=True)
+              f"rounds {r.sketch_rounds} launches {r.launches} chunks {r.chunks} maxr {r.max_far_rank}",
+              flush=True)
     print({f[0]: getattr(info, f[0]) for f in info._fields_ if f[0] != "created"}, flush=True)
     ranks = C.leaf_rank[C.plan_leaves["kind"] == 1]
     ms = C.plan_leaves["m"][C.plan_leaves["kind"] == 1]
