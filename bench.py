@@ -299,7 +299,8 @@ def bench_ours(args, rank, world, local):
         lv = full.leaves()
         cost = np.zeros(bct.n_nodes)
         cost[lv["ids"]] = leaf_costs(lv)
-        mask = multiply.subtree_partition(bct, cost, world)[3][rank]
+        mask = multiply.subtree_partition(
+            bct, cost, world, unit_cost=lambda us: multiply.plan_unit_costs(A, B, us))[3][rank]
         full.close()
     setup_s = time.time() - t_setup
     # tensor-core work of this rank's plan (outside the timed region)

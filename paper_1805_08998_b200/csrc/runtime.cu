@@ -264,6 +264,67 @@ struct GemmSet {
         tiles.push_back(tl);
       }
   }
+  // Like cover() for a sum of terms that each meet only a band of output rows, [lo,
+  // lo + len) (band (0, R): every row): each 64-row tile lists only the terms whose band
+  // meets it, through group entries over runs of terms sharing a band (terms are stored
+  // once, full-band ones first), instead of staging every term of the sum in every tile.
+  void cover_banded(const std::vector<Term>& ts, const std::vector<std::pair<int, int>>& band,
+                    uint8_t out_buf, int64_t out_off, int32_t ld, int R, int C, int row0,
+                    int col0) {
+    std::vector<int> o(ts.size());
+    for (size_t i = 0; i < o.size(); ++i) o[i] = int(i);
+    auto full = [&](int i) { return band[size_t(i)].first <= 0 && band[size_t(i)].second >= R; };
+    std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
+      const bool fa = full(a), fb = full(b);
+      if (fa != fb) return fa;
+      if (!fa && band[size_t(a)] != band[size_t(b)]) return band[size_t(a)] < band[size_t(b)];
+      // one staging layout per chunk: keep equal layouts adjacent
+      const int la = ts[size_t(a)].a_kc * 4 + ts[size_t(a)].b_kc;
+      const int lb = ts[size_t(b)].a_kc * 4 + ts[size_t(b)].b_kc;
+      return la < lb;
+    });
+    const int32_t t0 = int32_t(terms.size());
+    int32_t nf = 0;
+    struct Run {
+      int lo, hi;
+      int32_t b, e;
+    };
+    std::vector<Run> runs;
+    for (int i : o) {
+      const int32_t t = int32_t(terms.size());
+      terms.push_back(ts[size_t(i)]);
+      if (full(i)) {
+        ++nf;
+        continue;
+      }
+      const int lo = band[size_t(i)].first, hi = lo + band[size_t(i)].second;
+      if (!runs.empty() && runs.back().lo == lo && runs.back().hi == hi)
+        runs.back().e = t + 1;
+      else
+        runs.push_back(Run{lo, hi, t, t + 1});
+    }
+    for (int j = 0; j < C; j += 64)
+      for (int i = 0; i < R; i += 64) {
+        Tile tl;
+        std::memset(&tl, 0, sizeof(tl));
+        tl.out_off = out_off + i + int64_t(j) * ld;
+        tl.out_ld = ld;
+        tl.row0 = row0 + i;
+        tl.col0 = col0 + j;
+        tl.rows = int16_t(std::min(64, R - i));
+        tl.cols = int16_t(std::min(64, C - j));
+        tl.g_begin = int32_t(groups.size());
+        if (nf) groups.push_back(Group{t0, t0 + nf});
+        for (const Run& r : runs)
+          if (r.lo < i + 64 && r.hi > i) groups.push_back(Group{r.b, r.e});
+        if (int32_t(groups.size()) == tl.g_begin) groups.push_back(Group{t0, t0});
+        tl.g_end = int32_t(groups.size());
+        tl.aux = -1;
+        tl.out_buf = out_buf;
+        tl.mode = MODE_STORE;
+        tiles.push_back(tl);
+      }
+  }
   void cut() { cuts.push_back(tiles.size()); }
   size_t count(int b) const { return cuts[size_t(b) + 1] - cuts[size_t(b)]; }
 };
@@ -1274,20 +1335,22 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         } else if (f.implicit) {
           const OutLeaf& L = P->leaves[f.leaf];
           std::vector<Term> ts;
+          std::vector<std::pair<int, int>> band;
           for (const ImplTerm& x : f.it) {
             Term y = mk(x.t.a_buf, x.t.a_off, x.t.a_ld, x.t.a_kc, BUF_CORE, f.zoff + x.zrow,
                         int32_t(f.zrows), 1, x.k, x.t.rows, l + PR);
             y.r_lo = x.t.r_lo;
             ts.push_back(y);
+            band.emplace_back(x.ri, x.rn);
           }
           if (L.tile_end > L.tile_begin) {  // + T_sub Omega (the materialized sub-blocks)
             Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
                         f.n, f.m, l + PR);
             y.r_lo = int32_t(L.row0);
             ts.push_back(y);
+            band.emplace_back(0, f.m);
           }
-          const int32_t g = gm.group(ts.data(), ts.size());
-          gm.cover(g, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0);
+          gm.cover_banded(ts, band, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0);
         } else {
           const Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
                             f.n, f.m, l);
@@ -1364,20 +1427,22 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         if (f.implicit) {
           const OutLeaf& L = P->leaves[f.leaf];
           std::vector<Term> ts;
+          std::vector<std::pair<int, int>> band;
           for (const ImplTerm& x : f.it) {
             // R_t(j, kk) = Q_t(kk, j)
             Term y = mk(x.t.b_buf, x.t.b_off, x.t.b_ld, uint8_t(x.t.b_kc ? 1 : 0), BUF_CORE,
                         f.zoff + x.wrow, int32_t(f.zrows), 1, x.k, x.t.cols, l);
             y.r_lo = x.t.c_lo;
             ts.push_back(y);
+            band.emplace_back(x.ci, x.cn);
           }
           if (L.tile_end > L.tile_begin) {  // + T_sub^T Q
             Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
             y.r_lo = int32_t(L.col0);
             ts.push_back(y);
+            band.emplace_back(0, f.n);
           }
-          const int32_t g = gm.group(ts.data(), ts.size());
-          gm.cover(g, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0);
+          gm.cover_banded(ts, band, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0);
         } else {
           const Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
           const int32_t g = gm.group(&y, 1);

@@ -331,7 +331,7 @@ def chunk_masks(bct, n_chunks, base_mask=None):
     return [m for m in out if m.any()]
 
 
-def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8):
+def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8, unit_cost=None):
     """Multi-GPU partition of the output leaves: whole subtrees (the chunk
     units: subtrees at the first block level holding a far leaf, split further while
     there are fewer than ``min_units_per_rank`` per rank or one unit outweighs a quarter of
@@ -339,7 +339,9 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8):
     cost.  A rank then forms only the terms of its own subtrees (plus the few created at
     the split points), so no term formation is repeated across ranks the way a leaf-wise
     partition would repeat it at every shared ancestor.  ``leaf_cost`` is indexed by node
-    id.  Returns (owner rank per unit, the units, per-rank load, per-rank leaf masks)."""
+    id; ``unit_cost(units) -> costs`` (optional) prices the final units for the greedy
+    assignment, e.g. from their own plans (``plan_unit_costs``).  Returns (owner rank per
+    unit, the units, per-rank load, per-rank leaf masks)."""
     arr = block_arrays(bct)
     leaf = arr.kind_code != 0
     cc = np.concatenate([[0.0], np.cumsum(np.where(leaf, leaf_cost, 0.0))])
@@ -364,7 +366,8 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8):
             continue
         # the unit root is an inner block without payload: its children's subtrees cover it
         units[i:i + 1] = [(p[0][0], p[0][1]) for p in parts]
-    ucost = np.array([cost(u) for u in units])
+    ucost = np.array([cost(u) for u in units]) if unit_cost is None else \
+        np.asarray(unit_cost(units), dtype=float)
     owner = np.zeros(len(units), dtype=np.int64)
     load = np.zeros(world)
     for i in np.argsort(-ucost, kind="stable"):
@@ -379,6 +382,37 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8):
                 m[b0:b1] = leaf[b0:b1]
         masks.append(m)
     return owner, units, load, masks
+
+
+# per-phase rates of one B200 on config 2 (isolated phase times / plan work): term
+# formation ~3.8 TB/s of canonical bytes, materialization ~28 TFLOP/s, recompression
+# ~2.4 us per far leaf plus its sketch work
+FORM_BPS = 3.8e12
+MAT_FPS = 28e12
+FAR_S = 2.4e-6
+
+
+def plan_unit_costs(h, k, units, tile=None):
+    """Estimated device seconds of each unit (a subtree's masked plan): formation bytes,
+    materialization flops of its near and far leaves and a per-far-leaf recompression
+    term.  For the multi-GPU partition (planning is host work outside the timed step)."""
+    arr = block_arrays(h.bct)
+    leaf = arr.kind_code != 0
+    _, da = operand_directory(h)
+    _, db = (None, da) if k is h else operand_directory(k)
+    ta = tree_arrays(h.bct)
+    tile = tile or plan_tile(h.bct)
+    out = []
+    for b0, b1 in units:
+        m = np.zeros(arr.n_nodes, dtype=np.uint8)
+        m[b0:b1] = leaf[b0:b1]
+        p = _lib.Plan(ta, da, db, m, tile)
+        lv = p.leaves()
+        far = lv["kind"] == 1
+        mat = float(np.sum(2.0 * lv["m"] * lv["n"] * lv["K"] + lv["fdd"]))
+        out.append(p.info.bytes_form / FORM_BPS + mat / MAT_FPS + FAR_S * float(far.sum()))
+        p.close()
+    return out
 
 
 def plan_bytes(info):

@@ -20,7 +20,7 @@ def _cfg1_plan_inputs():
     A = O.assemble_o("exp", obt, O.Eps(1e-8), pts)
     H = hx.HMatrix(bct, A.data)
     _, d = hmatrix.pack_operand(H)
-    return bct, d
+    return bct, d, H
 
 
 def test_lpt_partition_balances():
@@ -43,7 +43,7 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    bct, d = _cfg1_plan_inputs()
+    bct, d, H = _cfg1_plan_inputs()
     full = _lib.Plan(hmatrix.tree_arrays(bct), d, d, None, multiply.plan_tile(bct))
     lv = full.leaves()
     cost = np.zeros(bct.n_nodes)
@@ -99,7 +99,7 @@ def test_subtree_partition_covers_and_balances():
     import bench
     from paper_1805_08998_b200 import _lib, hmatrix, multiply
 
-    bct, d = _cfg1_plan_inputs()
+    bct, d, H = _cfg1_plan_inputs()
     full = _lib.Plan(hmatrix.tree_arrays(bct), d, d, None, multiply.plan_tile(bct))
     lv = full.leaves()
     cost = np.zeros(bct.n_nodes)
@@ -115,3 +115,24 @@ def test_subtree_partition_covers_and_balances():
         assert all(a[1] <= b[0] for a, b in zip(spans, spans[1:]))
         ucost = [cost[u0:u1].sum() for u0, u1 in units]
         assert load.max() <= load.mean() + max(ucost) + 1e-9
+
+
+def test_subtree_partition_with_planned_unit_costs():
+    from paper_1805_08998_b200 import multiply
+
+    bct, d, H = _cfg1_plan_inputs()
+    cost = np.ones(bct.n_nodes)
+    seen = []
+
+    def uc(units):
+        c = multiply.plan_unit_costs(H, H, units)
+        seen.append(c)
+        return c
+
+    owner, units, load, masks = multiply.subtree_partition(bct, cost, 4, unit_cost=uc)
+    assert len(seen) == 1 and len(seen[0]) == len(units)
+    assert all(c > 0 for c in seen[0])
+    assert np.isclose(load.sum(), sum(seen[0]))
+    tot = np.sum(masks, axis=0)
+    assert np.array_equal(tot, (bct.kind_code != 0).astype(tot.dtype))
+    assert load.max() <= load.mean() + max(seen[0]) + 1e-12

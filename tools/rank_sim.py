@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--worlds", default="2,4,8")
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--leafwise", action="store_true", help="old leaf-wise LPT partition")
+    ap.add_argument("--leafcost", action="store_true", help="units priced by leaf costs only")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     bct, A, B = configs.build_operands(c)
@@ -62,7 +63,8 @@ def main():
                 m[lv["ids"][owner == r]] = 1
                 masks.append(m)
         else:
-            _, units, load, masks = multiply.subtree_partition(bct, cost, w)
+            uc = None if a.leafcost else (lambda us: multiply.plan_unit_costs(A, B, us))
+            _, units, load, masks = multiply.subtree_partition(bct, cost, w, unit_cost=uc)
         per = []
         for r in range(w):
             t, rep = timed(A, B, cfg, masks[r], a.steps)
