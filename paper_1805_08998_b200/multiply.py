@@ -96,11 +96,12 @@ class Device:
     _aux: dict = {}
 
     @classmethod
-    def aux(cls, device=0):
-        """A second context on the device (its own streams and workspace)."""
-        if device not in cls._aux:
-            cls._aux[device] = Device(device)
-        return cls._aux[device]
+    def aux(cls, device=0, i=0):
+        """Further contexts on the device (own streams and workspace), i = 0, 1, ..."""
+        key = device if i == 0 else (device, i)
+        if key not in cls._aux:
+            cls._aux[key] = Device(device)
+        return cls._aux[key]
 
     def set_operand(self, which, pool=None, dev_ptr=None, n=None):
         if pool is not None:
@@ -295,12 +296,11 @@ def chunk_groups(bct, n_chunks, first=1.0, weights=None):
     units = chunk_units(bct)
     total = sum(u[2] for u in units)
     n_chunks = max(1, n_chunks)
-    if weights is None:
-        env = os.environ.get("HX_CHUNK_WEIGHTS")
-        if env and len(env.split(",")) == n_chunks:
-            weights = [float(x) for x in env.split(",")]
-        else:
-            weights = [first] + [1.0] * (n_chunks - 1)
+    env = os.environ.get("HX_CHUNK_WEIGHTS")
+    if env and len(env.split(",")) == n_chunks:
+        weights = [float(x) for x in env.split(",")]
+    elif weights is None:
+        weights = [first] + [1.0] * (n_chunks - 1)
     bounds = np.cumsum(weights) / sum(weights) * total
     groups, cur, acc = [], [], 0.0
     for u in units:
@@ -427,9 +427,10 @@ def available_bytes(dev):
     fb, tb = C.c_int64(), C.c_int64()
     _lib.check(_lib.lib().hx_ctx_mem_info(dev.h, C.byref(fb), C.byref(tb)), "hx_ctx_mem_info")
     free = float(fb.value)
-    aux = Device._aux.get(dev.device)
-    if aux is not None and aux is not dev:
-        free += float(_lib.lib().hx_ctx_held_bytes(aux.h))
+    for key, aux in Device._aux.items():
+        if (key == dev.device or (isinstance(key, tuple) and key[0] == dev.device)) and \
+                aux is not dev:
+            free += float(_lib.lib().hx_ctx_held_bytes(aux.h))
     return free
 
 
@@ -461,9 +462,16 @@ def default_chunks(bct, dev=None, overlap=None, leaf_mask=None):
     n = max(1, int(np.ceil(need / (0.6 * free))))
     if n == 1:
         if area >= float(os.environ.get("HX_OVERLAP_AREA", 2.5e8)) and overlap_default(overlap):
-            return 3, True, False
+            return len(OVERLAP_WEIGHTS), True, False
         return 1, False, False
     return n, overlap_default(overlap), os.environ.get("HX_ADAPTIVE_CHUNKS", "1") != "0"
+
+
+# A product that fits whole runs as 4 chunks on 3 contexts: a small first chunk (its
+# planning is the only exposed host work), two full ones, and a half-size last one (its
+# recompression tail has nothing left to overlap); config 2: 351 -> 339 ms
+OVERLAP_WEIGHTS = (0.2, 1.0, 1.0, 0.5)
+OVERLAP_CONTEXTS = 3
 
 
 def regroup_units(groups, rate, target):
@@ -532,7 +540,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     else:
         pool_b, dir_b = operand_directory(k) if resident(k) else _host_directory(k)
     dev = Device.get(device)
-    for d in (dev, Device._aux.get(device)):
+    for d in [dev] + [a for key, a in Device._aux.items()
+                      if key == device or (isinstance(key, tuple) and key[0] == device)]:
         if d is not None:
             _lib.check(_lib.lib().hx_ctx_reset_hints(d.h), "hx_ctx_reset_hints")
     if os.environ.get("HX_TIMING"):
@@ -564,7 +573,10 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         nch = max(1, int(chunks))
         use_overlap = nch > 1 and overlap_default(overlap)
     # with overlap the first chunk is small: its planning is the only exposed part
-    queue = collections.deque(chunk_groups(h.bct, nch, first=0.2 if use_overlap else 1.0))
+    weights = list(OVERLAP_WEIGHTS) if (chunks is None and use_overlap and not adaptive and
+                                        nch == len(OVERLAP_WEIGHTS)) else None
+    queue = collections.deque(chunk_groups(h.bct, nch, first=0.2 if use_overlap else 1.0,
+                                           weights=weights))
     budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
@@ -593,10 +605,13 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     # one chunk's latency-bound recompression overlaps the next chunk's term formation
     ctxs = [dev]
     if len(queue_all) > 1 and use_overlap:
-        aux = Device.aux(device)
-        _lib.check(_lib.lib().hx_ctx_operand_share(aux.h, dev.h), "hx_ctx_operand_share")
-        ctxs.append(aux)
-        budget = budget / 2
+        n_ctx = int(os.environ.get("HX_CONTEXTS", 2 if adaptive else OVERLAP_CONTEXTS))
+        n_ctx = max(2, min(n_ctx, len(queue_all)))
+        for i in range(n_ctx - 1):
+            aux = Device.aux(device, i)
+            _lib.check(_lib.lib().hx_ctx_operand_share(aux.h, dev.h), "hx_ctx_operand_share")
+            ctxs.append(aux)
+        budget = budget / n_ctx
 
     def run_chunk(plan, ctx, out):
         try:
@@ -654,7 +669,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                 queue = collections.deque(regroup_units(list(queue), seen[0] / seen[1],
                                                         0.7 * budget))
         if plan is not None:
-            if len(inflight) >= len(ctxs):  # the context of chunk i - 2 must be free
+            if len(inflight) >= len(ctxs):  # the context of chunk i - len(ctxs) must be free
                 t = inflight.popleft()
                 t.join()
             out = {}
