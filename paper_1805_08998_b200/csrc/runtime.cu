@@ -380,6 +380,7 @@ struct hx_ctx {
   // sketch-width hints: the largest rank seen per log2(min(m, n)) class by earlier chunks
   // of the same product (hx_ctx_reset_hints between products), for the same policy
   int rank_hint[32];
+  int8_t class_retry[32];  // a block of the class needed a wider sketch (retry round)
   double hint_key[4] = {-1, -1, -1, -1};
   int64_t omega_rows = 0;
   int omega_cols = 0;
@@ -809,6 +810,7 @@ extern "C" int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src) {
 extern "C" int hx_ctx_reset_hints(hx_ctx* c) {
   if (!c) return fail(HX_EINVAL, "null context");
   std::fill(c->rank_hint, c->rank_hint + 32, -1);
+  std::fill(c->class_retry, c->class_retry + 32, int8_t(0));
   return HX_OK;
 }
 
@@ -914,6 +916,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       if (!std::equal(key, key + 4, c->hint_key)) {
         std::copy(key, key + 4, c->hint_key);
         std::fill(c->rank_hint, c->rank_hint + 32, -1);
+        std::fill(c->class_retry, c->class_retry + 32, int8_t(0));
       }
     }
     static const bool use_hints = std::getenv("HX_NO_RANK_HINT") == nullptr;
@@ -1231,9 +1234,14 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         } else if (f.l == 0) {
           l = cfg->sketch0 > 0 ? cfg->sketch0 : default_sketch(f.mu);
           const int h = c->rank_hint[ilog2(f.mu)];
-          // narrowed only when the saving is large: a hint that undershoots costs a retry
+          // narrowed only when the saving is large (a hint that undershoots costs a retry);
+          // widened when blocks of this class needed a retry before (config 5's 128-blocks:
+          // ranks up to 19 against a 24-column default sketch)
           const int lh = std::max(16, (h + over + 8 + 7) & ~7);
-          if (cfg->sketch0 <= 0 && h >= 0 && use_hints && 4 * lh <= 3 * l) l = lh;
+          if (cfg->sketch0 <= 0 && h >= 0 && use_hints) {
+            if (c->class_retry[ilog2(f.mu)]) l = std::max(l, lh);
+            else if (4 * lh <= 3 * l) l = lh;
+          }
         } else {
           l = 2 * f.l;
         }
@@ -1587,6 +1595,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     for (const FarBlock& f : fb) {
       int& h = c->rank_hint[ilog2(f.mu)];
       h = std::max(h, f.rank);
+      if (f.round > 0) c->class_retry[ilog2(f.mu)] = 1;
     }
 
     // ---- 4. output factors

@@ -390,12 +390,16 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8, unit_cost=Non
 FORM_BPS = 3.8e12
 MAT_FPS = 28e12
 FAR_S = 2.4e-6
+# host planning throughput (restrict terms per second, 16 host cores); a rank's wall time is
+# the larger of its device time and its planning time (the two overlap chunk by chunk)
+PLAN_TPS = 8e6
 
 
 def plan_unit_costs(h, k, units, tile=None):
-    """Estimated device seconds of each unit (a subtree's masked plan): formation bytes,
-    materialization flops of its near and far leaves and a per-far-leaf recompression
-    term.  For the multi-GPU partition (planning is host work outside the timed step)."""
+    """Estimated seconds of each unit (a subtree's masked plan): the larger of its device
+    time (formation bytes, materialization flops of its near and far leaves, a per-far-leaf
+    recompression term) and its host planning time (terms of its restrict descent).  For
+    the multi-GPU partition (these plans are made once, outside the timed step)."""
     arr = block_arrays(h.bct)
     leaf = arr.kind_code != 0
     _, da = operand_directory(h)
@@ -410,7 +414,9 @@ def plan_unit_costs(h, k, units, tile=None):
         lv = p.leaves()
         far = lv["kind"] == 1
         mat = float(np.sum(2.0 * lv["m"] * lv["n"] * lv["K"] + lv["fdd"]))
-        out.append(p.info.bytes_form / FORM_BPS + mat / MAT_FPS + FAR_S * float(far.sum()))
+        dev = p.info.bytes_form / FORM_BPS + mat / MAT_FPS + FAR_S * float(far.sum())
+        host = (p.info.n_terms_real + p.info.n_terms_expand) / PLAN_TPS
+        out.append(max(dev, host))
         p.close()
     return out
 
@@ -646,13 +652,23 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
 
     chunks_out = []
     seen = [0.0, 0.0]  # planned workspace bytes and leaf area (adaptive chunking)
+    last_rate = [0.0]  # workspace rate of the last rejected (too large) plan
     inflight = collections.deque()
     group = queue.popleft()
     plan = make_plan(group)
     while True:
         # a chunk whose workspace would not fit is split and planned again
         while plan is not None and plan_bytes(plan.info) > budget:
-            parts = split_chunk(h.bct, group)
+            # split once into as many parts as the measured workspace per leaf area asks
+            # for (not by repeated halving: every rejected plan is wasted host time)
+            pb = plan_bytes(plan.info)
+            area = sum(u[2] for u in group)
+            rate = pb / max(area, 1.0)
+            last_rate[0] = max(last_rate[0], rate)
+            units = group if len(group) > 1 else [p[0] for p in split_chunk(h.bct, group)]
+            parts = regroup_units([units], rate, 0.7 * budget) if len(units) > 1 else [units]
+            if len(parts) == 1:
+                parts = split_chunk(h.bct, units)
             if len(parts) == 1:
                 break
             group_split[0] = True
@@ -661,13 +677,16 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
             queue.extendleft(reversed(parts[1:]))
             plan = make_plan(group)
         if adaptive and plan is not None and queue:
-            # workspace per unit of leaf area over the plans so far (self-correcting: the
-            # first subtrees hold the dense diagonal); the rest is regrouped to fill budget
-            seen[0] += plan_bytes(plan.info)
-            seen[1] += sum(u[2] for u in group)
-            if seen[1] > 0:
-                queue = collections.deque(regroup_units(list(queue), seen[0] / seen[1],
-                                                        0.7 * budget))
+            # workspace per unit of leaf area: the larger of the average over the plans so
+            # far and the latest plan's (dense regions are priced by their own rate); the
+            # remaining subtrees are regrouped to fill the budget
+            pb = plan_bytes(plan.info)
+            area = sum(u[2] for u in group)
+            seen[0] += pb
+            seen[1] += area
+            rate = max(seen[0] / max(seen[1], 1.0), pb / max(area, 1.0), last_rate[0])
+            last_rate[0] = 0.0
+            queue = collections.deque(regroup_units(list(queue), rate, 0.7 * budget))
         if plan is not None:
             if len(inflight) >= len(ctxs):  # the context of chunk i - len(ctxs) must be free
                 t = inflight.popleft()

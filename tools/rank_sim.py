@@ -19,9 +19,9 @@ import paper_1805_08998_b200 as hx  # noqa: E402
 from paper_1805_08998_b200 import _lib, configs, hmatrix, multiply  # noqa: E402
 
 
-def timed(A, B, cfg, mask, steps):
+def timed(A, B, cfg, mask, steps, warm=2):
     import torch
-    for _ in range(2):
+    for _ in range(warm):
         multiply.multiply_device(A, B, cfg, leaf_mask=mask, fetch=False)
     ts = []
     for _ in range(steps):
@@ -38,8 +38,11 @@ def main():
     ap.add_argument("cfg", type=int)
     ap.add_argument("--worlds", default="2,4,8")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warm", type=int, default=2)
     ap.add_argument("--leafwise", action="store_true", help="old leaf-wise LPT partition")
     ap.add_argument("--leafcost", action="store_true", help="units priced by leaf costs only")
+    ap.add_argument("--ranks", default="", help="only these ranks (comma list)")
+    ap.add_argument("--skip-full", action="store_true")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     bct, A, B = configs.build_operands(c)
@@ -51,9 +54,11 @@ def main():
     lv = full.leaves()
     cost = np.zeros(bct.n_nodes)
     cost[lv["ids"]] = bench.leaf_costs(lv)
-    t1, r1 = timed(A, B, cfg, None, a.steps)
-    print(f"cfg{a.cfg} world 1: {t1:.1f} ms (form {r1.form_ms:.1f} mat {r1.materialize_ms:.1f} "
-          f"recomp {r1.recompress_ms:.1f})", flush=True)
+    t1, r1 = (1.0, None) if a.skip_full else timed(A, B, cfg, None, a.steps, a.warm)
+    if r1 is not None:
+        print(f"cfg{a.cfg} world 1: {t1:.1f} ms (form {r1.form_ms:.1f} "
+              f"mat {r1.materialize_ms:.1f} recomp {r1.recompress_ms:.1f})", flush=True)
+    only = [int(x) for x in a.ranks.split(",")] if a.ranks else None
     for w in [int(x) for x in a.worlds.split(",")]:
         if a.leafwise:
             owner, load = bench.lpt_partition(bench.leaf_costs(lv), w)
@@ -67,10 +72,14 @@ def main():
             _, units, load, masks = multiply.subtree_partition(bct, cost, w, unit_cost=uc)
         per = []
         for r in range(w):
-            t, rep = timed(A, B, cfg, masks[r], a.steps)
+            if only is not None and r not in only:
+                per.append(0.0)
+                continue
+            t, rep = timed(A, B, cfg, masks[r], a.steps, a.warm)
             per.append(t)
             print(f"  world {w} rank {r}: {t:.1f} ms (form {rep.form_ms:.1f} "
-                  f"mat {rep.materialize_ms:.1f} recomp {rep.recompress_ms:.1f}) "
+                  f"mat {rep.materialize_ms:.1f} recomp {rep.recompress_ms:.1f} "
+                  f"plan {rep.plan_ms:.1f} chunks {rep.chunks}) "
                   f"load {load[r] / load.sum():.3f}", flush=True)
         print(f"world {w}: max {max(per):.1f} ms mean {np.mean(per):.1f} ms "
               f"speed-up {t1 / max(per):.2f}x (efficiency {t1 / max(per) / w:.2f})", flush=True)
