@@ -120,6 +120,9 @@ struct Builder {
   // every sub-block term, the fully implicit route)
   double sketch_cols = std::getenv("HX_SKETCH_COLS") ? std::atof(std::getenv("HX_SKETCH_COLS"))
                                                      : 56.0;
+  // stacked-core runs start on multiples of this many rows (HX_CORE_ALIGN; 1: packed)
+  int64_t core_align = std::getenv("HX_CORE_ALIGN") ? std::max(1, std::atoi(std::getenv("HX_CORE_ALIGN")))
+                                                    : 8;
 
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
@@ -724,6 +727,9 @@ struct Builder {
         runs.back().count++;
         runs.back().rows += kl;
       } else {
+        // runs start on 8-row boundaries: a run's rows then fill whole 8 x 8 DMMA
+        // fragments instead of sharing a fragment with the previous run's K range
+        row = (row + core_align - 1) / core_align * core_align;
         runs.push_back(CoreRun{j, 1, row, kl});
       }
       if (soff) (*soff)[size_t(idx[size_t(j)])] = row;
@@ -850,22 +856,20 @@ struct Builder {
       subtree_leaves(opX, g.X, g.leaves, g.mv, g.bytes);
       const int64_t ct = nbands(g.ktot, T);
       const int64_t nb = nbands(g.R, T);
-      g.srows = 0;
       g.n_fac_terms = 0;
       for (int l : g.leaves) {
         const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];
-        if (isF(opX, l)) {
-          if (opX.rank[l] == 0) continue;
-          g.srows += opX.rank[l];
-        }
+        if (isF(opX, l) && opX.rank[l] == 0) continue;
         g.n_fac_terms += bands_hit(lo(ol) - lo(g.rows_cl), sz(ol), nb, T);
       }
-      const int64_t nbs = nbands(g.srows, T);
       int64_t terms = 0;
+      int64_t nbs = 0;
       {
         thread_local std::vector<int32_t> idx;
         thread_local std::vector<CoreRun> runs;
         core_layout(g, opX, idx, runs, nullptr);
+        g.srows = runs.empty() ? 0 : runs.back().row + runs.back().rows;
+        nbs = nbands(g.srows, T);
         for (const CoreRun& cr : runs) terms += bands_hit(cr.row, cr.rows, nbs, T);
       }
       g.n_core_terms = terms;
