@@ -501,7 +501,17 @@ void run_gemm_batch(hx_ctx* c, std::vector<Term>& terms, std::vector<Tile>& tile
 // (bucketed by height so that each launch sizes its smem slices tightly), taller ones one
 // CTA each, in shared memory when the panel fits.
 constexpr int QR_WARP_ROWS = 128;
-constexpr int TS_BLOCK = 128;  // TSQR row blocks of 128..255 rows (panels taller than 256)
+// TSQR row blocks of b..2b-1 rows: b = 128 for q <= 32 (blocks go to the register QR
+// kernel), else the tallest b <= 256 whose 2b-row block still fits the shared-memory QR
+// (HX_TSQR_BLOCK overrides)
+int ts_block(int q) {
+  static const int env = std::getenv("HX_TSQR_BLOCK") ? std::atoi(std::getenv("HX_TSQR_BLOCK"))
+                                                      : 0;
+  if (env > 0) return env;
+  if (q <= 32) return 128;
+  const int fit = int(size_t(SMEM_CAP) / (8 * size_t(q) + 8)) / 2;
+  return std::max(64, std::min(256, fit & ~7));
+}
 
 // Shared memory bounds occupancy here, so jobs are bucketed by their smem need (powers of
 // two) and every launch sizes its slices for its own bucket.
@@ -515,20 +525,21 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
   if (jobs.empty()) return;
   // TSQR decomposition of the tall panels (qr_rows.cuh): up-sweep levels of QR jobs and
   // down-sweep slab products; offsets into one workspace, sized before any pointer is taken
-  // panels up to ~2k rows are many (config 2: the 512- and 1024-blocks) and one CTA each
-  // is faster there; TSQR pays for the few very tall panels of the largest blocks
+  // panels above 512 rows (config 2: the 1024-blocks' sketches, which overflow shared
+  // memory; recompression 89 -> 80 ms) and the very tall panels of the largest blocks
   static const int ts_min = std::getenv("HX_TSQR_MIN") ? std::atoi(std::getenv("HX_TSQR_MIN"))
-                                                       : 2048;
+                                                       : 512;
   static const bool no_tsqr = std::getenv("HX_NO_TSQR") != nullptr;
   auto tall = [](const QrJob& j) {
-    return !no_tsqr && j.q <= TS_QMAX && j.p > std::max(ts_min, 2 * TS_BLOCK);
+    return !no_tsqr && j.q <= TS_QMAX && j.p > std::max(ts_min, 2 * ts_block(j.q));
   };
   int64_t ws = 0;
   for (const QrJob& j : jobs) {
     if (!tall(j)) continue;
     int64_t p = j.p;
-    while (p > 2 * TS_BLOCK) {
-      const int64_t nb = p / TS_BLOCK;
+    const int tb = ts_block(j.q);
+    while (p > 2 * tb) {
+      const int64_t nb = p / tb;
       ws += nb * j.q * j.q;
       p = nb * j.q;
     }
@@ -548,7 +559,7 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
     const int q = j.q;
     for (size_t L = 0;; ++L) {
       if (lev.size() <= L) lev.resize(L + 1);
-      if (p <= 2 * TS_BLOCK) {
+      if (p <= 2 * ts_block(q)) {
         QrJob t{X, j.R, p, q};
         t.ldx = ld;
         t.ldr = j.lr();
@@ -556,7 +567,7 @@ void run_qr(hx_ctx* c, const std::vector<QrJob>& jobs) {
         break;
       }
       if (down.size() <= L) down.resize(L + 1);
-      const int nb = p / TS_BLOCK;
+      const int nb = p / ts_block(q);
       const int ls = nb * q;  // rows (and ld) of the stacked R factors
       double* S = c->tsqr_ws.p + pos;
       pos += int64_t(ls) * q;
