@@ -85,7 +85,9 @@ __device__ __forceinline__ void rr_pair(int qe, int r, int k, int& i, int& j) {
   }
 }
 
-__global__ void __launch_bounds__(LA_THREADS) jacobi_svd_kernel(const JacJob* __restrict__ jobs) {
+// One CTA per factor; a warp per column pair of each round-robin round (launched with up to
+// one warp per pair, q/2 warps, so a round costs one pair rotation instead of several).
+__global__ void __launch_bounds__(1024) jacobi_svd_kernel(const JacJob* __restrict__ jobs) {
   extern __shared__ __align__(16) double dsm[];
   __shared__ int rotated;
   __shared__ int order[JAC_QMAX];

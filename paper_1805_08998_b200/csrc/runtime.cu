@@ -739,7 +739,10 @@ void run_jacobi(hx_ctx* c, const std::vector<JacJob>& jobs) {
     const size_t smem = size_t(2) * qs * qs * sizeof(double);
     CK(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             int(std::max<size_t>(smem, 1))));
-    jacobi_svd_kernel<<<int(nb), LA_THREADS, smem, c->s>>>(c->jac_jobs.p + n16 + n32);
+    // one warp per column pair of a round (widest job), 8..32 warps
+    static const int wide = std::getenv("HX_JAC_WIDE") ? std::atoi(std::getenv("HX_JAC_WIDE")) : 1;
+    const int nt = wide ? 32 * std::max(8, std::min(32, (qmax + 1) / 2)) : LA_THREADS;
+    jacobi_svd_kernel<<<int(nb), nt, smem, c->s>>>(c->jac_jobs.p + n16 + n32);
     CK(cudaGetLastError());
     c->launches++;
   }
