@@ -314,3 +314,35 @@ def test_hmx1_operand_roundtrip_product(tmp_path):
     exact = dense @ dense
     err = np.linalg.norm(hx.to_dense(C3) - exact) / np.linalg.norm(exact)
     assert err <= 1e-6, err
+
+
+@pytest.mark.parametrize("n,n_min", [(20, 32), (100, 16), (300, 8)])
+def test_edge_sizes_and_zero_operand(n, n_min):
+    """Degenerate shapes: a single near leaf (n < leaf size), few blocks, leaf 8; and a zero
+    operand (every far leaf rank 0, the product exactly zero, ranks 0)."""
+    import paper_1805_08998_b200 as hx
+
+    rng = np.random.default_rng(n)
+    pts = rng.uniform(0, 1, (n, 2))
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, n_min), 0.8)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, n_min), 0.8)
+    oa = O.assemble_o("exp", obt, O.Eps(1e-8), pts)
+    A = hx.HMatrix(bct, oa.data)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(1e-6))
+    C = hx.hmult_new(A, A, cfg)
+    dense = oa.to_dense()
+    exact = dense @ dense
+    err = np.linalg.norm(hx.to_dense(C) - exact) / np.linalg.norm(exact)
+    assert err <= 1e-6, err
+    ref = O.hmult_new_o(oa, oa, O.Eps(1e-6), "dense-svd")
+    for b, p in ref.data.items():
+        q = C.data[b]
+        if isinstance(p, O.LR):
+            assert abs(q.rank - p.rank) <= 1
+    # zero operand: exact zero product, rank-0 far blocks
+    zdata = {b: (O.LR(np.zeros((p.left.shape[0], 0)), np.zeros((p.right.shape[0], 0)))
+                 if isinstance(p, O.LR) else np.zeros_like(p)) for b, p in oa.data.items()}
+    Z = hx.HMatrix(bct, zdata)
+    CZ = hx.hmult_new(Z, Z, cfg)
+    assert not np.any(hx.to_dense(CZ))
+    assert all(q.rank == 0 for q in CZ.data.values() if hasattr(q, "left"))
