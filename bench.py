@@ -255,6 +255,7 @@ def bench_ours(args, rank, world, local):
     bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, c["n_min"]), c["eta"])
     h = c["n"] ** (-1.0 / 3.0)
     keep = []
+    bcast_ms, bcast_bytes = [], []  # NCCL operand broadcasts (setup, outside the timed step)
 
     def operand(kern):
         if world == 1:
@@ -271,7 +272,14 @@ def bench_ours(args, rank, world, local):
         buf = torch.empty(max(n_el, 1), dtype=torch.float64, device="cuda")
         if rank == 0:
             _copy_pool(H, buf, n_el)
+        e0b = torch.cuda.Event(enable_timing=True)
+        e1b = torch.cuda.Event(enable_timing=True)
+        e0b.record()
         dist.broadcast(buf, src=0)
+        e1b.record()
+        torch.cuda.synchronize()
+        bcast_ms.append(e0b.elapsed_time(e1b))
+        bcast_bytes.append(8 * max(n_el, 1))
         keep.append(buf)
         if rank != 0:
             H = hx.HMatrix(bct, {}, set(deg))
@@ -447,6 +455,12 @@ def bench_ours(args, rank, world, local):
             cpu = {"value": gf / tcpu, "unit": "GFLOP/s", "cores": threads, "kind": "port",
                    "sample": f"reference algorithm (oracle NumPy port, aca compressor) on the "
                              f"first {nl} output leaves in DFS order, {tcpu:.1f}s"}
+            # the reference's own parallelism is BLAS threads only: also one thread
+            from threadpoolctl import threadpool_limits
+            with threadpool_limits(limits=1):
+                gf1, t1, nl1, _ = cpu_sample(args.config, c, A, args.cpu_budget / 4, tag="aca")
+            cpu["one_thread"] = {"value": gf1 / t1, "unit": "GFLOP/s", "cores": 1,
+                                 "sample": f"first {nl1} output leaves, {t1:.1f}s"}
         except Exception as exc:  # pragma: no cover - reported, never fatal
             cpu = {"value": None, "unit": "GFLOP/s", "cores": None, "kind": "port",
                    "sample": f"failed: {exc!r}"}
@@ -468,6 +482,9 @@ def bench_ours(args, rank, world, local):
                               "(CUDA events per phase); timed steps overlap chunks on two "
                               "streams",
             "max_far_rank": rep.max_far_rank, "setup_s": setup_s,
+            "operand_broadcast": ({"ms": float(sum(bcast_ms)), "bytes": int(sum(bcast_bytes)),
+                                   "gbs": float(sum(bcast_bytes) / max(sum(bcast_ms), 1e-9)
+                                                / 1e6)} if world > 1 else None),
             "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "e2e": e2e, "clocks": ck,
         }
