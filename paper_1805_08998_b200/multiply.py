@@ -390,16 +390,16 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8, unit_cost=Non
 FORM_BPS = 3.8e12
 MAT_FPS = 28e12
 FAR_S = 2.4e-6
-# host planning throughput (restrict terms per second, 16 host cores); a rank's wall time is
-# the larger of its device time and its planning time (the two overlap chunk by chunk)
-PLAN_TPS = 8e6
+# a rank's wall time is the larger of its device time and its host planning time (the two
+# overlap chunk by chunk); the planning time of a unit is measured on its own plan
 
 
 def plan_unit_costs(h, k, units, tile=None):
     """Estimated seconds of each unit (a subtree's masked plan): the larger of its device
     time (formation bytes, materialization flops of its near and far leaves, a per-far-leaf
-    recompression term) and its host planning time (terms of its restrict descent).  For
-    the multi-GPU partition (these plans are made once, outside the timed step)."""
+    recompression term) and its host planning time (measured: the time its plan took, work
+    lists included).  For the multi-GPU partition (these plans are made once, outside the
+    timed step)."""
     arr = block_arrays(h.bct)
     leaf = arr.kind_code != 0
     _, da = operand_directory(h)
@@ -407,15 +407,20 @@ def plan_unit_costs(h, k, units, tile=None):
     ta = tree_arrays(h.bct)
     tile = tile or plan_tile(h.bct)
     out = []
+    if units:  # warm-up: the first plan also grows the page-locked plan-array cache
+        m = np.zeros(arr.n_nodes, dtype=np.uint8)
+        m[units[0][0]:units[0][1]] = leaf[units[0][0]:units[0][1]]
+        _lib.Plan(ta, da, db, m, tile).close()
     for b0, b1 in units:
         m = np.zeros(arr.n_nodes, dtype=np.uint8)
         m[b0:b1] = leaf[b0:b1]
-        p = _lib.Plan(ta, da, db, m, tile)
+        t0 = time.perf_counter()
+        p = _lib.Plan(ta, da, db, m, tile)  # all work lists filled: the unit's host work
+        host = time.perf_counter() - t0
         lv = p.leaves()
         far = lv["kind"] == 1
         mat = float(np.sum(2.0 * lv["m"] * lv["n"] * lv["K"] + lv["fdd"]))
         dev = p.info.bytes_form / FORM_BPS + mat / MAT_FPS + FAR_S * float(far.sum())
-        host = (p.info.n_terms_real + p.info.n_terms_expand) / PLAN_TPS
         out.append(max(dev, host))
         p.close()
     return out
