@@ -392,6 +392,7 @@ struct hx_ctx {
   int64_t out_far = 0, near_begin = 0, near_elems = 0;
   int64_t launches = 0;
   cudaEvent_t ev[8];
+  cudaEvent_t up_ev = nullptr;  // end of the last host-to-device operand copy on s
 
   double* buf(int i) {
     if (i == BUF_A) return attached[0] ? attached[0] : own[BUF_A].p;
@@ -780,6 +781,7 @@ extern "C" int hx_ctx_create(int device, hx_ctx** out) {
     CK(cudaStreamCreateWithPriority(&c->s_hi, cudaStreamNonBlocking, hi_prio));
     CK(cudaStreamCreateWithFlags(&c->s3, cudaStreamNonBlocking));
     for (auto& e : c->ev) CK(cudaEventCreate(&e));
+    CK(cudaEventCreateWithFlags(&c->up_ev, cudaEventDisableTiming));
     *out = c;
     return HX_OK;
   });
@@ -796,6 +798,7 @@ extern "C" int hx_ctx_operand(hx_ctx* c, int which, const double* host, const do
       c->own[which].ensure(size_t(n));
       CK(cudaMemcpyAsync(c->own[which].p, host, size_t(n) * sizeof(double),
                          cudaMemcpyHostToDevice, c->s));
+      CK(cudaEventRecord(c->up_ev, c->s));  // contexts sharing the pool wait on this
     } else if (device) {
       c->attached[which] = const_cast<double*>(device);
     } else {
@@ -811,7 +814,9 @@ extern "C" int hx_ctx_operand_share(hx_ctx* dst, hx_ctx* src) {
     if (!dst || !src || dst == src) return fail(HX_EINVAL, "bad contexts");
     if (dst->device != src->device) return fail(HX_EINVAL, "contexts on different devices");
     if (!src->buf(BUF_A) || !src->buf(BUF_B)) return fail(HX_EINVAL, "source operands not set");
-    CK(cudaStreamSynchronize(src->s));  // host-copied pools complete
+    // host-copied pools: the sharing context's stream waits for the upload on the device,
+    // so the host goes on planning the first chunks while the pools are in flight
+    CK(cudaStreamWaitEvent(dst->s, src->up_ev, 0));
     dst->attached[0] = src->buf(BUF_A);
     dst->opnd_elems[0] = src->opnd_elems[0];
     dst->alias = src->alias;
@@ -2012,6 +2017,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   c->rank_d.release();
   c->retry_d.release();
   for (auto& e : c->ev) cudaEventDestroy(e);
+  cudaEventDestroy(c->up_ev);
   cudaStreamDestroy(c->s);
   cudaStreamDestroy(c->s2);
   cudaStreamDestroy(c->s_hi);
