@@ -9,6 +9,8 @@
 //      -> select_rank with the exact unsampled tail -> factors (U S, V)
 //      blocks whose selected rank leaves less than `oversample` spare sketch columns are
 //      redone with a doubled sketch; a sketch that spans the block is exact.
+#include <sched.h>
+
 #include <chrono>
 #include <cuda_runtime.h>
 
@@ -19,6 +21,9 @@
 #include <mutex>
 #include <unordered_set>
 #include <string>
+#include <exception>
+#include <functional>
+#include <thread>
 #include <vector>
 
 #include "dense_la.cuh"
@@ -222,6 +227,7 @@ struct FarBlock {
   // implicit route: terms and the row count of their stacked Z / W blocks
   int implicit = 0;
   std::vector<ImplTerm> it;
+  std::vector<int> zorder, worder;  // it indices by Z row (lr, column band) / W row (row band)
   int64_t zrows = 0;
   int64_t zoff = 0;  // Z / W block in BUF_CORE for this round
   // pointers into that round's workspace
@@ -268,13 +274,17 @@ struct GemmSet {
   // lo + len) (band (0, R): every row): each 64-row tile lists only the terms whose band
   // meets it, through group entries over runs of terms sharing a band (terms are stored
   // once, full-band ones first), instead of staging every term of the sum in every tile.
+  // presorted: ts already come in band order (terms sharing a band adjacent); full-band
+  // terms then form ordinary runs that meet every tile
   void cover_banded(const std::vector<Term>& ts, const std::vector<std::pair<int, int>>& band,
                     uint8_t out_buf, int64_t out_off, int32_t ld, int R, int C, int row0,
-                    int col0) {
+                    int col0, bool presorted = false) {
     std::vector<int> o(ts.size());
     for (size_t i = 0; i < o.size(); ++i) o[i] = int(i);
-    auto full = [&](int i) { return band[size_t(i)].first <= 0 && band[size_t(i)].second >= R; };
-    std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
+    auto full = [&](int i) {
+      return !presorted && band[size_t(i)].first <= 0 && band[size_t(i)].second >= R;
+    };
+    if (!presorted) std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
       const bool fa = full(a), fb = full(b);
       if (fa != fb) return fa;
       if (!fa && band[size_t(a)] != band[size_t(b)]) return band[size_t(a)] < band[size_t(b)];
@@ -336,6 +346,107 @@ struct GatherSet {
   void cut() { cuts.push_back(tiles.size()); }
   size_t count(int b) const { return cuts[size_t(b) + 1] - cuts[size_t(b)]; }
 };
+
+// host threads this process may run on (the affinity mask: a GPU box slice can expose far
+// fewer cores than std::thread::hardware_concurrency reports)
+int host_threads() {
+  static const int n = [] {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, int(CPU_COUNT(&set)));
+    return std::max(1, int(std::thread::hardware_concurrency()));
+  }();
+  return n;
+}
+
+// fn(i) for i < n on host threads (contiguous ranges; the first exception is rethrown)
+void par_for(int n, const std::function<void(int)>& fn) {
+  const int hw = host_threads();
+  const int nt = std::max(1, std::min(hw, n / 8));
+  std::exception_ptr err;
+  std::mutex em;
+  auto run = [&](int t) {
+    try {
+      const int a0 = int(int64_t(n) * t / nt), a1 = int(int64_t(n) * (t + 1) / nt);
+      for (int a = a0; a < a1; ++a) fn(a);
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(em);
+      err = std::current_exception();
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(run, t);
+  run(0);
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+}
+
+// One batch of per-leaf work lists built by host threads over contiguous ranges of the
+// active leaves, merged in leaf order: the same lists as a sequential build (body(i, gm,
+// ga) appends leaf i's terms / tiles / gathered rows to the thread's own sets).
+void par_build(const std::vector<int>& active, GemmSet& gm, GatherSet& ga,
+               const std::function<void(int, GemmSet&, GatherSet&)>& body) {
+  const int n = int(active.size());
+  const int nt = std::max(1, std::min(host_threads(), n / 64));
+  std::vector<GemmSet> gsets(static_cast<size_t>(nt));
+  std::vector<GatherSet> asets(static_cast<size_t>(nt));
+  auto run = [&](int t) {
+    const int a0 = int(int64_t(n) * t / nt), a1 = int(int64_t(n) * (t + 1) / nt);
+    for (int a = a0; a < a1; ++a) body(active[size_t(a)], gsets[size_t(t)], asets[size_t(t)]);
+  };
+  std::vector<std::thread> th;
+  std::exception_ptr err;
+  std::mutex em;
+  for (int t = 1; t < nt; ++t)
+    th.emplace_back([&, t] {
+      try {
+        run(t);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(em);
+        err = std::current_exception();
+      }
+    });
+  try {
+    run(0);
+  } catch (...) {
+    std::lock_guard<std::mutex> lk(em);
+    err = std::current_exception();
+  }
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+  size_t nterms = 0, ntiles = 0, ngroups = 0, nsegs = 0, ngt = 0;
+  for (int t = 0; t < nt; ++t) {
+    nterms += gsets[size_t(t)].terms.size();
+    ntiles += gsets[size_t(t)].tiles.size();
+    ngroups += gsets[size_t(t)].groups.size();
+    nsegs += asets[size_t(t)].segs.size();
+    ngt += asets[size_t(t)].tiles.size();
+  }
+  gm.terms.reserve(gm.terms.size() + nterms);
+  gm.tiles.reserve(gm.tiles.size() + ntiles);
+  gm.groups.reserve(gm.groups.size() + ngroups);
+  ga.segs.reserve(ga.segs.size() + nsegs);
+  ga.tiles.reserve(ga.tiles.size() + ngt);
+  for (int t = 0; t < nt; ++t) {
+    GemmSet& g = gsets[size_t(t)];
+    const int32_t t0 = int32_t(gm.terms.size()), g0 = int32_t(gm.groups.size());
+    gm.terms.insert(gm.terms.end(), g.terms.begin(), g.terms.end());
+    for (Group gr : g.groups) gm.groups.push_back(Group{gr.t_begin + t0, gr.t_end + t0});
+    for (Tile tl : g.tiles) {
+      tl.g_begin += g0;
+      tl.g_end += g0;
+      gm.tiles.push_back(tl);
+    }
+    GatherSet& x = asets[size_t(t)];
+    const int32_t s0 = int32_t(ga.segs.size());
+    ga.segs.insert(ga.segs.end(), x.segs.begin(), x.segs.end());
+    for (GTile gt : x.tiles) {
+      gt.seg_begin += s0;
+      gt.seg_end += s0;
+      ga.tiles.push_back(gt);
+    }
+  }
+}
 
 struct hx_ctx {
   int device = 0;
@@ -1102,9 +1213,12 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     // implicit-route leaves: their terms clipped to the leaf; Z rows ordered by column range
     // (factor pairs first), W rows by row range, so that each gathered tile shares one range
     int64_t zmax = 0;
-    for (FarBlock& f : fb) {
+    std::vector<int> impl_idx;
+    for (int i = 0; i < int(fb.size()); ++i)
+      if (P->leaves[fb[size_t(i)].leaf].implicit) impl_idx.push_back(i);
+    par_for(int(impl_idx.size()), [&](int q) {
+      FarBlock& f = fb[size_t(impl_idx[size_t(q)])];
       const OutLeaf& L = P->leaves[f.leaf];
-      if (!L.implicit) continue;
       f.implicit = 1;
       for (int32_t g = L.g_begin; g < L.g_end; ++g) {
         const Group gr = P->mat_groups[g];
@@ -1142,6 +1256,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         r = (r + f.it[i].k + 1) & ~int64_t(1);
       }
       f.zrows = r;
+      f.zorder = o;
       std::stable_sort(o.begin(), o.end(), [&](int a, int b) {
         const ImplTerm &x = f.it[a], &y = f.it[b];
         if (x.lr != y.lr) return x.lr > y.lr;
@@ -1153,7 +1268,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         f.it[i].wrow = r;
         r = (r + f.it[i].k + 1) & ~int64_t(1);
       }
-    }
+      f.worder = o;
+    });
     (void)zmax;
     if (std::getenv("HX_IMPL_STATS")) {
       double full = 0, part = 0, part_area = 0, dd = 0, nl_impl = 0, full_terms = 0, part_terms = 0;
@@ -1296,6 +1412,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         return p;
       };
       auto woff = [&](const double* p) { return int64_t(p - wb); };
+      pm.mark("l-widths", s);
       // every work list of the round is known up front: one upload, then launches in order
       GemmSet gm;
       GatherSet ga;
@@ -1321,15 +1438,19 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         f.W = take(int64_t(l) * l);
         f.V = take(int64_t(l) * l);
         f.sig = take(l);
-        if (!f.implicit) continue;
+        if (f.implicit) matvecs += 2 * (l + PR);
+        else if (f.dense) matvecs += f.n;
+        else matvecs += 2 * l;
+      }
+      par_build(active, gm, ga, [&](int i, GemmSet& gm, GatherSet& ga) {
+        FarBlock& f = fb[i];
+        const int l = f.l;
+        if (!f.implicit) return;
         const OutLeaf& L = P->leaves[f.leaf];
         const int Lw = l + PR;
         std::vector<GSeg> run;
         int64_t have = 0;  // rows covered so far (pad segments fill the alignment gaps)
-        std::vector<int> o(f.it.size());
-        for (size_t q = 0; q < o.size(); ++q) o[q] = int(q);
-        std::sort(o.begin(), o.end(), [&](int a, int b) { return f.it[a].zrow < f.it[b].zrow; });
-        for (int q : o) {
+        for (int q : f.zorder) {  // ascending Z rows
           const ImplTerm& x = f.it[q];
           const Term& tm = x.t;
           const int64_t jo = L.col0 + x.ci - tm.c_lo;  // first leaf column, term-local
@@ -1349,21 +1470,28 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         }
         gather_rows(ga, run, BUF_CORE, f.zoff, int32_t(f.zrows), BUF_OMEGA, 0,
                     int32_t(c->omega_rows), Lw);
-        matvecs += 2 * Lw;
-      }
+      });
       gm.cut();  // gemm batch 0
       ga.cut();  // gather batch 0
+      pm.mark("l-b0", s);
       // -- batch 1: Y = T Omega (materialized) / Y = sum L_t Z_t (implicit)
       for (int i : active) {
+        const FarBlock& f = fb[i];
+        qy.push_back(QrJob{f.Y, f.R, f.m, f.dense ? f.n : f.l});
+      }
+      par_build(active, gm, ga, [&](int i, GemmSet& gm, GatherSet&) {
         FarBlock& f = fb[i];
         const int l = f.l;
         if (f.dense) {
-          matvecs += f.n;
+          return;
         } else if (f.implicit) {
           const OutLeaf& L = P->leaves[f.leaf];
           std::vector<Term> ts;
           std::vector<std::pair<int, int>> band;
-          for (const ImplTerm& x : f.it) {
+          ts.reserve(f.it.size() + 1);
+          band.reserve(f.it.size() + 1);
+          for (int q : f.worder) {  // (lr, row band): terms sharing a band are adjacent
+            const ImplTerm& x = f.it[size_t(q)];
             Term y = mk(x.t.a_buf, x.t.a_off, x.t.a_ld, x.t.a_kc, BUF_CORE, f.zoff + x.zrow,
                         int32_t(f.zrows), 1, x.k, x.t.rows, l + PR);
             y.r_lo = x.t.r_lo;
@@ -1377,17 +1505,16 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             ts.push_back(y);
             band.emplace_back(0, f.m);
           }
-          gm.cover_banded(ts, band, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0);
+          gm.cover_banded(ts, band, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0, true);
         } else {
           const Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
                             f.n, f.m, l);
           const int32_t g = gm.group(&y, 1);
           gm.cover(g, BUF_WORK, woff(f.Y), f.m, f.m, l, 0, 0);
-          matvecs += 2 * l;
         }
-        qy.push_back(QrJob{f.Y, f.R, f.m, f.dense ? f.n : l});
-      }
+      });
       gm.cut();  // gemm batch 1
+      pm.mark("l-b1", s);
       // -- batches 2, 3 (implicit): C1 = Q^T Y_probe; ||Y_probe - Q C1||^2 per tile
       for (int i : active) {
         FarBlock& f = fb[i];
@@ -1413,18 +1540,16 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         est_e.push_back(est_slots);
       }
       gm.cut();  // gemm batch 3
+      pm.mark("l-b23", s);
       // -- gather 1 + batch 4: W = L^T Q (implicit), rows sharing a row range
-      for (int i : active) {
+      par_build(active, gm, ga, [&](int i, GemmSet& gm, GatherSet& ga) {
         FarBlock& f = fb[i];
-        if (!f.implicit) continue;
+        if (!f.implicit) return;
         const OutLeaf& L = P->leaves[f.leaf];
         const int l = f.l;
         std::vector<GSeg> run;
         int64_t have = 0;  // rows covered so far (pad segments fill the alignment gaps)
-        std::vector<int> o(f.it.size());
-        for (size_t q = 0; q < o.size(); ++q) o[q] = int(q);
-        std::sort(o.begin(), o.end(), [&](int a, int b) { return f.it[a].wrow < f.it[b].wrow; });
-        for (int q : o) {
+        for (int q : f.worder) {  // ascending W rows
           const ImplTerm& x = f.it[q];
           const Term& tm = x.t;
           const int64_t io = L.row0 + x.ri - tm.r_lo;  // first leaf row, term-local
@@ -1443,19 +1568,27 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
           }
         }
         gather_rows(ga, run, BUF_CORE, f.zoff, int32_t(f.zrows), BUF_WORK, woff(f.Y), f.m, l);
-      }
+      });
       gm.cut();  // gemm batch 4
       ga.cut();  // gather batch 1
+      pm.mark("l-b4", s);
       // -- batch 5: Bt = T^T Q (materialized) / Bt = sum R_t W_t (implicit)
       for (int i : active) {
+        const FarBlock& f = fb[i];
+        if (!f.dense) qb.push_back(QrJob{f.Bt, f.R, f.n, f.l});
+      }
+      par_build(active, gm, ga, [&](int i, GemmSet& gm, GatherSet&) {
         FarBlock& f = fb[i];
-        if (f.dense) continue;
+        if (f.dense) return;
         const int l = f.l;
         if (f.implicit) {
           const OutLeaf& L = P->leaves[f.leaf];
           std::vector<Term> ts;
           std::vector<std::pair<int, int>> band;
-          for (const ImplTerm& x : f.it) {
+          ts.reserve(f.it.size() + 1);
+          band.reserve(f.it.size() + 1);
+          for (int q : f.zorder) {  // (lr, column band): terms sharing a band are adjacent
+            const ImplTerm& x = f.it[size_t(q)];
             // R_t(j, kk) = Q_t(kk, j)
             Term y = mk(x.t.b_buf, x.t.b_off, x.t.b_ld, uint8_t(x.t.b_kc ? 1 : 0), BUF_CORE,
                         f.zoff + x.wrow, int32_t(f.zrows), 1, x.k, x.t.cols, l);
@@ -1469,15 +1602,15 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             ts.push_back(y);
             band.emplace_back(0, f.n);
           }
-          gm.cover_banded(ts, band, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0);
+          gm.cover_banded(ts, band, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0, true);
         } else {
           const Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
           const int32_t g = gm.group(&y, 1);
           gm.cover(g, BUF_WORK, woff(f.Bt), f.n, f.n, l, 0, 0);
         }
-        qb.push_back(QrJob{f.Bt, f.R, f.n, l});
-      }
+      });
       gm.cut();  // gemm batch 5
+      pm.mark("l-b5", s);
       // -- batch 6: tight tolerances, materialized blocks: ||T||^2 - sum s_i^2 cancels below
       // ~1e-15 ||T||^2, so the unsampled tail is measured directly as ||T - Q Bt^T||_F^2
       for (int i : active) {
