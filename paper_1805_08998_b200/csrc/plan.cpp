@@ -30,6 +30,7 @@
 //   core  : V_l^T G (A side) / U_l^T G (B side) for the low-rank leaves l of X (stacked)
 //   fac   : row bands of X G / X^T G  (dense leaves D_l G, low-rank leaves U_l core_l)
 //   mat   : every output leaf materialized tile by tile from the terms of its root path
+#include <nvtx3/nvToolsExt.h>
 #include <omp.h>
 
 #include <algorithm>
@@ -1202,6 +1203,10 @@ struct Builder {
 
 extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,
                               const uint8_t* leaf_mask, int tile, int flags, hx_plan** out) {
+  struct Range {  // NVTX range over the planning (no-op without a tool attached)
+    Range() { nvtxRangePushA("hx::plan"); }
+    ~Range() { nvtxRangePop(); }
+  } range;
   return hx::guarded([&]() -> int {
     if (!tree || !a || !b || !out) return hx::fail(HX_EINVAL, "null argument");
     if (tile != 32 && tile != 64) return hx::fail(HX_EINVAL, "tile must be 32 or 64");

@@ -13,6 +13,7 @@
 
 #include <chrono>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cmath>
@@ -1009,6 +1010,19 @@ extern "C" int hx_ctx_operand_alias(hx_ctx* c) {
   return HX_OK;
 }
 
+// NVTX ranges over the product phases (visible in Nsight timelines; no-ops without a tool)
+struct NvtxPhases {
+  bool open = false;
+  void next(const char* name) {
+    if (open) nvtxRangePop();
+    nvtxRangePushA(name);
+    open = true;
+  }
+  ~NvtxPhases() {
+    if (open) nvtxRangePop();
+  }
+};
+
 // HX_RECOMP_TIMING: synchronizing wall-clock marks through the recompression phase (a
 // diagnostic: it serializes host list building and device work)
 struct PhaseMarks {
@@ -1040,6 +1054,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     if (!c->buf(BUF_A) || !c->buf(BUF_B)) return fail(HX_EINVAL, "operands not set");
     CK(cudaSetDevice(c->device));
     const int over = cfg->oversample > 0 ? cfg->oversample : 6;
+    NvtxPhases nvtx;
+    nvtx.next("hx::setup");
     c->launches = 0;
     {
       const double key[4] = {double(cfg->policy), cfg->eps, double(cfg->k_max), double(cfg->tag)};
@@ -1099,6 +1115,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     BufPtrs bp = c->ptrs();
     CK(cudaEventRecord(c->ev[5], s));
 
+    nvtx.next("hx::form");
     // ---- 1. term formation: gather thin factors per X-group, cores, X G products.
     // Deferred plans fill each batch's work lists here, on the host, while the device
     // runs the previous batch.
@@ -1146,6 +1163,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaStreamWaitEvent(s, c->ev[6], 0));
     }
     CK(cudaEventRecord(c->ev[1], s));
+    nvtx.next("hx::materialize");
     // ---- 2. materialization
     CK(cudaStreamWaitEvent(s, c->ev[7], 0));
     launch_gemm(c, P->tile, c->tiles[2].p, c->groups[2].p, c->terms[2].p,
@@ -1169,6 +1187,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->launches++;
     }
 
+    nvtx.next("hx::recompress");
     // ---- 3. recompression of far leaves, on the high-priority stream
     const cudaStream_t s_main = s;
     CK(cudaEventRecord(c->ev[6], s));
@@ -1750,6 +1769,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       if (f.round > 0) c->class_retry[ilog2(f.mu)] = 1;
     }
 
+    nvtx.next("hx::output");
     // ---- 4. output factors
     const int nf = int(fb.size());
     c->res_rank.assign(nl, -1);

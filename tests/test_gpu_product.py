@@ -346,3 +346,34 @@ def test_edge_sizes_and_zero_operand(n, n_min):
     CZ = hx.hmult_new(Z, Z, cfg)
     assert not np.any(hx.to_dense(CZ))
     assert all(q.rank == 0 for q in CZ.data.values() if hasattr(q, "left"))
+
+
+def test_negative_control_corrupted_block_is_detected():
+    """The verification's negative control (reference cli.run_verify(corrupt=True) scales
+    one far factor by 1.01, cli.py:197-203): the exact check and the GPU estimator both
+    pass on the product and both flag the corrupted one."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200.matvec import product_error
+
+    rng = np.random.default_rng(11)
+    pts = rng.uniform(0, 1, (1024, 2))
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, 32), 0.8)
+    A = hx.assemble_hmatrix("exp", bct, hx.EpsRank(1e-8), pts, device=0)
+    tol = 1e-6
+    C = hx.hmult_new(A, A, hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"),
+                                             policy=hx.EpsRank(tol)))
+    dense = hx.to_dense(A)
+    exact = dense @ dense
+    nrm = np.linalg.norm(exact)
+    assert np.linalg.norm(hx.to_dense(C) - exact) / nrm <= tol
+    est0, _ = product_error(C, A, A, probes=16)
+    assert est0 <= 2 * tol
+    far = [(b, p) for b, p in C.data.items() if hasattr(p, "left") and p.rank > 0]
+    b, p = max(far, key=lambda bp: np.linalg.norm(bp[1].to_dense()))
+    data = dict(C.data.items())
+    data[b] = hx.LowRank(p.left * 1.01, p.right)
+    bad = hx.HMatrix(bct, data)
+    err1 = np.linalg.norm(hx.to_dense(bad) - exact) / nrm
+    assert err1 > 10 * tol
+    est1, _ = product_error(bad, A, A, probes=16)
+    assert est1 > 10 * tol
