@@ -352,6 +352,7 @@ struct GatherSet {
 // fewer cores than std::thread::hardware_concurrency reports)
 int host_threads() {
   static const int n = [] {
+    if (const char* e = std::getenv("HX_LIST_THREADS")) return std::max(1, std::atoi(e));
     cpu_set_t set;
     CPU_ZERO(&set);
     if (sched_getaffinity(0, sizeof(set), &set) == 0) return std::max(1, int(CPU_COUNT(&set)));

@@ -16,6 +16,11 @@ def main():
     bct, A, B = configs.build_operands(c)
     cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(c["tol"]))
     walls = []
+    import gc
+    import os
+    if os.environ.get("NO_GC"):
+        gc.collect()
+        gc.disable()
     for _ in range(steps):
         C = multiply.multiply_device(A, B, cfg, fetch=False)
         walls.append(C.report.wall_s * 1e3)
