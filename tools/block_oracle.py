@@ -1,0 +1,95 @@
+"""Per-block oracle check of a large BASELINE config ("Cfg3-5: per-block oracle").
+
+The GPU product runs on the full config; for a stratified sample of output leaves (every
+far size class up to --max-size, the largest included, plus some near leaves) the oracle
+restatement rebuilds S(leaf) along its root-to-leaf chain (``leaf_expr``, the reference's
+sumexpr_root + restrict, sumexpr.py:78-154), densifies it and takes its best approximation
+at the tolerance (dense-svd semantics, compressors.py:431-438 with select_rank,
+lowrank.py:75-90).  Contract per block: rank within +-1, relative difference <= 10 tol;
+near blocks exact to 1e-12.
+
+usage: python tools/block_oracle.py CFG [--per-class 8] [--max-size 4096] [--near 8]
+"""
+import argparse
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_1805_08998_b200 as hx  # noqa: E402
+from oracle import hmat_oracle as O  # noqa: E402
+from paper_1805_08998_b200 import configs  # noqa: E402
+
+
+def oracle_operand(H, obt):
+    data = {}
+    for b, p in H.data.items():
+        data[b] = O.LR(np.ascontiguousarray(p.left), np.ascontiguousarray(p.right)) \
+            if hasattr(p, "left") else np.ascontiguousarray(p)
+    return O.HMatO(obt, data, H.degraded)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("cfg", type=int)
+    ap.add_argument("--per-class", type=int, default=8)
+    ap.add_argument("--max-size", type=int, default=4096)
+    ap.add_argument("--near", type=int, default=8)
+    ap.add_argument("--seed", type=int, default=1)
+    a = ap.parse_args()
+    c = configs.CONFIGS[a.cfg]
+    tol = c["tol"]
+    t0 = time.time()
+    bct, A, B = configs.build_operands(c)
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    C = hx.hmult_new(A, B, cfg)
+    print(f"cfg{a.cfg}: GPU product {C.report.wall_s:.1f} s (setup {time.time() - t0:.1f} s)",
+          flush=True)
+    pts = configs.make_points(c)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, c["n_min"]), c["eta"])
+    oa = oracle_operand(A, obt)
+    ob = oa if B is A else oracle_operand(B, obt)
+    rng = np.random.default_rng(a.seed)
+    lo, hi = bct.tree.lo, bct.tree.hi
+    size = (hi[bct.tau] - lo[bct.tau])
+    far = np.flatnonzero(bct.kind_code == 1)
+    near = np.flatnonzero(bct.kind_code == 2)
+    sample = []
+    for m in np.unique(size[far]):
+        if m > a.max_size:
+            continue
+        ids = far[size[far] == m]
+        pick = rng.choice(ids, size=min(a.per_class, len(ids)), replace=False)
+        sample += [int(b) for b in pick]
+    sample += [int(b) for b in rng.choice(near, size=min(a.near, len(near)), replace=False)]
+    worst_rank, worst_far, worst_near = 0, 0.0, 0.0
+    t1 = time.time()
+    for b in sample:
+        s = O.leaf_expr(oa, ob, b)
+        m, n = s.shape
+        dense = s.mat(np.eye(n))
+        q = C.data[b]
+        if bct.kind_code[b] == 2:
+            d = np.linalg.norm(q - dense) / max(np.linalg.norm(dense), 1e-300)
+            worst_near = max(worst_near, d)
+            print(f"  near {b:8d} {m}x{n}: rel diff {d:.2e}", flush=True)
+            continue
+        u, sv, vt = np.linalg.svd(dense, full_matrices=False)
+        r = O.eps_rank(sv, O.Eps(tol))
+        best = (u[:, :r] * sv[:r]) @ vt[:r]
+        d = np.linalg.norm(q.to_dense() - best) / max(np.linalg.norm(best), 1e-300)
+        worst_rank = max(worst_rank, abs(q.rank - r))
+        worst_far = max(worst_far, d)
+        print(f"  far  {b:8d} {m}x{n}: rank gpu {q.rank} oracle {r}, rel diff {d:.2e}",
+              flush=True)
+    print(f"cfg{a.cfg}: {len(sample)} blocks checked in {time.time() - t1:.0f} s: worst rank "
+          f"difference {worst_rank}, worst far rel diff {worst_far:.2e} (10 tol = "
+          f"{10 * tol:.0e}), worst near rel diff {worst_near:.2e}", flush=True)
+    ok = worst_rank <= 1 and worst_far <= 10 * tol and worst_near <= 1e-12
+    print("PASS" if ok else "FAIL", flush=True)
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())
