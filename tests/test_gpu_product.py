@@ -377,3 +377,41 @@ def test_negative_control_corrupted_block_is_detected():
     assert err1 > 10 * tol
     est1, _ = product_error(bad, A, A, probes=16)
     assert est1 > 10 * tol
+
+
+def test_block_oracle_large_tree():
+    """Per-block oracle at a size where the implicit route (far leaves >= 512) and TSQR
+    (sketch panels > 512 rows) run: n = 16384 points in [0,1]^2, GPU-assembled exp(-r)
+    operand, tol 1e-6; sampled far leaves of every size class and some near leaves are
+    rebuilt by the oracle along their root chains (rank +-1, <= 10 tol; near exact)."""
+    import paper_1805_08998_b200 as hx
+
+    n, n_min, eta, tol = 16384, 64, 0.8, 1e-6
+    rng = np.random.default_rng(21)
+    pts = rng.uniform(0, 1, (n, 2))
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, n_min), eta)
+    A = hx.assemble_hmatrix("exp", bct, hx.EpsRank(1e-8), pts, device=0)
+    C = hx.hmult_new(A, A, hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"),
+                                             policy=hx.EpsRank(tol)))
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, n_min), eta)
+    data = {b: (O.LR(np.ascontiguousarray(p.left), np.ascontiguousarray(p.right))
+                if hasattr(p, "left") else np.ascontiguousarray(p)) for b, p in A.data.items()}
+    oa = O.HMatO(obt, data)
+    size = bct.tree.hi[bct.tau] - bct.tree.lo[bct.tau]
+    far = np.flatnonzero(bct.kind_code == 1)
+    near = np.flatnonzero(bct.kind_code == 2)
+    assert size[far].max() >= 1024  # implicit route and TSQR are exercised
+    sample = [int(b) for m in np.unique(size[far]) for b in far[size[far] == m][:3]]
+    sample += [int(b) for b in near[:3]]
+    for b in sample:
+        s = O.leaf_expr(oa, oa, b)
+        dense = s.mat(np.eye(s.shape[1]))
+        q = C.data[b]
+        if bct.kind_code[b] == 2:
+            assert np.linalg.norm(q - dense) <= 1e-12 * np.linalg.norm(dense)
+            continue
+        u, sv, vt = np.linalg.svd(dense, full_matrices=False)
+        r = O.eps_rank(sv, O.Eps(tol))
+        best = (u[:, :r] * sv[:r]) @ vt[:r]
+        assert abs(q.rank - r) <= 1, (b, q.rank, r)
+        assert np.linalg.norm(q.to_dense() - best) <= 10 * tol * np.linalg.norm(best), b

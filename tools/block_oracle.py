@@ -23,10 +23,10 @@ from paper_1805_08998_b200 import configs  # noqa: E402
 
 
 def oracle_operand(H, obt):
+    # views into the downloaded pool, no copies (config 5's operands are ~60 GB)
     data = {}
     for b, p in H.data.items():
-        data[b] = O.LR(np.ascontiguousarray(p.left), np.ascontiguousarray(p.right)) \
-            if hasattr(p, "left") else np.ascontiguousarray(p)
+        data[b] = O.LR(p.left, p.right) if hasattr(p, "left") else p
     return O.HMatO(obt, data, H.degraded)
 
 
