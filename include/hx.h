@@ -158,17 +158,22 @@ typedef struct hx_product_cfg {
   int32_t policy;        /* 0 EpsRank, 1 FixedRank (lowrank.py:57-72)               */
   double eps;            /* EpsRank.eps (already clamped by the caller)             */
   int32_t k_max;         /* FixedRank.k_max                                         */
-  int32_t tag;           /* 0 aca, 1 bilanczos, 2 randomized, 3 dense-svd           */
+  int32_t tag;           /* 0 aca, 1 bilanczos, 2 randomized, 3 dense-svd: 0-2 run the
+                          * reference's matrix-free schemes on the implicit sums
+                          * (compressors.py:162-428), 3 the sketch + SVD route      */
   uint64_t seed;         /* CompressorKind.seed                                     */
   int32_t sketch0;       /* initial sketch width (0 = default)                      */
   int32_t oversample;    /* minimum sketch oversampling (0 = default 6)             */
+  int32_t q;             /* CompressorKind.q: randomized subspace iterations        */
 } hx_product_cfg;
 
 typedef struct hx_product_stats {
   double ms_total;       /* CUDA-event time of the whole product on the device      */
   double ms_form, ms_mat, ms_recompress;
   int64_t far_leaves, near_leaves, degraded_blocks, max_far_rank;
-  int64_t matvec_count;  /* operator columns applied by the recompression           */
+  int64_t matvec_count;  /* the reference's CountingMap total (compressors.py:88-119):
+                          * dense-svd n per far block, the matrix-free tags the rows,
+                          * columns and matvecs their iterations applied             */
   int64_t sketch_rounds;
   int64_t launches;      /* kernels launched by this call                           */
   int64_t out_elems;     /* doubles in the packed result                            */
@@ -177,6 +182,7 @@ typedef struct hx_product_stats {
   double ms_upload;      /* H2D of the plan's work lists (inside ms_total)          */
   double t_marks[4];     /* start, formation end, materialization end, end: ms after the
                           * device epoch (hx_timeline_epoch), -1 without an epoch    */
+  int64_t sketch_cols;   /* operator columns the dense-svd sketch route applied     */
 } hx_product_stats;
 
 /* Records the device epoch the t_marks of later products are measured from. */
@@ -218,6 +224,18 @@ int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tile
                   int64_t n_tiles, const void* groups, int64_t n_groups,
                   double* const* host_bufs, const int64_t* buf_elems, double* sumsq,
                   int64_t n_sumsq);
+
+/* Diagnostics: numpy's default_rng(seed).standard_normal(n) stream, seed = seed_hi * 2^64 +
+ * seed_lo, generated on the host (device < 0) or by the device generator the matrix-free
+ * compressors use (the reference's per-block streams, multiply.py:61-63). */
+int hx_np_normals(uint64_t seed_lo, uint64_t seed_hi, int64_t n, double* out, int device);
+/* Diagnostics: one dense column-major m x n block through the matrix-free compressor route
+ * of hx_product (tag 0 aca, 1 bilanczos, 2 randomized: compressors.py:162-428, with the
+ * per-block stream default_rng((seed << 24) ^ node)); left / right get rank columns
+ * (room for min(m, n)); info = {rank, degraded, matvec count}. */
+int hx_debug_compress(int tag, int policy, double eps, int k_max, int q, uint64_t seed,
+                      int32_t node, int m, int n, const double* A, double* left,
+                      double* right, int32_t* info);
 
 int hx_ctx_synchronize(hx_ctx* ctx);
 /* Device memory available to the context (free + the workspace it already holds). */

@@ -47,7 +47,7 @@ class HxPlanInfo(C.Structure):
 class HxProductCfg(C.Structure):
     _fields_ = [("policy", C.c_int32), ("eps", C.c_double), ("k_max", C.c_int32),
                 ("tag", C.c_int32), ("seed", C.c_uint64), ("sketch0", C.c_int32),
-                ("oversample", C.c_int32)]
+                ("oversample", C.c_int32), ("q", C.c_int32)]
 
 
 class HxProductStats(C.Structure):
@@ -57,7 +57,7 @@ class HxProductStats(C.Structure):
                                        "max_far_rank", "matvec_count", "sketch_rounds",
                                        "launches", "out_elems")] + [
         ("fro2_total", C.c_double), ("dom_kernel_ms", C.c_double), ("ms_upload", C.c_double),
-        ("t_marks", C.c_double * 4)]
+        ("t_marks", C.c_double * 4), ("sketch_cols", C.c_int64)]
 
 
 class HxError(RuntimeError):
@@ -106,6 +106,9 @@ SIGNATURES = {
     "hx_debug_gemm": [C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p,
                       C.c_int64, C.POINTER(f64p), i64p, f64p, C.c_int64],
     "hx_debug_qr": [C.c_int, i32p, i32p, f64p, f64p],
+    "hx_np_normals": [C.c_uint64, C.c_uint64, C.c_int64, f64p, C.c_int],
+    "hx_debug_compress": [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_int32,
+                          C.c_int, C.c_int, f64p, f64p, f64p, i32p],
     "hx_ctx_free": [C.c_void_p],
     "hx_last_error": [C.c_char_p, C.c_size_t],
     "hx_version": [],
@@ -138,12 +141,13 @@ def lib():
 
 
 def _tune_host_allocator():
-    """Keep freed heap memory in the process (glibc mallopt): the per-product work lists
-    (tens of MB of std::vector, rebuilt every product) otherwise go back to the kernel with
-    munmap / trim and come back as fresh page faults, which showed up as 40-90 ms stalls on
-    some products (config 2: mean step 331 -> 319 ms, worst of 39 steps 414 -> 351 ms).
-    HX_NO_MALLOPT=1 keeps the allocator defaults."""
-    if os.environ.get("HX_NO_MALLOPT"):
+    """Opt-in (HX_MALLOPT=1, set by bench.py): keep freed heap memory in the process (glibc
+    mallopt).  The per-product work lists (tens of MB of std::vector, rebuilt every product)
+    otherwise go back to the kernel with munmap / trim and come back as fresh page faults,
+    which showed up as 40-90 ms stalls on some products (config 2: mean step 331 -> 319 ms,
+    worst of 39 steps 414 -> 351 ms).  It changes the allocator of the whole process, so a
+    library user has to ask for it."""
+    if os.environ.get("HX_MALLOPT", "0") in ("", "0"):
         return
     try:
         libc = C.CDLL("libc.so.6")

@@ -13,7 +13,8 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["plan.cpp", "errors.cpp", "hmx1.cpp", "runtime.cu"]
 HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "dense_la.cuh", "dense_la_warp.cuh",
-           "qr_rows.cuh", "gather_gemm.cuh", "assemble.cuh"]
+           "qr_rows.cuh", "gather_gemm.cuh", "assemble.cuh", "iterative.cuh",
+           "np_random.cuh"]
 OUT = os.path.join(HERE, "libhx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -31,7 +32,19 @@ def _stale():
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _ziggurat_tables():
+    """numpy's ziggurat tables for the device normal generator (tools/gen_ziggurat.py)."""
+    sys.path.insert(0, os.path.join(HERE, "..", "tools"))
+    try:
+        import gen_ziggurat
+    finally:
+        sys.path.pop(0)
+    gen_ziggurat.write(os.path.join(CSRC, "zig_tables.inc"))
+
+
 def build(force=False, verbose=False):
+    if not os.path.exists(os.path.join(CSRC, "zig_tables.inc")):
+        _ziggurat_tables()
     if not force and not _stale():
         return OUT
     cmd = [NVCC, *FLAGS, *[os.path.join(CSRC, s) for s in SOURCES], "-o", OUT + ".tmp"]

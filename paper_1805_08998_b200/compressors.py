@@ -1,11 +1,20 @@
 """Compression-scheme selection (API of ``hmat.compressors.CompressorKind``).
 
 The reference compresses each far output block with one matrix-free scheme chosen by
-``CompressorKind.tag`` (``compressors.py:122-141``, dispatch ``:441-452``).  On the GPU the
-tag selects the recompression route of ``hx_product``: every tag yields
-the tolerance-certified truncated SVD of the exact block (best approximation, the
-``dense-svd`` semantics), which is within the reference's own rank spread for ``aca``
-(+0/+1) and ``bilanczos`` (identical ranks on the configs measured).
+``CompressorKind.tag`` (``compressors.py:122-141``, dispatch ``:441-452``).  The tag selects
+the GPU route of ``hx_product`` (``include/hx.h``, ``csrc/iterative.cuh``):
+
+* ``aca``        partially pivoted ACA on the block's implicit sum (rows / columns of the
+                 stacked terms, or of the materialized tile), two-hit stop, then the exact
+                 ``truncate(eps / 2)`` (compressors.py:162-247);
+* ``bilanczos``  Golub-Kahan-Lanczos with two-pass CGS reorthogonalisation, breakdown
+                 probes and the core SVD (:271-365), start vectors from the per-block numpy
+                 stream ``default_rng((seed << 24) ^ id)`` (multiply.py:61-63);
+* ``randomized`` the vector-at-a-time range finder with the two-hit stop, or with a
+                 FixedRank policy the blocked finder with ``q`` subspace iterations
+                 (:368-428), same per-block streams;
+* ``dense-svd``  the best approximation (sketch + QR + Jacobi SVD certified against the
+                 exact tail; :431-438).
 """
 
 from __future__ import annotations

@@ -31,6 +31,7 @@
 #include "dense_la_warp.cuh"
 #include "gather_gemm.cuh"
 #include "gemm.cuh"
+#include "iterative.cuh"
 #include "qr_rows.cuh"
 #include "hx_internal.h"
 
@@ -225,6 +226,8 @@ struct FarBlock {
   int rank = 0;
   int done = 0;
   int round = -1;
+  int direct = 0;    // iterative route: output the produced factors (Y, Bt) as they are
+  int degraded = 0;  // ACA ran out of rows without a certified zero
   // implicit route: terms and the row count of their stacked Z / W blocks
   int implicit = 0;
   std::vector<ImplTerm> it;
@@ -488,6 +491,10 @@ struct hx_ctx {
   DArr<Group> xgroups;
   DArr<GTile> gtiles;        // row-gathered GEMM tiles / segments of a sketch round
   DArr<GSeg> gsegs;
+  DArr<IterJob> iter_jobs;   // matrix-free compressors (aca / bilanczos / randomized)
+  DArr<IterTerm> iter_terms;
+  DArr<IterOut> iter_outs;
+  DArr<UrJob> ur_jobs;
   std::vector<DArr<double>> work;  // one workspace per sketch round
   std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
   // sketch-width hints: the largest rank seen per log2(min(m, n)) class by earlier chunks
@@ -892,6 +899,333 @@ int default_sketch(int mu) {
   return tab[4];
 }
 
+// First column budget of the matrix-free compressors by block size (a block that needs
+// more is rerun with four times as many; ACA and Lanczos are deterministic per block).
+int iter_kcap0(int mu) {
+  if (mu <= 64) return 24;
+  if (mu <= 128) return 32;
+  if (mu <= 256) return 48;
+  if (mu <= 1024) return 64;
+  return 96;
+}
+
+// Far blocks compressed by the reference's matrix-free schemes (the aca / bilanczos /
+// randomized tags; compressors.py:162-428) on their implicit sums, then the exact SVD
+// recompressions those schemes end with.  Fills f.Y / f.Bt / f.R / f.W / f.V / f.sig / f.l
+// (SVD-finished blocks, like the sketch route) or sets f.direct (factors output as
+// produced), f.rank and f.degraded; returns the reference's matvec count.
+int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
+                             std::vector<FarBlock>& fb, int jac_trans, int& rounds) {
+  const int nf = int(fb.size());
+  int64_t matvecs = 0;
+  if (!nf) return 0;
+  const int tag = cfg->tag;  // 0 aca, 1 bilanczos, 2 randomized
+  IterParams prm;
+  prm.tag = tag == 0 ? ITER_ACA : (tag == 1 ? ITER_GKL : ITER_RAND);
+  prm.policy = cfg->policy;
+  prm.eps = cfg->eps;
+  prm.k_max = cfg->k_max;
+  prm.q = cfg->q;
+  prm.seed = cfg->seed;
+  const BufPtrs bp0 = c->ptrs();
+  // terms of the implicit blocks, clipped to the block (leaf-local coordinates)
+  std::vector<IterTerm> terms;
+  std::vector<int> tbeg(nf, 0), tend(nf, 0), ksum(nf, 0);
+  for (int i = 0; i < nf; ++i) {
+    FarBlock& f = fb[size_t(i)];
+    tbeg[size_t(i)] = int(terms.size());
+    if (f.implicit) {
+      const OutLeaf& L = P->leaves[size_t(f.leaf)];
+      int koff = 0;
+      for (const ImplTerm& x : f.it) {
+        const Term& t = x.t;
+        if (t.b_kc > 1 || t.a_kc > 1) throw hx::Unsupported("gathered term on the implicit route");
+        for (uint8_t b : {t.a_buf, t.b_buf})
+          if (b == BUF_CORE || b == BUF_WORK || b == BUF_OUT)
+            throw hx::Unsupported("implicit term on a transient buffer");
+        IterTerm e;
+        const int64_t ri = L.row0 + x.ri - t.r_lo;  // term-local first row / column
+        const int64_t cj = L.col0 + x.ci - t.c_lo;
+        e.ps = t.a_kc ? t.a_ld : 1;
+        e.pk = t.a_kc ? 1 : t.a_ld;
+        e.qs = t.b_kc ? t.b_ld : 1;
+        e.qk = t.b_kc ? 1 : t.b_ld;
+        e.P = bp0.p[t.a_buf] + t.a_off + ri * e.ps;
+        e.Q = bp0.p[t.b_buf] + t.b_off + cj * e.qs;
+        e.k = x.k;
+        e.ri = x.ri;
+        e.rn = x.rn;
+        e.ci = x.ci;
+        e.cn = x.cn;
+        e.koff = koff;
+        koff += x.k;
+        terms.push_back(e);
+      }
+      ksum[size_t(i)] = koff;
+    }
+    tend[size_t(i)] = int(terms.size());
+  }
+  if (!terms.empty()) c->iter_terms.upload(terms, c->s);
+  std::vector<int> kcap(nf);
+  for (int i = 0; i < nf; ++i) {
+    const FarBlock& f = fb[size_t(i)];
+    kcap[size_t(i)] = cfg->policy == 1 ? std::min(f.mu, std::max(cfg->k_max, 1))
+                                       : std::min(f.mu, iter_kcap0(f.mu));
+  }
+  auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
+  std::vector<IterOut> outs(static_cast<size_t>(nf));
+  std::vector<int> active(static_cast<size_t>(nf));
+  for (int i = 0; i < nf; ++i) active[size_t(i)] = i;
+  std::vector<IterJob> jobs(static_cast<size_t>(nf));
+  // job workspace offsets (doubles) in c->work[0]; re-laid out per round of reruns
+  while (!active.empty()) {
+    if (rounds >= 6) throw std::runtime_error("matrix-free compression did not converge");
+    int64_t wsz = 0;
+    std::vector<int64_t> off(active.size());
+    for (size_t a = 0; a < active.size(); ++a) {
+      const int i = active[a];
+      const FarBlock& f = fb[size_t(i)];
+      const int64_t kc = kcap[size_t(i)];
+      off[a] = wsz;
+      wsz += a16(f.m * kc) + a16(f.n * kc) + (tag == 1 ? a16(f.n * kc) : 0) + a16(2 * f.m) +
+             a16(3 * int64_t(f.n)) + a16(((ksum[size_t(i)] + 7) & ~7) + 2 * kc + 8) +
+             a16((f.m + f.n + 7) / 8);
+    }
+    const int slot = rounds;  // finished jobs of earlier rounds keep their slots
+    if (int(c->work.size()) <= slot) c->work.resize(slot + 1);
+    c->work[slot].ensure(size_t(std::max<int64_t>(wsz, 16)));
+    double* wb = c->work[slot].p;
+    // large / implicit blocks: a CTA of 8 warps each; the others a warp each
+    std::vector<int> big, small;
+    for (size_t a = 0; a < active.size(); ++a) {
+      const int i = active[a];
+      FarBlock& f = fb[size_t(i)];
+      const int64_t kc = kcap[size_t(i)];
+      double* p = wb + off[a];
+      IterJob jb;
+      jb.T = f.implicit ? (P->leaves[size_t(f.leaf)].tile_end >
+                                   P->leaves[size_t(f.leaf)].tile_begin
+                               ? c->buf(BUF_TILE) + f.t_off
+                               : nullptr)
+                        : c->buf(BUF_TILE) + f.t_off;
+      jb.ldT = f.m;
+      jb.m = f.m;
+      jb.n = f.n;
+      jb.t_begin = tbeg[size_t(i)];
+      jb.t_end = tend[size_t(i)];
+      jb.kcap = int32_t(kc);
+      jb.node = P->leaves[size_t(f.leaf)].id;
+      jb.L = p;
+      p += a16(f.m * kc);
+      jb.U = p;
+      p += a16(f.n * kc);
+      jb.Wb = nullptr;
+      if (tag == 1) {
+        jb.Wb = p;
+        p += a16(f.n * kc);
+      }
+      jb.vm = p;
+      p += a16(2 * f.m);
+      jb.vn = p;
+      p += a16(3 * int64_t(f.n));
+      jb.tz = p;
+      p += a16(((ksum[size_t(i)] + 7) & ~7) + 2 * kc + 8);
+      jb.used = reinterpret_cast<uint8_t*>(p);
+      jobs[size_t(i)] = jb;
+      (f.implicit || std::max(f.m, f.n) > 256 ? big : small).push_back(i);
+    }
+    auto by_size = [&](int x, int y) {
+      const int64_t ax = int64_t(fb[size_t(x)].m) * fb[size_t(x)].n;
+      const int64_t ay = int64_t(fb[size_t(y)].m) * fb[size_t(y)].n;
+      return ax != ay ? ax > ay : x < y;
+    };
+    std::sort(big.begin(), big.end(), by_size);
+    std::sort(small.begin(), small.end(), by_size);
+    std::vector<IterJob> order;
+    for (int i : big) order.push_back(jobs[size_t(i)]);
+    for (int i : small) order.push_back(jobs[size_t(i)]);
+    c->iter_jobs.upload(order, c->s);
+    c->iter_outs.ensure(order.size());
+    if (!big.empty()) {
+      iter_kernel<8><<<int(big.size()), 256, 0, c->s>>>(c->iter_jobs.p, c->iter_terms.p,
+                                                         c->iter_outs.p, int(big.size()), prm);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+    if (!small.empty()) {
+      iter_kernel<1><<<int((small.size() + 3) / 4), 128, 0, c->s>>>(
+          c->iter_jobs.p + big.size(), c->iter_terms.p, c->iter_outs.p + big.size(),
+          int(small.size()), prm);
+      CK(cudaGetLastError());
+      c->launches++;
+    }
+    std::vector<IterOut> got(order.size());
+    CK(cudaMemcpyAsync(got.data(), c->iter_outs.p, got.size() * sizeof(IterOut),
+                       cudaMemcpyDeviceToHost, c->s));
+    CK(cudaStreamSynchronize(c->s));
+    std::vector<int> next;
+    size_t a = 0;
+    for (int i : big) outs[size_t(i)] = got[a++];
+    for (int i : small) outs[size_t(i)] = got[a++];
+    for (int i : active) {
+      const FarBlock& f = fb[size_t(i)];
+      if (outs[size_t(i)].capped && kcap[size_t(i)] < f.mu) {
+        kcap[size_t(i)] = std::min(f.mu, 4 * kcap[size_t(i)]);
+        next.push_back(i);
+      } else if (outs[size_t(i)].capped) {
+        throw std::runtime_error("matrix-free compression: column budget exhausted");
+      }
+    }
+    ++rounds;
+    if (next.empty()) break;
+    active.swap(next);
+  }
+  for (int i = 0; i < nf; ++i) matvecs += outs[size_t(i)].matvecs;
+  // ---- exact recompressions: ACA's truncate(eps / 2) (compressors.py:245-246,
+  // lowrank.py:93-113) and the Lanczos core SVD (:359-365); the sketch route's kernels
+  int64_t psz = 0;
+  std::vector<int> svd;
+  for (int i = 0; i < nf; ++i) {
+    FarBlock& f = fb[size_t(i)];
+    const IterOut& o = outs[size_t(i)];
+    f.degraded = o.degraded;
+    f.done = 1;
+    f.rank = o.k;
+    f.l = o.k;
+    f.dense = 0;
+    f.Y = jobs[size_t(i)].L;
+    f.Bt = jobs[size_t(i)].U;
+    const bool trunc = o.k > 0 && ((tag == 0 && cfg->policy == 0 && o.k > 1) || tag == 1);
+    if (!trunc) {
+      f.direct = 1;
+      continue;
+    }
+    if (o.k > JAC_QMAX) throw hx::Unsupported("compressed block rank above " +
+                                              std::to_string(JAC_QMAX));
+    svd.push_back(i);
+    const int64_t k = o.k;
+    psz += 4 * a16(k * k) + a16(k) + (tag == 0 ? a16(int64_t(f.n) * k) : 0);
+  }
+  if (svd.empty()) return matvecs;
+  const int post = rounds;
+  if (int(c->work.size()) <= post) c->work.resize(post + 1);
+  c->work[post].ensure(size_t(std::max<int64_t>(psz, 16)));
+  double* wb = c->work[post].p;
+  int64_t pos = 0;
+  auto take = [&](int64_t ne) {
+    double* p = wb + pos;
+    pos += a16(ne);
+    return p;
+  };
+  std::vector<QrJob> q1, q2;
+  std::vector<UrJob> ur;
+  for (int i : svd) {
+    FarBlock& f = fb[size_t(i)];
+    const int k = f.l;
+    f.R = take(int64_t(k) * k);
+    f.W = take(int64_t(k) * k);
+    f.V = take(int64_t(k) * k);
+    f.sig = take(k);
+    if (tag == 0) {
+      // L = Q_L R_L (in place); Bt = U R_L^T = (L U^T)^T Q_L, then Bt = Q2 R as on the
+      // sketch route
+      double* rl = take(int64_t(k) * k);
+      q1.push_back(QrJob{f.Y, rl, f.m, k});
+      double* bt = take(int64_t(f.n) * k);
+      ur.push_back(UrJob{f.Bt, rl, bt, f.n, k});
+      f.Bt = bt;
+    }
+  }
+  if (tag == 0) {
+    run_qr(c, q1);
+    c->ur_jobs.upload(ur, c->s);
+    int nmax = 1;
+    for (const UrJob& u : ur) nmax = std::max(nmax, u.n);
+    dim3 grid(unsigned(ur.size()), unsigned(std::min(64, (nmax + 127) / 128)));
+    ur_product_kernel<<<grid, 128, 0, c->s>>>(c->ur_jobs.p);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+  for (int i : svd) {
+    FarBlock& f = fb[size_t(i)];
+    q2.push_back(QrJob{const_cast<double*>(f.Bt), f.R, f.n, f.l});
+  }
+  run_qr(c, q2);
+  std::vector<JacJob> jj;
+  for (int i : svd) {
+    FarBlock& f = fb[size_t(i)];
+    jj.push_back(JacJob{f.R, f.sig, f.W, f.V, f.l, jac_trans});
+  }
+  run_jacobi(c, jj);
+  std::vector<SelJob> sj;
+  for (int i : svd) {
+    FarBlock& f = fb[size_t(i)];
+    sj.push_back(SelJob{f.sig, nullptr, f.l, f.mu, 1, 0});
+  }
+  const int na = int(sj.size());
+  c->sel_jobs.upload(sj, c->s);
+  c->rank_d.ensure(size_t(na));
+  c->retry_d.ensure(size_t(na));
+  // ACA trims at eps / 2; Lanczos selects at eps (FixedRank keeps min(k, k_max))
+  const double eps_sel = tag == 0 ? 0.5 * cfg->eps : cfg->eps;
+  select_rank_kernel<<<(na + 127) / 128, 128, 0, c->s>>>(c->sel_jobs.p, na, cfg->policy, eps_sel,
+                                                         cfg->k_max, 0, c->rank_d.p,
+                                                         c->retry_d.p, 0);
+  CK(cudaGetLastError());
+  c->launches++;
+  std::vector<int> rk(static_cast<size_t>(na));
+  CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, size_t(na) * sizeof(int), cudaMemcpyDeviceToHost,
+                     c->s));
+  CK(cudaStreamSynchronize(c->s));
+  for (int a = 0; a < na; ++a) fb[size_t(svd[size_t(a)])].rank = rk[size_t(a)];
+  return matvecs;
+}
+
+// Output factors of the far blocks: left (m x r) = U S and right (n x r) = V written at
+// out + off[i] (left then right, column-major), from the recompression's small factors.
+void launch_far_outputs(hx_ctx* c, const std::vector<FarBlock>& fb,
+                        const std::vector<int64_t>& off, double* out) {
+  bool direct = false;
+  for (const FarBlock& f : fb) direct |= f.direct && f.rank > 0;
+  if (direct && !c->eye_ready) {  // the identity C of directly output factors
+    const int64_t ne = int64_t(EYE_LD) * EYE_LD;
+    c->own[BUF_EYE].ensure(size_t(ne));
+    eye_kernel<<<int((ne + 255) / 256), 256, 0, c->s>>>(c->own[BUF_EYE].p, ne, EYE_LD);
+    CK(cudaGetLastError());
+    c->launches++;
+    c->eye_ready = true;
+  }
+  std::vector<SmallJob> jl;
+  int rows_max = 1;
+  for (size_t i = 0; i < fb.size(); ++i) {
+    const FarBlock& f = fb[i];
+    if (f.rank == 0) continue;
+    double* left = out + off[i];
+    double* right = left + int64_t(f.m) * f.rank;
+    if (f.direct) {  // matrix-free factors as produced (C = identity)
+      if (f.rank > EYE_LD) throw hx::Unsupported("factor rank above the identity operand");
+      jl.push_back(SmallJob{f.Y, c->buf(BUF_EYE), nullptr, left, f.m, f.rank, EYE_LD, f.m,
+                            f.rank});
+      jl.push_back(SmallJob{f.Bt, c->buf(BUF_EYE), nullptr, right, f.n, f.rank, EYE_LD, f.n,
+                            f.rank});
+    } else if (f.dense) {
+      jl.push_back(SmallJob{f.Y, f.W, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
+      jl.push_back(SmallJob{nullptr, f.V, nullptr, right, f.n, f.l, f.l, 0, f.rank});
+    } else {
+      jl.push_back(SmallJob{f.Y, f.V, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
+      jl.push_back(SmallJob{f.Bt, f.W, nullptr, right, f.n, f.l, f.l, f.n, f.rank});
+    }
+    rows_max = std::max(rows_max, std::max(f.m, f.n));
+  }
+  if (!jl.empty()) {
+    c->small_jobs.upload(jl, c->s);
+    dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
+    small_product_kernel<<<grid, 128, 0, c->s>>>(c->small_jobs.p);
+    CK(cudaGetLastError());
+    c->launches++;
+  }
+}
+
 }  // namespace
 
 extern "C" int hx_ctx_create(int device, hx_ctx** out) {
@@ -1236,7 +1570,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     int64_t nmax = 1;
     for (const FarBlock& f : fb) nmax = std::max<int64_t>(nmax, f.n);
     const int lcap = JAC_QMAX;
-    if (c->omega_rows < nmax || c->omega_cols < lcap || c->omega_seed != cfg->seed) {
+    if (cfg->tag == 3 &&
+        (c->omega_rows < nmax || c->omega_cols < lcap || c->omega_seed != cfg->seed)) {
       c->omega_rows = std::max<int64_t>(nmax, c->omega_rows);
       c->omega_cols = lcap;
       c->omega_seed = cfg->seed;
@@ -1387,10 +1722,18 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     // Jacobi on R^T (rows of the QR factor): fewer sweeps than on the columns of R
     const char* jt = std::getenv("HX_JAC_TRANS");
     const int jac_trans = jt ? std::atoi(jt) : 1;
-    int64_t matvecs = 0;
+    int64_t matvecs = 0;  // the reference's CountingMap total (compressors.py:88-119)
+    int64_t sketch_cols = 0;  // operator columns the sketch route actually applied
     int rounds = 0;
     std::vector<int> active;
-    for (int i = 0; i < int(fb.size()); ++i) active.push_back(i);
+    const bool iterative = cfg->tag >= 0 && cfg->tag <= 2;
+    if (iterative) {
+      matvecs = recompress_iterative(c, P, cfg, fb, jac_trans, rounds);
+    } else {
+      for (int i = 0; i < int(fb.size()); ++i) active.push_back(i);
+      // dense-svd materializes S I (apply_mat of the identity): n columns per block
+      for (const FarBlock& f : fb) matvecs += f.n;
+    }
     const bool explicit_tail = cfg->policy == 0 && cfg->eps < 1e-6;
     while (!active.empty()) {
       if (rounds >= 6) throw std::runtime_error("sketch adaptation did not converge");
@@ -1474,9 +1817,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         f.W = take(int64_t(l) * l);
         f.V = take(int64_t(l) * l);
         f.sig = take(l);
-        if (f.implicit) matvecs += 2 * (l + PR);
-        else if (f.dense) matvecs += f.n;
-        else matvecs += 2 * l;
+        if (f.implicit) sketch_cols += 2 * (l + PR);
+        else if (f.dense) sketch_cols += f.n;
+        else sketch_cols += 2 * l;
       }
       par_build(active, gm, ga, [&](int i, GemmSet& gm, GatherSet& ga) {
         FarBlock& f = fb[i];
@@ -1760,8 +2103,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->retry_d.ensure(size_t(na));
       select_rank_kernel<<<(na + 127) / 128, 128, 0, s>>>(c->sel_jobs.p, na, cfg->policy,
                                                           cfg->eps, cfg->k_max, over,
-                                                          c->rank_d.p, c->retry_d.p,
-                                                          cfg->tag == 2 ? 1 : 0);
+                                                          c->rank_d.p, c->retry_d.p, 0);
       CK(cudaGetLastError());
       c->launches++;
       std::vector<int> rk(na), rt(na);
@@ -1781,6 +2123,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     }
     CK(cudaEventRecord(c->ev[3], s));
     for (const FarBlock& f : fb) {
+      if (iterative) break;
       int& h = c->rank_hint[ilog2(f.mu)];
       h = std::max(h, f.rank);
       if (f.round > 0) c->class_retry[ilog2(f.mu)] = 1;
@@ -1794,8 +2137,11 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     c->res_off.assign(nl, 0);
     int64_t pos = 0;
     int64_t max_rank = 0;
+    int64_t n_degraded = 0;
     for (const FarBlock& f : fb) {
       c->res_rank[f.leaf] = f.rank;
+      c->res_deg[f.leaf] = int8_t(f.degraded ? 1 : 0);
+      n_degraded += f.degraded ? 1 : 0;
       c->res_off[f.leaf] = pos;
       pos += int64_t(f.m + f.n) * f.rank;
       max_rank = std::max<int64_t>(max_rank, f.rank);
@@ -1803,29 +2149,10 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     c->out_far = pos;
     c->own[BUF_OUT].ensure(size_t(std::max<int64_t>(pos, 1)));
     double* out = c->own[BUF_OUT].p;
-    std::vector<SmallJob> jl;
-    int qmax = 1;
-    int rows_max = 1;
-    for (const FarBlock& f : fb) {
-      if (f.rank == 0) continue;
-      double* left = out + c->res_off[f.leaf];
-      double* right = left + int64_t(f.m) * f.rank;
-      if (f.dense) {
-        jl.push_back(SmallJob{f.Y, f.W, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
-        jl.push_back(SmallJob{nullptr, f.V, nullptr, right, f.n, f.l, f.l, 0, f.rank});
-      } else {
-        jl.push_back(SmallJob{f.Y, f.V, f.sig, left, f.m, f.l, f.l, f.m, f.rank});
-        jl.push_back(SmallJob{f.Bt, f.W, nullptr, right, f.n, f.l, f.l, f.n, f.rank});
-      }
-      qmax = std::max(qmax, f.l);
-      rows_max = std::max(rows_max, std::max(f.m, f.n));
-    }
-    if (!jl.empty()) {
-      c->small_jobs.upload(jl, s);
-      dim3 grid(unsigned(jl.size()), unsigned(std::min(8, (rows_max + 127) / 128)));
-      small_product_kernel<<<grid, 128, 0, s>>>(c->small_jobs.p);
-      CK(cudaGetLastError());
-      c->launches++;
+    {
+      std::vector<int64_t> offs;
+      for (const FarBlock& f : fb) offs.push_back(c->res_off[f.leaf]);
+      launch_far_outputs(c, fb, offs, out);
     }
     pm.mark("output", s);
     // near leaves: payload stays in BUF_TILE after the far blocks
@@ -1854,7 +2181,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       st->ms_recompress = ms;
       st->far_leaves = nf;
       st->near_leaves = nl - nf;
-      st->degraded_blocks = 0;
+      st->degraded_blocks = n_degraded;
+      st->sketch_cols = sketch_cols;
       st->max_far_rank = max_rank;
       st->matvec_count = matvecs;
       st->sketch_rounds = rounds;
@@ -1986,6 +2314,89 @@ extern "C" int hx_debug_qr(int n_jobs, const int32_t* p, const int32_t* q, doubl
     tmp.tsqr_ws.release();
     return HX_OK;
   });
+}
+
+// numpy's default_rng(seed).standard_normal(n) with seed = seed_hi * 2^64 + seed_lo, from
+// the host (device < 0) or the device generator (np_random.cuh; parity tests).
+extern "C" int hx_np_normals(uint64_t seed_lo, uint64_t seed_hi, int64_t n, double* out,
+                             int device) {
+  return guarded([&]() -> int {
+    if (n < 0 || (n && !out)) return fail(HX_EINVAL, "bad arguments");
+    if (device < 0) {
+      NpRng g;
+      g.seed(seed_lo, seed_hi);
+      for (int64_t e = 0; e < n; ++e) out[e] = g.normal();
+      return HX_OK;
+    }
+    CK(cudaSetDevice(device));
+    DArr<double> d;
+    d.ensure(size_t(std::max<int64_t>(n, 1)));
+    np_normals_kernel<<<1, 32>>>(seed_lo, seed_hi, d.p, n);
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    if (n) CK(cudaMemcpy(out, d.p, size_t(n) * sizeof(double), cudaMemcpyDeviceToHost));
+    d.release();
+    return HX_OK;
+  });
+}
+
+// One block through the matrix-free compressor route of hx_product (tag 0 aca,
+// 1 bilanczos, 2 randomized; compressors.py:162-428) on a dense column-major m x n host
+// matrix: the per-block stream is default_rng((seed << 24) ^ node).  left (m x rank) and
+// right (n x rank) receive the factors (room for min(m, n) columns each); info[0..2] =
+// rank, degraded flag, matvec count.
+extern "C" int hx_debug_compress(int tag, int policy, double eps, int k_max, int q,
+                                 uint64_t seed, int32_t node, int m, int n, const double* A,
+                                 double* left, double* right, int32_t* info) {
+  hx_ctx* c = nullptr;
+  const int rc = guarded([&]() -> int {
+    if (tag < 0 || tag > 2 || m < 1 || n < 1 || !A || !left || !right || !info)
+      return fail(HX_EINVAL, "bad arguments");
+    if (policy == 0 && !(eps > 0.0)) return fail(HX_EINVAL, "eps must be positive");
+    if (policy == 1 && k_max < 1) return fail(HX_EINVAL, "k_max must be >= 1");
+    const int st = hx_ctx_create(0, &c);
+    if (st != HX_OK) return st;
+    c->own[BUF_TILE].upload(A, size_t(m) * n, c->s);
+    hx_plan P;
+    P.leaves.resize(1);
+    OutLeaf& L = P.leaves[0];
+    std::memset(&L, 0, sizeof(L));
+    L.id = node;
+    L.kind = 1;
+    L.m = m;
+    L.n = n;
+    std::vector<FarBlock> fb(1);
+    fb[0].leaf = 0;
+    fb[0].m = m;
+    fb[0].n = n;
+    fb[0].mu = std::min(m, n);
+    fb[0].t_off = 0;
+    hx_product_cfg cfg;
+    std::memset(&cfg, 0, sizeof(cfg));
+    cfg.policy = policy;
+    cfg.eps = policy == 0 ? eps : 1.0;
+    cfg.k_max = k_max;
+    cfg.tag = tag;
+    cfg.seed = seed;
+    cfg.q = q;
+    int rounds = 0;
+    const int64_t mv = recompress_iterative(c, &P, &cfg, fb, 1, rounds);
+    const int r = fb[0].rank;
+    c->own[BUF_OUT].ensure(size_t(std::max<int64_t>(int64_t(m + n) * r, 1)));
+    launch_far_outputs(c, fb, std::vector<int64_t>{0}, c->own[BUF_OUT].p);
+    CK(cudaStreamSynchronize(c->s));
+    if (r) {
+      CK(cudaMemcpy(left, c->own[BUF_OUT].p, size_t(m) * r * 8, cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(right, c->own[BUF_OUT].p + int64_t(m) * r, size_t(n) * r * 8,
+                    cudaMemcpyDeviceToHost));
+    }
+    info[0] = r;
+    info[1] = fb[0].degraded;
+    info[2] = int32_t(mv);
+    return HX_OK;
+  });
+  if (c) hx_ctx_free(c);
+  return rc;
 }
 
 // H-matrix times a block of s vectors, Y = M X or M^T X (hmat_vec / _node_matmat,

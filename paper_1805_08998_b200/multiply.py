@@ -504,12 +504,17 @@ def regroup_units(groups, rate, target):
 # --------------------------------------------------------------------------- product
 
 IMPLICIT_MIN = 512  # far leaves with min(m, n) >= this are sketched without materialization
+# The matrix-free tags read rows / columns / matvecs of a block (r + 2 of each for ACA):
+# from the stacked terms that costs (r + 2) K (m + n) words against 2 m n K flops for
+# materializing the block once, so only very large blocks stay implicit for them.
+IMPLICIT_MIN_ITERATIVE = 4096
 
 
-def implicit_flags(implicit_min=None):
+def implicit_flags(implicit_min=None, tag="dense-svd"):
     """HX_PLAN_IMPLICIT bits for a threshold (power of two; 0 disables; env HX_IMPLICIT)."""
     if implicit_min is None:
-        implicit_min = int(os.environ.get("HX_IMPLICIT", IMPLICIT_MIN))
+        implicit_min = int(os.environ.get("HX_IMPLICIT", IMPLICIT_MIN if tag == "dense-svd"
+                                          else IMPLICIT_MIN_ITERATIVE))
     if implicit_min <= 0:
         return 0
     lg = int(np.ceil(np.log2(implicit_min)))
@@ -574,7 +579,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     marks.append(("operands", time.perf_counter()))
     comp = cfg.compressor
     pc = _lib.HxProductCfg(kind, eps, kmax, TAG_CODES[comp.tag], int(comp.seed) & (2**64 - 1),
-                           int(sketch0), int(oversample))
+                           int(sketch0), int(oversample), int(getattr(comp, "q", 1)))
     ta = tree_arrays(h.bct)
     tile = plan_tile(h.bct)
     adaptive = False
@@ -592,7 +597,7 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
 
     plan_ms = [0.0]
     timeline = []  # (what, host start, host end) for HX_TIMING
-    iflags = implicit_flags(implicit_min)
+    iflags = implicit_flags(implicit_min, cfg.compressor.tag)
 
     def make_plan(group):
         mask = group_mask(h.bct, group, leaf_mask) if (len(queue_all) > 1 or leaf_mask
@@ -721,8 +726,8 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
                                                             "res"))
         if fetch:
             fetched.append((leaves, rank, deg, off, res))
-            far_deg = (leaves["kind"] == 1) & (deg != 0)
-            degraded.update(leaves["ids"][far_deg].tolist())
+        far_deg = (leaves["kind"] == 1) & (deg != 0)
+        degraded.update(leaves["ids"][far_deg].tolist())
         rep.degraded_blocks += int(st.degraded_blocks)
         rep.max_far_rank = max(rep.max_far_rank, int(st.max_far_rank))
         rep.matvec_count += int(st.matvec_count)
@@ -748,6 +753,13 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
         print("[hx timeline] " + " ".join(f"{w}:{1e3 * (a - t00):.0f}-{1e3 * (b - t00):.0f}"
                                           for w, a, b in sorted(timeline, key=lambda x: x[1])),
               flush=True)
+    if degraded:  # the reference's warning per degraded block (multiply.py:73-78)
+        arr = block_arrays(h.bct)
+        lo, hi = arr.tree.lo, arr.tree.hi
+        for b in sorted(degraded):
+            t, sg = arr.tau[b], arr.sigma[b]
+            rep.warnings.append(f"block {b} rows [{lo[t]},{hi[t]}) cols [{lo[sg]},{hi[sg]}): "
+                                "compression did not certify convergence")
     rep.chunks = n_run
     rep.plan_ms = plan_ms[0]
     rep.wall_s = time.perf_counter() - t_start

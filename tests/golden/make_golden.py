@@ -233,8 +233,8 @@ if __name__ == "__main__":
     case_compressors()
     all_tags = ("dense-svd", "aca", "bilanczos", "randomized")
     case_products("small2d.npz", 256, "square", 16, 0.8, "exp", None, 1e-8, 1e-6,
-                  all_tags, dense_tags=("dense-svd", "aca"))
+                  all_tags, dense_tags=all_tags)
     case_products("ragged3d.npz", 200, "cube", 12, 1.0, "exp0.5", "inv", 1e-8, 1e-8,
-                  ("dense-svd", "aca"), dense_tags=("dense-svd",))
+                  all_tags, dense_tags=all_tags)
     case_products("cfg1.npz", 2048, "square", 32, 0.8, "exp", None, 1e-8, 1e-6,
-                  ("dense-svd", "aca"), sample="auto")
+                  all_tags, sample="auto")
