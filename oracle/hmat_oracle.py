@@ -623,6 +623,18 @@ class HMatO:
         return math.sqrt(tot)
 
 
+def assemble_leaf_o(kern, near, xr, xc, pol, h=None):
+    """One leaf of ``assemble_hmatrix`` (``hmatrix.py:97-118``): dense near block, or ACA
+    with the dense fallback when ACA cannot certify convergence.  Returns (payload,
+    degraded)."""
+    if near:
+        return kernel_matrix(kern, xr, xc, h), False
+    blk = aca_o(EntryOp(kern, xr, xc, h), pol)
+    if blk.degraded:
+        return kernel_matrix(kern, xr, xc, h), True
+    return blk, False
+
+
 def assemble_o(kern, bt: BlockTreeO, policy, points, h=None):
     """``assemble_hmatrix`` (``hmatrix.py:97-118``) for a point kernel."""
     pts = np.asarray(points, dtype=float)
@@ -632,16 +644,57 @@ def assemble_o(kern, bt: BlockTreeO, policy, points, h=None):
     for b in bt.leaves():
         r0, r1 = bt.rows(b)
         c0, c1 = bt.cols(b)
-        xr, xc = pts[perm[r0:r1]], pts[perm[c0:c1]]
-        if bt.kind[b] == NEAR:
-            data[b] = kernel_matrix(kern, xr, xc, h)
-            continue
-        blk = aca_o(EntryOp(kern, xr, xc, h), pol)
-        if blk.degraded:
+        data[b], deg = assemble_leaf_o(kern, bt.kind[b] == NEAR, pts[perm[r0:r1]],
+                                       pts[perm[c0:c1]], pol, h)
+        if deg:
             bad.add(b)
-            data[b] = kernel_matrix(kern, xr, xc, h)
-        else:
-            data[b] = blk
+    return HMatO(bt, data, bad)
+
+
+def _assemble_chunk_o(kern, pol, h, pts, jobs):
+    """Worker of ``assemble_parallel_o``: jobs = [(id, near, row points, col points)];
+    single-threaded BLAS inside (the processes are the parallelism)."""
+    from threadpoolctl import threadpool_limits
+
+    out = []
+    with threadpool_limits(limits=1):
+        for b, near, ir, ic in jobs:
+            p, deg = assemble_leaf_o(kern, near, pts[ir], pts[ic], pol, h)
+            out.append((b, (p.left, p.right) if isinstance(p, LR) else p, deg))
+    return out
+
+
+def assemble_parallel_o(kern, bt: BlockTreeO, policy, points, h=None, workers=None):
+    """``assemble_o`` with the leaves spread over worker processes (spawned, so the
+    parent's BLAS thread pool is never forked); the same per-leaf arithmetic, so the same
+    operand.  Assembly is setup, outside any timed region (as ``cli.py:150-158``)."""
+    import os
+    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
+
+    pts = np.asarray(points, dtype=float)
+    perm = bt.tree.perm
+    pol = policy_of(policy)
+    workers = workers or os.cpu_count() or 1
+    leaves = bt.leaves()
+    # cost-balanced round-robin over leaves ordered by size
+    cost = [bt.shape(b)[0] * bt.shape(b)[1] for b in leaves]
+    order = np.argsort(cost)[::-1]
+    n_jobs = 4 * workers
+    jobs = [[] for _ in range(n_jobs)]
+    for i, j in enumerate(order):
+        b = leaves[j]
+        r0, r1 = bt.rows(b)
+        c0, c1 = bt.cols(b)
+        jobs[i % n_jobs].append((b, bt.kind[b] == NEAR, perm[r0:r1], perm[c0:c1]))
+    data, bad = {}, set()
+    with ProcessPoolExecutor(max_workers=workers, mp_context=mp.get_context("spawn")) as ex:
+        futs = [ex.submit(_assemble_chunk_o, kern, pol, h, pts, js) for js in jobs if js]
+        for f in futs:
+            for b, p, deg in f.result():
+                data[b] = LR(p[0], p[1]) if isinstance(p, tuple) else p
+                if deg:
+                    bad.add(b)
     return HMatO(bt, data, bad)
 
 
@@ -922,11 +975,14 @@ def hmult_new_o(A: HMatO, B: HMatO, policy, tag="dense-svd", q=1, seed=0, log=No
 
 
 def _parents(bt: BlockTreeO):
-    par = np.full(bt.n_nodes, -1, dtype=np.int64)
-    for b in range(bt.n_nodes):
-        for c in bt.children[b]:
-            if c >= 0:
-                par[c] = b
+    par = getattr(bt, "_parents", None)
+    if par is None:
+        par = np.full(bt.n_nodes, -1, dtype=np.int64)
+        for b in range(bt.n_nodes):
+            for c in bt.children[b]:
+                if c >= 0:
+                    par[c] = b
+        bt._parents = par
     return par
 
 

@@ -19,7 +19,7 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from .hmatrix import HMatrix, block_arrays, tree_arrays
+from .hmatrix import HMatrix, LeafDict, block_arrays, tree_arrays
 from .lowrank import LowRank
 from .multiply import Device
 
@@ -48,7 +48,7 @@ class DevicePool:
             pass
 
 
-class _LazyLeaves(dict):
+class _LazyLeaves(LeafDict):
     """Leaf payload dict filled from the device pool on first access."""
 
     def __init__(self, owner):
@@ -63,11 +63,17 @@ class _LazyLeaves(dict):
         h = self._owner
         pool = h._hx_pool.download()
         h._hx_packed = (pool, h._hx_packed[1])
-        super().update(unpack_leaves(h.bct, pool, h._hx_packed[1]))
+        dict.update(self, unpack_leaves(h.bct, pool, h._hx_packed[1]))
+
+    def __contains__(self, key):
+        self._fill()
+        return super().__contains__(key)
 
     def __missing__(self, key):
         self._fill()
-        return super().__getitem__(key)
+        if dict.__contains__(self, key):
+            return dict.__getitem__(self, key)
+        raise KeyError(key)
 
     def __iter__(self):
         self._fill()
@@ -134,13 +140,14 @@ def assemble_hmatrix(kind, bct, policy, panels, h=None, device=0):
     degraded = np.zeros(nn, np.int8)
     pool = C.c_void_p()
     n_el = C.c_int64()
-    dev = Device.get(device)
-    _lib.check(_lib.lib().hx_assemble(dev.h, C.byref(tb.st), _lib.ptr(tree_pts, _lib.f64p),
-                                      tree_pts.shape[1], KERNELS[kind], float(h), eps,
-                                      _lib.ptr(payload, _lib.i8p), _lib.ptr(rank, _lib.i32p),
-                                      _lib.ptr(u_off, _lib.i64p), _lib.ptr(v_off, _lib.i64p),
-                                      _lib.ptr(d_off, _lib.i64p), _lib.ptr(degraded, _lib.i8p),
-                                      C.byref(pool), C.byref(n_el)), "hx_assemble")
+    with Device.lock(device):
+        dev = Device.get(device)
+        _lib.check(_lib.lib().hx_assemble(
+            dev.h, C.byref(tb.st), _lib.ptr(tree_pts, _lib.f64p), tree_pts.shape[1],
+            KERNELS[kind], float(h), eps, _lib.ptr(payload, _lib.i8p),
+            _lib.ptr(rank, _lib.i32p), _lib.ptr(u_off, _lib.i64p), _lib.ptr(v_off, _lib.i64p),
+            _lib.ptr(d_off, _lib.i64p), _lib.ptr(degraded, _lib.i8p), C.byref(pool),
+            C.byref(n_el)), "hx_assemble")
     H = HMatrix(bct, {}, set(np.flatnonzero(degraded).tolist()))
     H.data = _LazyLeaves(H)
     H._hx_pool = DevicePool(dev, pool.value, int(n_el.value))

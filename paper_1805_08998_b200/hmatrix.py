@@ -24,12 +24,105 @@ from .lowrank import LowRank
 MAX_DENSE = 6144
 
 
+class LeafDict(dict):
+    """The ``data`` dict of an ``HMatrix``: a plain ``{leaf id: payload}`` dict that counts
+    its mutations.  The packed operand pool (and a device copy of it) is cached on the
+    ``HMatrix`` under the dict's identity and version, so assigning, deleting or updating
+    entries -- or replacing ``h.data`` -- makes the next product or ``save_hmatrix`` repack
+    instead of using stale payloads.  Lazy subclasses (payloads unpacked from a pool on
+    first access) fill themselves before any mutation, and ``get`` / ``copy`` see lazy
+    entries like indexing does."""
+
+    def __init__(self, *args, **kw):
+        super().__init__(*args, **kw)
+        self.version = 0
+
+    def _fill(self):  # lazy subclasses materialize every entry here
+        pass
+
+    def __setitem__(self, key, value):
+        self._fill()
+        super().__setitem__(key, value)
+        self.version += 1
+
+    def __delitem__(self, key):
+        self._fill()
+        super().__delitem__(key)
+        self.version += 1
+
+    def update(self, *args, **kw):
+        self._fill()
+        super().update(*args, **kw)
+        self.version += 1
+
+    def pop(self, *args):
+        self._fill()
+        self.version += 1
+        return super().pop(*args)
+
+    def popitem(self):
+        self._fill()
+        self.version += 1
+        return super().popitem()
+
+    def setdefault(self, key, default=None):
+        if key in self:
+            return self[key]
+        self[key] = default
+        return default
+
+    def clear(self):
+        self._fill()
+        super().clear()
+        self.version += 1
+
+    def get(self, key, default=None):
+        try:
+            return self[key]
+        except KeyError:
+            return default
+
+    def copy(self):
+        self._fill()
+        return dict(self.items())
+
+
 class HMatrix:
     def __init__(self, bct, data, degraded=None):
         self.bct = bct
         self.data = data
         self.degraded = set(degraded or ())
         self.report = None
+
+    @property
+    def data(self):
+        return self._data
+
+    @data.setter
+    def data(self, value):
+        # a plain dict is taken over as a LeafDict (same entries) so that its mutations
+        # invalidate the packed-pool cache
+        self._data = value if isinstance(value, LeafDict) else LeafDict(value)
+
+    def _data_key(self):
+        return (id(self._data), self._data.version)
+
+    @property
+    def _hx_packed(self):
+        """(host pool or None, directory) of the packed operand, or None when the payloads
+        changed since it was packed (the device copy is dropped with it)."""
+        c = self.__dict__.get("_hx_packed_c")
+        if c is None:
+            return None
+        if c[1] != self._data_key():
+            for name in ("_hx_packed_c", "_hx_device", "_hx_pool", "_hx_pool_pinned"):
+                self.__dict__.pop(name, None)
+            return None
+        return c[0]
+
+    @_hx_packed.setter
+    def _hx_packed(self, value):
+        self.__dict__["_hx_packed_c"] = (value, self._data_key())
 
     @property
     def n(self):
@@ -172,7 +265,7 @@ def frobenius_norm(h):
 
 
 # ------------------------------------------------------------------ HMX1 operator files
-class _PoolLeaves(dict):
+class _PoolLeaves(LeafDict):
     """Leaf payloads unpacked on first access from a packed host pool (loaded operands)."""
 
     def __init__(self, owner):
@@ -187,11 +280,13 @@ class _PoolLeaves(dict):
         from .assembly import unpack_leaves
         h = self._owner
         pool, d = h._hx_packed
-        super().update(unpack_leaves(h.bct, pool, d))
+        dict.update(self, unpack_leaves(h.bct, pool, d))
 
     def __missing__(self, key):
         self._fill()
-        return super().__getitem__(key)
+        if dict.__contains__(self, key):
+            return dict.__getitem__(self, key)
+        raise KeyError(key)
 
     def __contains__(self, key):
         self._fill()
@@ -288,6 +383,6 @@ def load_hmatrix(path, bct):
                                        _lib.ptr(pos, _lib.i64p), _lib.ptr(pool, _lib.f64p)),
                "load_hmatrix")
     H = HMatrix(bct, {}, set(np.flatnonzero(deg).tolist()))
-    H._hx_packed = (pool, d)
     H.data = _PoolLeaves(H)
+    H._hx_packed = (pool, d)  # keyed to the lazy dict just installed
     return H

@@ -48,14 +48,15 @@ def hmat_matmat(h, x, transpose=False, device=0):
     if X.shape[0] != h.n:
         raise ValueError(f"expected {h.n} rows, got {x.shape}")
     s = X.shape[1]
-    dev = Device.get(device)
-    d = _attach(h, dev, 0, device)
-    tb = _lib.TreeBuf(tree_arrays(h.bct))
-    ob = _lib.OperandBuf(d)
     Y = np.zeros((h.n, s), order="F")
-    _lib.check(_lib.lib().hx_hmatvec(dev.h, C.byref(tb.st), C.byref(ob.st), 0,
-                                     int(bool(transpose)), _lib.ptr(X, _lib.f64p),
-                                     _lib.ptr(Y, _lib.f64p), s), "hx_hmatvec")
+    with Device.lock(device):
+        dev = Device.get(device)
+        d = _attach(h, dev, 0, device)
+        tb = _lib.TreeBuf(tree_arrays(h.bct))
+        ob = _lib.OperandBuf(d)
+        _lib.check(_lib.lib().hx_hmatvec(dev.h, C.byref(tb.st), C.byref(ob.st), 0,
+                                         int(bool(transpose)), _lib.ptr(X, _lib.f64p),
+                                         _lib.ptr(Y, _lib.f64p), s), "hx_hmatvec")
     return Y[:, 0].copy() if vec else Y
 
 
@@ -83,3 +84,33 @@ def product_error(c, a, b, probes=8, seed=0, device=0):
     num = np.linalg.norm(cx - abx)
     den = np.linalg.norm(cx)
     return float(num / den), float(den / np.sqrt(probes))
+
+
+def estimate_product_error(h, k, l, iters=10, block_size=100, seed=0, device=0):
+    """Frobenius estimate of ||L - H K|| by block subspace iteration: the reference's
+    ``estimate_product_error`` (``multiply.py:266-294``, same signature and defaults).
+
+    Two-sided subspace iteration on the residual operator x -> L x - H (K x): start from
+    the Q factor of an n x b Gaussian block (``default_rng(seed)``), then ``iters`` rounds
+    of y = qr(R x), x = qr(R^T y); the value is the root of the summed squared singular
+    values of R x (a lower bound of ||R||_F that sharpens with b).  Every H-matrix x block
+    product runs on the GPU (``hmat_matmat``); the thin QRs and the final SVD of the
+    n x b blocks stay on the host, as in the reference."""
+    n = l.n
+    b = min(block_size, n)
+    rng = np.random.default_rng(seed)
+
+    def resid(x):
+        return hmat_matmat(l, x, device=device) - hmat_matmat(
+            h, hmat_matmat(k, x, device=device), device=device)
+
+    def resid_t(x):
+        return hmat_matmat(l, x, True, device) - hmat_matmat(
+            k, hmat_matmat(h, x, True, device), True, device)
+
+    x = np.linalg.qr(rng.standard_normal((n, b)))[0]
+    for _ in range(iters):
+        y = np.linalg.qr(resid(x))[0]
+        x = np.linalg.qr(resid_t(y))[0]
+    ritz = np.linalg.svd(resid(x), compute_uv=False)
+    return float(np.sqrt(np.sum(ritz ** 2)))

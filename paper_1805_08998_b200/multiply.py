@@ -31,7 +31,7 @@ import numpy as np
 
 from . import _lib
 from .compressors import TAG_CODES, CompressorKind, clamp_eps
-from .hmatrix import HMatrix, block_arrays, pack_operand, tree_arrays
+from .hmatrix import HMatrix, LeafDict, block_arrays, pack_operand, tree_arrays
 from .lowrank import EpsRank, FixedRank, LowRank
 
 CONVERTERS = ("hier-approx", "aca", "bilanczos", "randomized", "dense-svd")
@@ -94,6 +94,17 @@ class Device:
         return cls._cache[device]
 
     _aux: dict = {}
+    _locks: dict = {}
+    _locks_guard = threading.Lock()
+
+    @classmethod
+    def lock(cls, device=0):
+        """Per-device re-entrant lock: the contexts of a device (operand slots, streams,
+        workspaces) serve one product or H-matrix x block call at a time."""
+        with cls._locks_guard:
+            if device not in cls._locks:
+                cls._locks[device] = threading.RLock()
+            return cls._locks[device]
 
     @classmethod
     def aux(cls, device=0, i=0):
@@ -161,7 +172,7 @@ def _host_directory(h):
     return pool, d
 
 
-class _ProductLeaves(dict):
+class _ProductLeaves(LeafDict):
     """Leaf payloads of a product, built on first access from the downloaded result
     buffers (zero-copy views: far leaves LowRank(U*S, V), near leaves m x n arrays)."""
 
@@ -197,19 +208,19 @@ class _ProductLeaves(dict):
         if w is None:
             raise KeyError(key)
         v = self._make(*w)
-        super().__setitem__(key, v)
+        dict.__setitem__(self, key, v)
         return v
 
     def __contains__(self, key):
-        return key in self._index()
+        return key in self._index() if not self._filled else dict.__contains__(self, key)
 
     def _fill(self):
         if self._filled:
             return
         for ci, (lv, *_rest) in enumerate(self._chunks):
             for i, b in enumerate(lv["ids"].tolist()):
-                if not super().__contains__(b):
-                    super().__setitem__(b, self._make(ci, i))
+                if not dict.__contains__(self, b):
+                    dict.__setitem__(self, b, self._make(ci, i))
         self._filled = True
 
     def __iter__(self):
@@ -217,7 +228,7 @@ class _ProductLeaves(dict):
         return super().__iter__()
 
     def __len__(self):
-        return len(self._index())
+        return len(self._index()) if not self._filled else dict.__len__(self)
 
     def keys(self):
         self._fill()
@@ -529,14 +540,27 @@ def overlap_default(overlap=None):
 
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
                     device_operands=True, fetch=True, chunks=None, implicit_min=None,
-                    overlap=None):
+                    overlap=None, device_pools=None):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
     assembly) instead of uploading the host copy.  ``leaf_mask`` restricts the product to
     the owned output leaves (multi-GPU partition).  ``fetch=False`` leaves the output
     blocks in device memory (only ranks and the report come back): the device-resident
-    measurement of bench.py.  ``chunks``: number of pipelined chunks (default by size)."""
+    measurement of bench.py.  ``chunks``: number of pipelined chunks (default by size).
+    ``device_pools``: ((ptr, n) of A, (ptr, n) of B), packed pools already on this device
+    (replicas of a multi-GPU product, ``distributed.py``).  Calls on the same device are
+    serialized (``Device.lock``)."""
+    if h.bct is not k.bct:
+        raise ValueError("factors must live on the same block-cluster tree")
+    with Device.lock(device):
+        return _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample,
+                                device_operands, fetch, chunks, implicit_min, overlap,
+                                device_pools)
+
+
+def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_operands,
+                     fetch, chunks, implicit_min, overlap, device_pools):
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     policy = cfg.policy
@@ -547,6 +571,9 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     same = k is h
 
     def resident(x):
+        if device_pools is not None:
+            p = device_pools[0 if x is h else 1]
+            return (device, p[0], p[1])
         d = getattr(x, "_hx_device", None)
         return d if (device_operands and d is not None and d[0] == device) else None
 
@@ -664,56 +691,66 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     seen = [0.0, 0.0]  # planned workspace bytes and leaf area (adaptive chunking)
     last_rate = [0.0]  # workspace rate of the last rejected (too large) plan
     inflight = collections.deque()
-    group = queue.popleft()
-    plan = make_plan(group)
-    while True:
-        # a chunk whose workspace would not fit is split and planned again
-        while plan is not None and plan_bytes(plan.info) > budget:
-            # split once into as many parts as the measured workspace per leaf area asks
-            # for (not by repeated halving: every rejected plan is wasted host time)
-            pb = plan_bytes(plan.info)
-            area = sum(u[2] for u in group)
-            rate = pb / max(area, 1.0)
-            last_rate[0] = max(last_rate[0], rate)
-            units = group if len(group) > 1 else [p[0] for p in split_chunk(h.bct, group)]
-            parts = regroup_units([units], rate, 0.7 * budget) if len(units) > 1 else [units]
-            if len(parts) == 1:
-                parts = split_chunk(h.bct, units)
-            if len(parts) == 1:
-                break
-            group_split[0] = True
-            plan.close()
-            group = parts[0]
-            queue.extendleft(reversed(parts[1:]))
-            plan = make_plan(group)
-        if adaptive and plan is not None and queue:
-            # workspace per unit of leaf area: the larger of the average over the plans so
-            # far and the latest plan's (dense regions are priced by their own rate); the
-            # remaining subtrees are regrouped to fill the budget
-            pb = plan_bytes(plan.info)
-            area = sum(u[2] for u in group)
-            seen[0] += pb
-            seen[1] += area
-            rate = max(seen[0] / max(seen[1], 1.0), pb / max(area, 1.0), last_rate[0])
-            last_rate[0] = 0.0
-            queue = collections.deque(regroup_units(list(queue), rate, 0.7 * budget))
-        if plan is not None:
-            if len(inflight) >= len(ctxs):  # the context of chunk i - len(ctxs) must be free
-                t = inflight.popleft()
-                t.join()
-            out = {}
-            chunks_out.append(out)
-            t = threading.Thread(target=run_chunk,
-                                 args=(plan, ctxs[(len(chunks_out) - 1) % len(ctxs)], out))
-            t.start()
-            inflight.append(t)
-        if not queue:
-            break
-        # plan the next chunk while the device runs the current one(s)
+    plan = None
+    try:
         group = queue.popleft()
         plan = make_plan(group)
-    for t in inflight:
-        t.join()
+        while True:
+            # a chunk whose workspace would not fit is split and planned again
+            while plan is not None and plan_bytes(plan.info) > budget:
+                # split once into as many parts as the measured workspace per leaf area asks
+                # for (not by repeated halving: every rejected plan is wasted host time)
+                pb = plan_bytes(plan.info)
+                area = sum(u[2] for u in group)
+                rate = pb / max(area, 1.0)
+                last_rate[0] = max(last_rate[0], rate)
+                units = group if len(group) > 1 else \
+                    [p[0] for p in split_chunk(h.bct, group)]
+                parts = regroup_units([units], rate, 0.7 * budget) if len(units) > 1 \
+                    else [units]
+                if len(parts) == 1:
+                    parts = split_chunk(h.bct, units)
+                if len(parts) == 1:
+                    break
+                group_split[0] = True
+                plan.close()
+                group = parts[0]
+                queue.extendleft(reversed(parts[1:]))
+                plan = make_plan(group)
+            if adaptive and plan is not None and queue:
+                # workspace per unit of leaf area: the larger of the average over the plans
+                # so far and the latest plan's (dense regions are priced by their own rate);
+                # the remaining subtrees are regrouped to fill the budget
+                pb = plan_bytes(plan.info)
+                area = sum(u[2] for u in group)
+                seen[0] += pb
+                seen[1] += area
+                rate = max(seen[0] / max(seen[1], 1.0), pb / max(area, 1.0), last_rate[0])
+                last_rate[0] = 0.0
+                queue = collections.deque(regroup_units(list(queue), rate, 0.7 * budget))
+            if plan is not None:
+                if len(inflight) >= len(ctxs):  # chunk i - len(ctxs)'s context must be free
+                    t = inflight.popleft()
+                    t.join()
+                out = {}
+                chunks_out.append(out)
+                t = threading.Thread(target=run_chunk,
+                                     args=(plan, ctxs[(len(chunks_out) - 1) % len(ctxs)], out))
+                t.start()
+                inflight.append(t)
+                plan = None  # owned (and closed) by the chunk thread now
+            if not queue:
+                break
+            # plan the next chunk while the device runs the current one(s)
+            group = queue.popleft()
+            plan = make_plan(group)
+    finally:
+        if plan is not None:
+            plan.close()
+        # every chunk thread is joined, also when planning raised (e.g. MemoryError): no
+        # thread may keep running hx_product on this device's contexts after we return
+        for t in inflight:
+            t.join()
     marks.append(("products", time.perf_counter()))
     degraded = set()
     leaves_all, ranks_all, infos, fetched = [], [], [], []
@@ -786,8 +823,19 @@ def _sum_info(infos):
     return tot
 
 
-def hmult_new(h, k, cfg):
-    """Product H K with one direct compression per farfield leaf (GPU)."""
+def hmult_new(h, k, cfg, devices=None):
+    """Product H K with one direct compression per farfield leaf (reference signature,
+    ``multiply.py:252-256``).  ``devices`` (optional; default ``HX_DEVICES`` = comma list,
+    else GPU 0): with several GPUs the output subtrees are partitioned over them and the
+    operand pools replicated by an NCCL broadcast (``distributed.multiply_devices``)."""
     if cfg.mode != "new":
         raise ValueError("config mode must be 'new'")
-    return multiply_device(h, k, cfg)
+    if h.bct is not k.bct:
+        raise ValueError("factors must live on the same block-cluster tree")
+    if devices is None:
+        env = os.environ.get("HX_DEVICES", "")
+        devices = [int(x) for x in env.split(",") if x.strip()] or [0]
+    if len(devices) > 1:
+        from .distributed import multiply_devices
+        return multiply_devices(h, k, cfg, devices)
+    return multiply_device(h, k, cfg, device=int(devices[0]))

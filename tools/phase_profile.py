@@ -1,7 +1,7 @@
 """One product of a BASELINE config under an ncu range (second product; the first warms up).
 
 usage: ncu --profile-from-start off --metrics gpu__time_duration.sum,dram__bytes_read.sum,\
-dram__bytes_write.sum --csv --log-file out.csv python tools/phase_profile.py CFG
+dram__bytes_write.sum --csv --log-file out.csv python tools/phase_profile.py CFG [--tag aca]
 then:  python tools/phase_profile.py --summarize out.csv
 """
 import collections
@@ -49,8 +49,8 @@ def main():
 
     c = configs.CONFIGS[int(sys.argv[1])]
     bct, A, B = configs.build_operands(c)
-    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"),
-                            policy=hx.EpsRank(c["tol"]))
+    tag = sys.argv[sys.argv.index("--tag") + 1] if "--tag" in sys.argv else "aca"
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(tag), policy=hx.EpsRank(c["tol"]))
     hx.multiply.multiply_device(A, B, cfg, fetch=False)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
