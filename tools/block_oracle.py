@@ -5,10 +5,15 @@ far size class up to --max-size, the largest included, plus some near leaves) th
 restatement rebuilds S(leaf) along its root-to-leaf chain (``leaf_expr``, the reference's
 sumexpr_root + restrict, sumexpr.py:78-154), densifies it and takes its best approximation
 at the tolerance (dense-svd semantics, compressors.py:431-438 with select_rank,
-lowrank.py:75-90).  Contract per block: rank within +-1, relative difference <= 10 tol;
-near blocks exact to 1e-12.
+lowrank.py:75-90).  Blocks larger than --dense-max (the reference's own dense cap is 6144,
+compressors.py:31) are checked matrix-free, as SURVEY 8(c) prescribes: the oracle's
+restatement of the reference ``bilanczos`` (compressors.py:271-365, which reproduces the
+dense-svd ranks) runs on S(leaf) through its matvecs, with the per-block seed, and the
+factored results are compared through their Gram matrices (no densification).  Contract
+per block: rank within +-1, relative difference <= 10 tol; near blocks exact to 1e-12.
 
-usage: python tools/block_oracle.py CFG [--per-class 8] [--max-size 4096] [--near 8]
+usage: python tools/block_oracle.py CFG [--per-class 8] [--max-size 0] [--near 8]
+                                        [--dense-max 4096] [--tag dense-svd]
 """
 import argparse
 import sys
@@ -30,11 +35,23 @@ def oracle_operand(H, obt):
     return O.HMatO(obt, data, H.degraded)
 
 
+def lr_rel_diff(u1, v1, u2, v2):
+    """||U1 V1^T - U2 V2^T||_F / ||U2 V2^T||_F through k x k Gram matrices."""
+    L = np.hstack([u1, -u2])
+    R = np.hstack([v1, v2])
+    num = np.sqrt(max(np.trace((L.T @ L) @ (R.T @ R)), 0.0))
+    den = np.sqrt(max(np.trace((u2.T @ u2) @ (v2.T @ v2)), 0.0))
+    return float(num / max(den, 1e-300))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cfg", type=int)
     ap.add_argument("--per-class", type=int, default=8)
-    ap.add_argument("--max-size", type=int, default=4096)
+    ap.add_argument("--max-size", type=int, default=0, help="skip far sizes above (0: none)")
+    ap.add_argument("--dense-max", type=int, default=4096,
+                    help="larger blocks: matrix-free (Lanczos) oracle")
+    ap.add_argument("--tag", default="dense-svd")
     ap.add_argument("--near", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1)
     a = ap.parse_args()
@@ -42,7 +59,7 @@ def main():
     tol = c["tol"]
     t0 = time.time()
     bct, A, B = configs.build_operands(c)
-    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(tol))
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(a.tag), policy=hx.EpsRank(tol))
     C = hx.hmult_new(A, B, cfg)
     print(f"cfg{a.cfg}: GPU product {C.report.wall_s:.1f} s (setup {time.time() - t0:.1f} s)",
           flush=True)
@@ -57,7 +74,7 @@ def main():
     near = np.flatnonzero(bct.kind_code == 2)
     sample = []
     for m in np.unique(size[far]):
-        if m > a.max_size:
+        if a.max_size and m > a.max_size:
             continue
         ids = far[size[far] == m]
         pick = rng.choice(ids, size=min(a.per_class, len(ids)), replace=False)
@@ -68,8 +85,17 @@ def main():
     for b in sample:
         s = O.leaf_expr(oa, ob, b)
         m, n = s.shape
-        dense = s.mat(np.eye(n))
         q = C.data[b]
+        if bct.kind_code[b] == 1 and min(m, n) > a.dense_max:
+            tl = time.time()
+            ref = O.lanczos_o(s, O.Eps(tol), seed=O.block_seed(0, b))
+            d = lr_rel_diff(q.left, q.right, ref.left, ref.right)
+            worst_rank = max(worst_rank, abs(q.rank - ref.rank))
+            worst_far = max(worst_far, d)
+            print(f"  far  {b:8d} {m}x{n}: rank gpu {q.rank} oracle {ref.rank} (Lanczos, "
+                  f"matrix-free, {time.time() - tl:.0f} s), rel diff {d:.2e}", flush=True)
+            continue
+        dense = s.mat(np.eye(n))
         if bct.kind_code[b] == 2:
             d = np.linalg.norm(q - dense) / max(np.linalg.norm(dense), 1e-300)
             worst_near = max(worst_near, d)

@@ -40,6 +40,8 @@ def main():
     ap.add_argument("--tag", default="dense-svd")
     ap.add_argument("--check", action="store_true")
     ap.add_argument("--estimate", type=int, default=0, help="probes of the GPU estimator")
+    ap.add_argument("--ref-estimate", action="store_true",
+                    help="the reference's estimate_product_error (subspace iteration) on the GPU")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     t0 = time.time()
@@ -70,6 +72,13 @@ def main():
         est, cn = product_error(C, A, B, probes=a.estimate)
         print(f"estimated ||C - AB||/||C|| = {est:.3e} ({a.estimate} probes, tol {c['tol']}) "
               f"||C|| ~ {cn:.4e} check {time.time()-t0:.1f}s", flush=True)
+    if a.ref_estimate:
+        from paper_1805_08998_b200.matvec import estimate_product_error
+        t0 = time.time()
+        est = estimate_product_error(A, B, C)
+        fro = hx.frobenius_norm(C)
+        print(f"estimate_product_error (10 iterations, block 100): ||C - AB|| ~ {est:.4e}, "
+              f"/ ||C||_F = {est / fro:.3e} (tol {c['tol']}) {time.time()-t0:.1f}s", flush=True)
     if a.check:
         import torch
         t0 = time.time()
