@@ -219,7 +219,8 @@ int hx_pool_free(hx_ctx* ctx, double* pool_dev);
 int hx_debug_qr(int n_jobs, const int32_t* p, const int32_t* q, double* X, double* R);
 /* Diagnostics: run the grouped DMMA GEMM kernel on host data (Term / Tile / Group records
  * of paper_1805_08998_b200/csrc/hx_types.h; host_bufs/buf_elems: 10 buffer slots, copied to
- * the device and back).  Used by the kernel-level parity tests. */
+ * the device and back).  tile = 32 or 64, or -64 for the 64-tile kernel configured for
+ * short-K batches (term formation).  Used by the kernel-level parity tests. */
 int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const void* tiles,
                   int64_t n_tiles, const void* groups, int64_t n_groups,
                   double* const* host_bufs, const int64_t* buf_elems, double* sumsq,

@@ -12,7 +12,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["plan.cpp", "errors.cpp", "hmx1.cpp", "runtime.cu"]
-HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "dense_la.cuh", "dense_la_warp.cuh",
+HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "gemm_ws.cuh", "dense_la.cuh", "dense_la_warp.cuh",
            "qr_rows.cuh", "gather_gemm.cuh", "assemble.cuh", "iterative.cuh",
            "np_random.cuh"]
 OUT = os.path.join(HERE, "libhx.so")

@@ -31,6 +31,7 @@
 #include "dense_la_warp.cuh"
 #include "gather_gemm.cuh"
 #include "gemm.cuh"
+#include "gemm_ws.cuh"
 #include "iterative.cuh"
 #include "qr_rows.cuh"
 #include "hx_internal.h"
@@ -124,6 +125,34 @@ __global__ void eye_kernel(double* __restrict__ m, int64_t n, int ld) {
 
 cudaEvent_t g_epoch;
 bool g_epoch_set = false;
+std::chrono::steady_clock::time_point g_host_epoch;
+
+// Host-side milestones of one hx_product (HX_TIMING, after hx_timeline_epoch): milliseconds
+// since the epoch, printed on exit, next to the device marks of hx_product_stats.t_marks.
+struct HostMarks {
+  bool on = g_epoch_set && std::getenv("HX_TIMING") != nullptr;
+  const void* who;
+  std::vector<std::pair<const char*, double>> m;
+  explicit HostMarks(const void* c) : who(c) { mark("entry"); }
+  void mark(const char* what) {
+    if (!on) return;
+    m.emplace_back(what, std::chrono::duration<double, std::milli>(
+                             std::chrono::steady_clock::now() - g_host_epoch).count());
+  }
+  ~HostMarks() {
+    if (!on) return;
+    mark("exit");
+    std::string line = "[hx host] ";
+    char buf[64];
+    std::snprintf(buf, sizeof(buf), "%p:", who);
+    line += buf;
+    for (auto& x : m) {
+      std::snprintf(buf, sizeof(buf), " %s %.1f", x.first, x.second);
+      line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
+};
 
 }  // namespace
 
@@ -132,6 +161,7 @@ extern "C" int hx_timeline_epoch(void) {
     if (!g_epoch_set) CK(cudaEventCreate(&g_epoch));
     g_epoch_set = true;
     CK(cudaEventRecord(g_epoch, 0));
+    g_host_epoch = std::chrono::steady_clock::now();
     return HX_OK;
   });
 }
@@ -454,6 +484,22 @@ void par_build(const std::vector<int>& active, GemmSet& gm, GatherSet& ga,
 }
 
 struct hx_ctx {
+  // page-locked staging of the product's small device-to-host reads (ranks, flags, norms):
+  // a copy into pageable memory goes through the driver's shared staging path and was seen
+  // waiting ~60 ms behind other contexts' transfers
+  void* stage = nullptr;
+  size_t stage_bytes = 0;
+  void d2h(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    if (bytes > stage_bytes) {
+      if (stage) hx::pinned_free(stage, stage_bytes);
+      stage_bytes = std::max(bytes, size_t(1) << 20);
+      stage = hx::pinned_alloc(stage_bytes);
+    }
+    CK(cudaMemcpyAsync(stage, src, bytes, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::memcpy(dst, stage, bytes);
+  }
   int device = 0;
   cudaStream_t s = nullptr;
   cudaStream_t s2 = nullptr;  // copy stream (materialization work lists)
@@ -548,6 +594,64 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
     attr = true;
   }
   static const bool use_short = !std::getenv("HX_NO_SHORTK");
+  // warp-specialized persistent kernel (gemm_ws.cuh) unless HX_GEMM_WS=0
+  static const bool use_ws = !(std::getenv("HX_GEMM_WS") && std::getenv("HX_GEMM_WS")[0] == '0');
+  if (tile == 64 && use_ws) {
+    static int grid_s = 0, grid_l = 0, grid_s2 = 0, grid_s4 = 0, grid_l4 = 0;
+    static const bool short2 = std::getenv("HX_WS_SHORT2") != nullptr;
+    static const bool npw4 = std::getenv("HX_WS_NPW") && std::atoi(std::getenv("HX_WS_NPW")) == 4;
+    if (!grid_s) {
+      auto grid_of = [](auto kern, int threads, int smem) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int dev = 0, sms = 0, b = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem));
+        return std::max(1, b) * sms;
+      };
+      grid_s4 = grid_of(grouped_gemm_ws_kernel<Ws64s4>, Ws64s4::THREADS, Ws64s4::SMEM);
+      grid_l4 = grid_of(grouped_gemm_ws_kernel<Ws64x4>, Ws64x4::THREADS, Ws64x4::SMEM);
+      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64s>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64s::SMEM));
+      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64s2>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64s2::SMEM));
+      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64::SMEM));
+      int dev = 0, sms = 0, bs = 0, bl = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bs, grouped_gemm_ws_kernel<Ws64s>,
+                                                       Ws64s::THREADS, Ws64s::SMEM));
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, grouped_gemm_ws_kernel<Ws64>,
+                                                       Ws64::THREADS, Ws64::SMEM));
+      grid_s = std::max(1, bs) * sms;
+      grid_l = std::max(1, bl) * sms;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bs, grouped_gemm_ws_kernel<Ws64s2>,
+                                                       Ws64s2::THREADS, Ws64s2::SMEM));
+      grid_s2 = std::max(1, bs) * sms;
+    }
+    if (npw4 && short_k && use_short)
+      grouped_gemm_ws_kernel<Ws64s4><<<std::min(n_tiles, grid_s4), Ws64s4::THREADS,
+                                       Ws64s4::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
+                                                           n_tiles, gcols);
+    else if (npw4)
+      grouped_gemm_ws_kernel<Ws64x4><<<std::min(n_tiles, grid_l4), Ws64x4::THREADS,
+                                       Ws64x4::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
+                                                           n_tiles, gcols);
+    else if (short_k && use_short && short2)
+      grouped_gemm_ws_kernel<Ws64s2><<<std::min(n_tiles, grid_s2), Ws64s2::THREADS,
+                                       Ws64s2::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
+                                                           n_tiles, gcols);
+    else if (short_k && use_short)
+      grouped_gemm_ws_kernel<Ws64s><<<std::min(n_tiles, grid_s), Ws64s::THREADS, Ws64s::SMEM,
+                                      st>>>(tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+    else
+      grouped_gemm_ws_kernel<Ws64><<<std::min(n_tiles, grid_l), Ws64::THREADS, Ws64::SMEM,
+                                     st>>>(tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+    CK(cudaGetLastError());
+    c->launches++;
+    return;
+  }
   if (tile == 64 && short_k && use_short)
     grouped_gemm_kernel<Gemm64s><<<n_tiles, Gemm64s::THREADS, Gemm64s::SMEM, st>>>(
         tiles, groups, terms, bp, sumsq, n_tiles, gcols);
@@ -1060,9 +1164,7 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->launches++;
     }
     std::vector<IterOut> got(order.size());
-    CK(cudaMemcpyAsync(got.data(), c->iter_outs.p, got.size() * sizeof(IterOut),
-                       cudaMemcpyDeviceToHost, c->s));
-    CK(cudaStreamSynchronize(c->s));
+    c->d2h(got.data(), c->iter_outs.p, got.size() * sizeof(IterOut), c->s);
     std::vector<int> next;
     size_t a = 0;
     for (int i : big) outs[size_t(i)] = got[a++];
@@ -1174,9 +1276,7 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
   CK(cudaGetLastError());
   c->launches++;
   std::vector<int> rk(static_cast<size_t>(na));
-  CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, size_t(na) * sizeof(int), cudaMemcpyDeviceToHost,
-                     c->s));
-  CK(cudaStreamSynchronize(c->s));
+  c->d2h(rk.data(), c->rank_d.p, size_t(na) * sizeof(int), c->s);
   for (int a = 0; a < na; ++a) fb[size_t(svd[size_t(a)])].rank = rk[size_t(a)];
   return matvecs;
 }
@@ -1405,6 +1505,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     if (!c->buf(BUF_A) || !c->buf(BUF_B)) return fail(HX_EINVAL, "operands not set");
     CK(cudaSetDevice(c->device));
     const int over = cfg->oversample > 0 ? cfg->oversample : 6;
+    HostMarks hm(c);
     NvtxPhases nvtx;
     nvtx.next("hx::setup");
     c->launches = 0;
@@ -1514,6 +1615,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaStreamWaitEvent(s, c->ev[6], 0));
     }
     CK(cudaEventRecord(c->ev[1], s));
+    hm.mark("form-issued");
     nvtx.next("hx::materialize");
     // ---- 2. materialization
     CK(cudaStreamWaitEvent(s, c->ev[7], 0));
@@ -1538,6 +1640,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       c->launches++;
     }
 
+    hm.mark("mat-issued");
     nvtx.next("hx::recompress");
     // ---- 3. recompression of far leaves, on the high-priority stream
     const cudaStream_t s_main = s;
@@ -1728,7 +1831,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     std::vector<int> active;
     const bool iterative = cfg->tag >= 0 && cfg->tag <= 2;
     if (iterative) {
+      hm.mark("iter-start");
       matvecs = recompress_iterative(c, P, cfg, fb, jac_trans, rounds);
+      hm.mark("iter-done");
     } else {
       for (int i = 0; i < int(fb.size()); ++i) active.push_back(i);
       // dense-svd materializes S I (apply_mat of the identity): n columns per block
@@ -2107,9 +2212,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       CK(cudaGetLastError());
       c->launches++;
       std::vector<int> rk(na), rt(na);
-      CK(cudaMemcpyAsync(rk.data(), c->rank_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaMemcpyAsync(rt.data(), c->retry_d.p, na * sizeof(int), cudaMemcpyDeviceToHost, s));
-      CK(cudaStreamSynchronize(s));
+      c->d2h(rk.data(), c->rank_d.p, na * sizeof(int), s);
+      c->d2h(rt.data(), c->retry_d.p, na * sizeof(int), s);
       pm.mark("select", s);
       std::vector<int> next;
       for (int a = 0; a < na; ++a) {
@@ -2129,6 +2233,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       if (f.round > 0) c->class_retry[ilog2(f.mu)] = 1;
     }
 
+    hm.mark("recomp-done");
     nvtx.next("hx::output");
     // ---- 4. output factors
     const int nf = int(fb.size());
@@ -2163,7 +2268,9 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       if (L.kind == 2) c->res_off[i] = c->out_far + (L.ws_off - P->near_ws_begin);
     }
     CK(cudaEventRecord(c->ev[4], s));
+    hm.mark("out-issued");
     CK(cudaEventSynchronize(c->ev[4]));
+    hm.mark("synced");
 
     if (st) {
       std::memset(st, 0, sizeof(*st));
@@ -2189,8 +2296,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       st->launches = c->launches;
       st->out_elems = c->out_far + c->near_elems;
       std::vector<double> f2(nl);
-      if (nl)
-        CK(cudaMemcpy(f2.data(), c->fro2.p, nl * sizeof(double), cudaMemcpyDeviceToHost));
+      if (nl) c->d2h(f2.data(), c->fro2.p, nl * sizeof(double), s);
       double tot = 0;
       for (double v : f2) tot += v;
       st->fro2_total = tot;
@@ -2241,6 +2347,9 @@ extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const
                              double* const* host_bufs, const int64_t* buf_elems, double* sumsq,
                              int64_t n_sumsq) {
   return guarded([&]() -> int {
+    // tile -64: the 64-tile kernel configured for short-K batches (term formation)
+    const bool short_k = tile == -64;
+    if (short_k) tile = 64;
     if ((tile != 32 && tile != 64) || !terms || !tiles || !groups || !host_bufs || !buf_elems)
       return fail(HX_EINVAL, "bad arguments");
     cudaStream_t s = nullptr;
@@ -2263,7 +2372,7 @@ extern "C" int hx_debug_gemm(int tile, const void* terms, int64_t n_terms, const
         bp.p[i] = db[i].p;
       }
     }
-    launch_gemm(&tmp, tile, dl.p, dg.p, dt.p, int(n_tiles), bp, ds.p);
+    launch_gemm(&tmp, tile, dl.p, dg.p, dt.p, int(n_tiles), bp, ds.p, nullptr, short_k);
     CK(cudaDeviceSynchronize());
     for (int i = 0; i < NUM_BUFS; ++i)
       if (bp.p[i])
@@ -2603,6 +2712,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
   cudaStreamDestroy(c->s2);
   cudaStreamDestroy(c->s_hi);
   cudaStreamDestroy(c->s3);
+  if (c->stage) hx::pinned_free(c->stage, c->stage_bytes);
   delete c;
 }
 

@@ -663,6 +663,7 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
             _lib.check(_lib.lib().hx_product(ctx.h, plan.h, C.byref(pc), C.byref(st)),
                        "hx_product")
             timeline.append(("product", t0, time.perf_counter()))
+            t_ret = time.perf_counter()
             if os.environ.get("HX_TIMING"):
                 tm = list(st.t_marks)
                 print(f"[hx device] ctx {ctxs.index(ctx)}: start {tm[0]:.1f} form-end "
@@ -682,10 +683,13 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
                                                          res.size), "hx_result_download")
             out.update(st=st, leaves=leaves, rank=rank, deg=deg, off=off, res=res,
                        info=plan.info)
+            timeline.append(("results", t_ret, time.perf_counter()))
         except BaseException as exc:  # re-raised on the main thread
             out["err"] = exc
         finally:
+            t_c = time.perf_counter()
             plan.close()
+            timeline.append(("close", t_c, time.perf_counter()))
 
     chunks_out = []
     seen = [0.0, 0.0]  # planned workspace bytes and leaf area (adaptive chunking)

@@ -109,3 +109,75 @@ def test_grouped_gemm_matches_numpy(tile, seed):
         assert np.allclose(got, exp, rtol=1e-12, atol=1e-12 * max(1.0, np.abs(exp).max())), ti
         if mode == 2:
             assert abs(sumsq[ti] - np.sum(exp * exp)) <= 1e-10 * max(1.0, np.sum(exp * exp))
+
+
+@pytest.mark.parametrize("tile", [64, -64])
+def test_grouped_gemm_many_tiles(tile):
+    """Thousands of tiles (more than one per resident CTA: the persistent kernel walks
+    several tiles per CTA and wraps its stage ring many times), random terms in every
+    layout, partial coverage, empty tiles, STORE / ADD / SUMSQ epilogues; -64 runs the
+    short-K configuration of the term-formation batches."""
+    from paper_1805_08998_b200 import _lib
+
+    T = 64
+    rng = np.random.default_rng(11)
+    n_tiles = 3000
+    src = np.zeros(40_000_000)
+    pos = 0
+    terms, groups, tiles, checks = [], [], [], []
+    out = np.zeros(n_tiles * T * T + 8)
+    for ti in range(n_tiles):
+        rows = T if rng.random() < 0.7 else int(rng.integers(1, T + 1))
+        cols = T if rng.random() < 0.7 else int(rng.integers(1, T + 1))
+        exp = np.zeros((rows, cols))
+        g0 = len(groups)
+        n_groups = 0 if rng.random() < 0.03 else int(rng.integers(1, 3))
+        for _ in range(n_groups):
+            t0 = len(terms)
+            for _ in range(int(rng.integers(1, 4))):
+                k = int(rng.integers(1, 40))
+                a_kc, b_kc = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+                partial = rng.random() < 0.25
+                dr = int(rng.integers(-8, 9)) if partial else 0
+                dc = int(rng.integers(-8, 9)) if partial else 0
+                trows = rows if not partial else int(rng.integers(1, T + 8))
+                tcols = cols if not partial else int(rng.integers(1, T + 8))
+                a_off, a_ld, P, pos = _operand(rng, src, pos, trows, k, a_kc)
+                b_off, b_ld, Qt, pos = _operand(rng, src, pos, tcols, k, b_kc)
+                # tile (i, j) <- term row i + dr, col j + dc  (r_lo = row0 - dr)
+                terms.append((a_off, b_off, a_ld, b_ld, k, -dr, -dc, trows, tcols, 0, 0,
+                              a_kc, b_kc))
+                i0, i1 = max(0, -dr), min(rows, trows - dr)
+                j0, j1 = max(0, -dc), min(cols, tcols - dc)
+                if i1 > i0 and j1 > j0:
+                    exp[i0:i1, j0:j1] += P[i0 + dr:i1 + dr] @ Qt[j0 + dc:j1 + dc].T
+            groups.append((t0, len(terms)))
+        mode = int(rng.integers(0, 3))
+        out_off = ti * T * T
+        if mode == 1:
+            base = rng.standard_normal((rows, cols))
+            out[out_off:out_off + T * cols].reshape(cols, T)[:, :rows] = base.T
+            exp = exp + base
+        tiles.append((out_off, T, 0, 0, rows, cols, g0, len(groups), ti, 1, mode, (0, 0)))
+        checks.append((out_off, rows, cols, exp, mode))
+    assert pos < src.size
+    t_arr = np.array(terms, dtype=TERM)
+    l_arr = np.array(tiles, dtype=TILE)
+    g_arr = np.array(groups if groups else [(0, 0)], dtype=GROUP)
+    bufs = (_lib.f64p * NBUF)()
+    elems = np.zeros(NBUF, np.int64)
+    bufs[0] = src.ctypes.data_as(_lib.f64p)
+    elems[0] = src.size
+    bufs[1] = out.ctypes.data_as(_lib.f64p)
+    elems[1] = out.size
+    sumsq = np.zeros(n_tiles)
+    rc = _lib.lib().hx_debug_gemm(tile, t_arr.ctypes.data, len(t_arr), l_arr.ctypes.data,
+                                  len(l_arr), g_arr.ctypes.data, len(g_arr), bufs,
+                                  elems.ctypes.data_as(_lib.i64p), sumsq.ctypes.data_as(_lib.f64p),
+                                  n_tiles)
+    assert rc == 0, _lib.last_error()
+    for ti, (off, rows, cols, exp, mode) in enumerate(checks):
+        got = out[off:off + T * cols].reshape(cols, T)[:, :rows].T
+        assert np.allclose(got, exp, rtol=1e-12, atol=1e-12 * max(1.0, np.abs(exp).max())), ti
+        if mode == 2:
+            assert abs(sumsq[ti] - np.sum(exp * exp)) <= 1e-10 * max(1.0, np.sum(exp * exp))

@@ -58,8 +58,12 @@ def main():
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
     r = out.report
+    walls = []
+    for _ in range(3):
+        walls.append(hx.multiply.multiply_device(A, B, cfg, fetch=False).report.wall_s * 1e3)
     print(f"plan {r.plan_ms:.0f} dev {r.device_ms:.1f} form {r.form_ms:.1f} "
-          f"mat {r.materialize_ms:.1f} recomp {r.recompress_ms:.1f}")
+          f"mat {r.materialize_ms:.1f} recomp {r.recompress_ms:.1f} wall(3 more) "
+          f"{' '.join(f'{w:.1f}' for w in walls)} ms")
     info = out.plan_info
     print({f[0]: getattr(info, f[0]) for f in info._fields_ if f[0] != "created"})
     if "--flops" in sys.argv:
