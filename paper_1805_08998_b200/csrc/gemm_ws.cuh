@@ -85,6 +85,67 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       : "memory");
 }
 
+// Producer cursor over the tile's (group, term, k offset), reading the term and group
+// records through warp-wide windows: lane i holds record base + i (one coalesced load per
+// window), the current one is broadcast by shuffles.  The cursor of the classic kernel
+// loads each record when it reaches it, a chain of dependent L2 round trips per segment
+// that bounds how fast the producers can stage (term formation: ~4 segments per chunk).
+struct WsCursor {
+  int g, g_end, t, t_end, k0;
+  int tbase, tn;  // term window [tbase, tbase + tn)
+  int gbase, gn;  // group window
+  Term tm;        // current term (uniform over the warp)
+  Term wt;        // this lane's term of the window
+  Group wg;       // this lane's group of the window
+};
+
+__device__ __forceinline__ Term shfl_term(const Term& x, int src) {
+  static_assert(sizeof(Term) == 48, "Term layout");
+  Term y;
+  const int* xi = reinterpret_cast<const int*>(&x);
+  int* yi = reinterpret_cast<int*>(&y);
+#pragma unroll
+  for (int w = 0; w < 12; ++w) yi[w] = __shfl_sync(0xffffffffu, xi[w], src);
+  return y;
+}
+
+__device__ __forceinline__ bool ws_next_term(WsCursor& c, const Group* __restrict__ groups,
+                                             const Term* __restrict__ terms, int lane) {
+  while (true) {
+    ++c.t;
+    if (c.t < c.t_end) {
+      if (c.t < c.tbase || c.t >= c.tbase + c.tn) {
+        c.tbase = c.t;
+        c.tn = min(32, c.t_end - c.t);
+        if (lane < c.tn) c.wt = terms[c.t + lane];
+      }
+      c.tm = shfl_term(c.wt, c.t - c.tbase);
+      c.k0 = 0;
+      if (c.tm.k > 0) return true;
+      continue;
+    }
+    ++c.g;
+    if (c.g >= c.g_end) return false;
+    if (c.g >= c.gbase + c.gn) {
+      c.gbase = c.g;
+      c.gn = min(32, c.g_end - c.g);
+      if (lane < c.gn) c.wg = groups[c.g + lane];
+    }
+    const int src = c.g - c.gbase;
+    c.t = __shfl_sync(0xffffffffu, c.wg.t_begin, src) - 1;
+    c.t_end = __shfl_sync(0xffffffffu, c.wg.t_end, src);
+  }
+}
+
+__device__ __forceinline__ void ws_cursor_init(WsCursor& c, const Tile& tl) {
+  c.g = tl.g_begin - 1;
+  c.g_end = tl.g_end;
+  c.t = c.t_end = 0;
+  c.k0 = 0;
+  c.tbase = c.tn = 0;
+  c.gbase = c.gn = 0;
+}
+
 // Producer-side staging of n slots of one operand segment (layouts as stage_seg in
 // gemm.cuh), spread over the C::NPT producer threads (tid in [0, NPT)).
 template <class C>
@@ -191,7 +252,7 @@ __device__ __forceinline__ void ws_zero_slots(double* s, int kc, int a, int b, i
 // Producer: fill one stage from the cursor; returns the descriptor (all producer threads
 // compute it identically).
 template <class C>
-__device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, Cursor& cur,
+__device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, WsCursor& cur,
                                                  bool& have, const Group* __restrict__ groups,
                                                  const Term* __restrict__ terms,
                                                  const BufPtrs& bufs, const Tile& tl,
@@ -235,7 +296,7 @@ __device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, Cursor&
     d.used += n;
     ++nseg;
     cur.k0 += n;
-    if (cur.k0 >= tm.k) have = next_term(cur, groups, terms);
+    if (cur.k0 >= tm.k) have = ws_next_term(cur, groups, terms, tid & 31);
   }
   const int padded = (d.used + 3) & ~3;
   ws_zero_slots<C>(sP, d.akc, d.used, padded, tid);
@@ -246,14 +307,32 @@ __device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, Cursor&
 template <class C, int AK, int BK>
 __device__ __forceinline__ void ws_mma_t(double (&acc)[C::FR][C::FR][2], const double* sP,
                                          const double* sQ, int used, int wm, int wn,
-                                         int lane) {
+                                         int lane, unsigned amask) {
   constexpr int SA_I = AK ? C::LDK : 1, SA_K = AK ? 1 : C::LDI;
   constexpr int SB_I = BK ? C::LDK : 1, SB_K = BK ? 1 : C::LDI;
   const int ksteps = (used + 3) >> 2;
   const int r = lane >> 2, q = lane & 3;
   const double* pa = sP + (wm * C::WT + r) * SA_I + q * SA_K;
   const double* pb = sQ + (wn * C::WT + r) * SB_I + q * SB_K;
-  // fragments outside every segment multiply staged zeros (unconditional DMMA, gemm.cuh)
+  if (amask != (1u << C::FR) - 1) {
+    // partially covered row half (stacked cores: a leaf's k_l rows, 8-row aligned): only
+    // the covered 8-row fragments, row-fragment-outer so that the skip is one warp-uniform
+    // branch per fragment and chunk (B fragments re-read from shared memory per row)
+#pragma unroll
+    for (int a = 0; a < C::FR; ++a) {
+      if (!((amask >> a) & 1u)) continue;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const double af = pa[a * 8 * SA_I + ks * 4 * SA_K];
+        double bf[C::FR];
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b) bf[b] = pb[b * 8 * SB_I + ks * 4 * SB_K];
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af, bf[b]);
+      }
+    }
+    return;
+  }
+  // column fragments outside every segment multiply staged zeros (unconditional DMMA)
   for (int ks = 0; ks < ksteps; ++ks) {
     double af[C::FR], bf[C::FR];
 #pragma unroll
@@ -308,12 +387,9 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
         }
         asm volatile("bar.sync 1, %0;\n" ::"n"(C::NPT));
       }
-      Cursor cur;
-      cur.g = tl.g_begin - 1;
-      cur.g_end = tl.g_end;
-      cur.t = cur.t_end = 0;
-      cur.k0 = 0;
-      bool have = next_term(cur, groups, terms);
+      WsCursor cur;
+      ws_cursor_init(cur, tl);
+      bool have = ws_next_term(cur, groups, terms, tid & 31);
       do {
         mbar_wait(&empty[stage], phase ^ 1u);
         double* sP = smem + stage * C::STAGE;
@@ -349,11 +425,12 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
       const WsDesc d = desc[stage];
       const double* sP = smem + stage * C::STAGE;
       if (d.used > 0 && d.amask[wm] && d.bmask[wn]) {
+        const unsigned am = d.amask[wm];
         switch (d.akc * 2 + d.bkc) {
-          case 0: ws_mma_t<C, 0, 0>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane); break;
-          case 1: ws_mma_t<C, 0, 1>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane); break;
-          case 2: ws_mma_t<C, 1, 0>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane); break;
-          default: ws_mma_t<C, 1, 1>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane); break;
+          case 0: ws_mma_t<C, 0, 0>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane, am); break;
+          case 1: ws_mma_t<C, 0, 1>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane, am); break;
+          case 2: ws_mma_t<C, 1, 0>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane, am); break;
+          default: ws_mma_t<C, 1, 1>(acc, sP, sP + C::OPSZ, d.used, wm, wn, lane, am); break;
         }
       }
       __syncwarp();

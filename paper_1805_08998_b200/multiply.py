@@ -634,8 +634,8 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
         t0 = time.perf_counter()
         # deferred: the per-batch factor work lists are filled inside hx_product while the
         # device runs the previous batch
-        p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile,
-                      flags=_lib.Plan.DEFER | iflags)
+        defer = 0 if os.environ.get("HX_PLAN_NODEFER") else _lib.Plan.DEFER
+        p = _lib.Plan(ta, dir_a, dir_a if same else dir_b, mask, tile, flags=defer | iflags)
         t1 = time.perf_counter()
         plan_ms[0] += (t1 - t0) * 1e3
         timeline.append(("plan", t0, t1))

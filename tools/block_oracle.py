@@ -52,6 +52,7 @@ def main():
     ap.add_argument("cfg", type=int)
     ap.add_argument("--per-class", type=int, default=8)
     ap.add_argument("--max-size", type=int, default=0, help="skip far sizes above (0: none)")
+    ap.add_argument("--min-size", type=int, default=0, help="skip far sizes below")
     ap.add_argument("--dense-max", type=int, default=4096,
                     help="blocks up to this: full SVD of the densified S(leaf)")
     ap.add_argument("--values-max", type=int, default=8192,
@@ -80,7 +81,7 @@ def main():
     near = np.flatnonzero(bct.kind_code == 2)
     sample = []
     for m in np.unique(size[far]):
-        if a.max_size and m > a.max_size:
+        if (a.max_size and m > a.max_size) or m < a.min_size:
             continue
         ids = far[size[far] == m]
         pick = rng.choice(ids, size=min(a.per_class, len(ids)), replace=False)
