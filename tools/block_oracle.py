@@ -47,6 +47,39 @@ def lr_rel_diff(u1, v1, u2, v2):
     return float(num / max(den, 1e-300))
 
 
+def certify(s, U, V, tol, batch):
+    """Exact epsilon-rank bracket of a block too large for a dense SVD, from the GPU's
+    factors: S is applied to the identity in column batches (exact densification, never
+    held whole) to measure ||S||_F and the GPU residual d = ||S - U V^T||_F exactly.
+    Upper bound: d <= tol ||S|| means the best rank-r error is <= tol ||S||, so the
+    epsilon-rank is <= r.  Lower bound (Weyl): sigma_i(S) >= sigma_i(U V^T) - d, so the
+    tail ||s[j:]|| >= sqrt(sum_{i >= j} (sigma_i(U V^T) - d)_+^2); any j whose lower bound
+    exceeds tol ||S|| is too small a rank."""
+    m, n = s.shape
+    fro2 = 0.0
+    res2 = 0.0
+    for j0 in range(0, n, batch):
+        j1 = min(n, j0 + batch)
+        E = np.zeros((n, j1 - j0))
+        E[np.arange(j0, j1), np.arange(j1 - j0)] = 1.0
+        blk = s.mat(E)
+        fro2 += float(np.sum(blk * blk))
+        blk -= U @ V[j0:j1].T
+        res2 += float(np.sum(blk * blk))
+    nrm = np.sqrt(fro2)
+    d = np.sqrt(res2)
+    r = U.shape[1]
+    hi = r if d <= tol * nrm else None
+    sv = np.linalg.svd(np.linalg.qr(U)[1] @ np.linalg.qr(V)[1].T, compute_uv=False)
+    low = np.maximum(sv - d, 0.0)
+    tails = np.sqrt(np.cumsum((low ** 2)[::-1])[::-1])
+    lo = 0
+    for j in range(r):
+        if tails[j] > tol * nrm:
+            lo = j + 1
+    return lo, (hi if hi is not None else r + 10 ** 6), d / nrm
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("cfg", type=int)
@@ -59,6 +92,10 @@ def main():
                     help="blocks up to this: singular values of the densified S(leaf) and "
                          "the GPU block's own residual; larger: matrix-free Lanczos")
     ap.add_argument("--tag", default="dense-svd")
+    ap.add_argument("--certify", action="store_true",
+                    help="above --values-max: exact rank bracket from the GPU factors and the "
+                         "exactly measured residual, besides the Lanczos comparison")
+    ap.add_argument("--batch", type=int, default=2048, help="columns per application of S")
     ap.add_argument("--near", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1)
     a = ap.parse_args()
@@ -111,6 +148,20 @@ def main():
                   f"{time.time() - tl:.0f} s), gpu residual {e_gpu:.2e}, best {e_best:.2e}, "
                   f"rel diff <= {d:.2e}", flush=True)
             del dense
+            continue
+        if bct.kind_code[b] == 1 and min(m, n) > a.values_max and a.certify:
+            tl = time.time()
+            lo_r, hi_r, e_gpu = certify(s, q.left, q.right, tol, a.batch)
+            ref = O.lanczos_o(s, O.Eps(tol), seed=O.block_seed(0, b))
+            dl = lr_rel_diff(q.left, q.right, ref.left, ref.right)
+            off = max(q.rank - lo_r, hi_r - q.rank)
+            worst_rank = max(worst_rank, off)
+            worst_far = max(worst_far, 2 * e_gpu)
+            print(f"  far  {b:8d} {m}x{n}: rank gpu {q.rank}, exact epsilon-rank in "
+                  f"[{lo_r}, {hi_r}] (certificate: S applied to the identity in column "
+                  f"batches), gpu residual {e_gpu:.2e} (rel diff to the best <= "
+                  f"{2 * e_gpu:.2e}); reference bilanczos rank {ref.rank}, diff {dl:.2e} "
+                  f"({time.time() - tl:.0f} s)", flush=True)
             continue
         if bct.kind_code[b] == 1 and min(m, n) > a.values_max:
             tl = time.time()
