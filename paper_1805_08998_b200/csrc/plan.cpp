@@ -585,43 +585,70 @@ struct Builder {
     ws_near_total = b_near[no];
     P.n_sumsq = int32_t(b_sumsq[no]);
     lap("merge alloc");
-#pragma omp parallel for schedule(dynamic, 1)
-    for (int64_t i = 0; i < int64_t(no); ++i) {
+    // balanced blocks of <= 64k elements over every output array: a few tasks (the top
+    // part, large subtrees) hold most of the records, so a loop over tasks alone leaves
+    // most threads idle behind them
+    struct Blk {
+      int32_t task, what;  // what: 0 terms, 1 recs, 2 tile groups, 3 leaves (+ tiles)
+      int64_t a, e;
+    };
+    std::vector<Blk> blks;
+    constexpr int64_t BS = int64_t(1) << 16;
+    for (size_t i = 0; i < no; ++i) {
       const Out& o = outs[i];
-      std::copy(o.terms.begin(), o.terms.end(), P.mat_terms.begin() + b_terms[i]);
-      for (size_t r = 0; r < o.recs.size(); ++r) {
-        TRec x = o.recs[r];
-        x.mat += int32_t(b_terms[i]);
-        recs[size_t(b_recs[i]) + r] = x;
+      const int64_t len[4] = {int64_t(o.terms.size()), int64_t(o.recs.size()),
+                              int64_t(o.tile_groups.size()), int64_t(o.leaves.size())};
+      for (int w = 0; w < 4; ++w) {
+        const int64_t bs = w == 3 ? BS / 16 : BS;
+        for (int64_t a = 0; a < len[w]; a += bs)
+          blks.push_back(Blk{int32_t(i), w, a, std::min(len[w], a + bs)});
       }
-      for (size_t g = 0; g < o.tile_groups.size(); ++g) {
-        const GRef ref = o.tile_groups[g];
-        Group gr = outs[ref.first].groups[ref.second];
-        gr.t_begin += int32_t(b_terms[ref.first]);
-        gr.t_end += int32_t(b_terms[ref.first]);
-        P.mat_groups[size_t(b_tg[i]) + g] = gr;
-      }
-      for (size_t l = 0; l < o.leaves.size(); ++l) {
-        hx::OutLeaf L = o.leaves[l];
-        const int64_t wb = L.kind == 1 ? b_far[i] : b_near[i];
-        L.ws_off += wb;
-        for (int32_t k = L.tile_begin; k < L.tile_end; ++k) {
-          Tile tl = o.tiles[k];
-          tl.out_off += wb;
-          tl.g_begin += int32_t(b_tg[i]);
-          tl.g_end += int32_t(b_tg[i]);
-          tl.aux += int32_t(b_sumsq[i]);
-          P.mat_tiles[size_t(b_tiles[i]) + k] = tl;
+    }
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t bi = 0; bi < int64_t(blks.size()); ++bi) {
+      const Blk bk = blks[size_t(bi)];
+      const size_t i = size_t(bk.task);
+      const Out& o = outs[i];
+      if (bk.what == 0) {
+        std::copy(o.terms.begin() + bk.a, o.terms.begin() + bk.e,
+                  P.mat_terms.begin() + b_terms[i] + bk.a);
+      } else if (bk.what == 1) {
+        for (int64_t r = bk.a; r < bk.e; ++r) {
+          TRec x = o.recs[size_t(r)];
+          x.mat += int32_t(b_terms[i]);
+          recs[size_t(b_recs[i] + r)] = x;
         }
-        L.tile_begin += int32_t(b_tiles[i]);
-        L.tile_end += int32_t(b_tiles[i]);
-        L.sumsq_begin += int32_t(b_sumsq[i]);
-        L.sumsq_end += int32_t(b_sumsq[i]);
-        if (L.implicit) {
-          L.g_begin += int32_t(b_tg[i]);
-          L.g_end += int32_t(b_tg[i]);
+      } else if (bk.what == 2) {
+        for (int64_t g = bk.a; g < bk.e; ++g) {
+          const GRef ref = o.tile_groups[size_t(g)];
+          Group gr = outs[ref.first].groups[ref.second];
+          gr.t_begin += int32_t(b_terms[ref.first]);
+          gr.t_end += int32_t(b_terms[ref.first]);
+          P.mat_groups[size_t(b_tg[i] + g)] = gr;
         }
-        P.leaves[size_t(b_leaves[i]) + l] = L;
+      } else {
+        for (int64_t l = bk.a; l < bk.e; ++l) {
+          hx::OutLeaf L = o.leaves[size_t(l)];
+          const int64_t wb = L.kind == 1 ? b_far[i] : b_near[i];
+          L.ws_off += wb;
+          for (int32_t k = L.tile_begin; k < L.tile_end; ++k) {
+            Tile tl = o.tiles[k];
+            tl.out_off += wb;
+            tl.g_begin += int32_t(b_tg[i]);
+            tl.g_end += int32_t(b_tg[i]);
+            tl.aux += int32_t(b_sumsq[i]);
+            P.mat_tiles[size_t(b_tiles[i]) + k] = tl;
+          }
+          L.tile_begin += int32_t(b_tiles[i]);
+          L.tile_end += int32_t(b_tiles[i]);
+          L.sumsq_begin += int32_t(b_sumsq[i]);
+          L.sumsq_end += int32_t(b_sumsq[i]);
+          if (L.implicit) {
+            L.g_begin += int32_t(b_tg[i]);
+            L.g_end += int32_t(b_tg[i]);
+          }
+          P.leaves[size_t(b_leaves[i] + l)] = L;
+        }
       }
     }
     lap("merge copy");
@@ -1077,11 +1104,16 @@ struct Builder {
           P.fac_groups[size_t(g.o_fg + band)] =
               Group{int32_t(g.o_fm + pos[size_t(band)]), int32_t(g.o_fm + pos[size_t(band) + 1])};
         }
+        // low-rank leaves first, then dense ones: on the B side their staging layouts
+        // differ (U_l vs D_l^T), and a chunk of the GEMM holds one layout, so interleaving
+        // them in DFS order would cut the band's K stream into short chunks
+        for (int pass = 0; pass < 2; ++pass)
         for (int i = 0; i < nl; ++i) {
           const int l = g.leaves[size_t(i)];
           const int rl = g.side == 0 ? t.sigma[l] : t.tau[l];  // middle-cluster part
           const int ol = g.side == 0 ? t.tau[l] : t.sigma[l];  // output rows
           const bool lr = isF(opX, l);
+          if (lr != (pass == 0)) continue;
           const int kl = lr ? opX.rank[l] : 0;
           if (lr && kl == 0) continue;
           const int64_t roff = lo(rl) - lo(g.rho);

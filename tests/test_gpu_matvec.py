@@ -55,3 +55,30 @@ def test_product_error_estimate(golden):
     # 32 Gaussian probes: the estimate is within a factor ~1.5 of the true ratio
     assert err / 1.6 <= est <= err * 1.6, (est, err)
     assert abs(cnorm - np.linalg.norm(exact)) <= 0.35 * np.linalg.norm(exact)
+
+
+def test_estimate_product_error_matches_reference_algorithm(golden):
+    """estimate_product_error (multiply.py:266-294) on the GPU against the same algorithm
+    on the dense matrices (same seed, same block, same iterations): equal to rounding,
+    and a lower bound of the exact ||C - A B||_F that captures most of it."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200.matvec import estimate_product_error
+
+    g = golden("cfg1.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "cfg1.npz")
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("aca"), policy=hx.EpsRank(tol))
+    C = hx.hmult_new(A, B, cfg)
+    da, db, dc = oa.to_dense(), ob.to_dense(), hx.to_dense(C)
+    est = estimate_product_error(A, B, C, iters=10, block_size=100, seed=0)
+    # the reference algorithm on dense operators
+    n = dc.shape[0]
+    rng = np.random.default_rng(0)
+    R = dc - da @ db
+    x = np.linalg.qr(rng.standard_normal((n, 100)))[0]
+    for _ in range(10):
+        y = np.linalg.qr(R @ x)[0]
+        x = np.linalg.qr(R.T @ y)[0]
+    ref = float(np.sqrt(np.sum(np.linalg.svd(R @ x, compute_uv=False) ** 2)))
+    exact = np.linalg.norm(R)
+    assert abs(est - ref) <= 1e-6 * ref, (est, ref)
+    assert 0 < est <= exact * (1 + 1e-9), (est, exact)

@@ -44,6 +44,7 @@ def main():
     ap.add_argument("cfg", type=int)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--fill", action="store_true", help="also fill every batch")
+    ap.add_argument("--eager", action="store_true", help="fill the batches in the plan call")
     ap.add_argument("--sizes", action="store_true", help="materialization flops by leaf size")
     ap.add_argument("--chunk", type=int, default=-1, help="plan only this chunk of 3")
     a = ap.parse_args()
@@ -60,7 +61,7 @@ def main():
         mask = multiply.group_mask(bct, groups[a.chunk])
     for _ in range(a.reps):
         t0 = time.perf_counter()
-        p = _lib.Plan(ta, d, d, mask, 64, flags=_lib.Plan.DEFER)
+        p = _lib.Plan(ta, d, d, mask, 64, flags=0 if a.eager else _lib.Plan.DEFER)
         t1 = time.perf_counter()
         msg = f"plan {1e3 * (t1 - t0):.1f} ms"
         if a.fill:

@@ -5,7 +5,11 @@ device, so its time is what that rank would take on its own B200 (no rank waits 
 another).  The predicted N-GPU step is the max over ranks; speed-up = t(1) / max.
 The NCCL operand broadcast is not part of the product step (it happens once, at setup).
 
-usage: python tools/rank_sim.py CFG [--worlds 2,4,8] [--steps 3] [--leafwise]
+usage: python tools/rank_sim.py CFG [--worlds 2,4,8] [--steps 3] [--leafwise] [--tag aca]
+
+A rank's share of the host (16 cores / 8 ranks) is simulated by running the ranks under
+`taskset -c 0-1` with OMP_NUM_THREADS=2 (--skip-full), and world 1 separately with the
+whole host.
 """
 import argparse
 import sys
@@ -43,10 +47,11 @@ def main():
     ap.add_argument("--leafcost", action="store_true", help="units priced by leaf costs only")
     ap.add_argument("--ranks", default="", help="only these ranks (comma list)")
     ap.add_argument("--skip-full", action="store_true")
+    ap.add_argument("--tag", default="dense-svd")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     bct, A, B = configs.build_operands(c)
-    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind("dense-svd"), policy=hx.EpsRank(c["tol"]))
+    cfg = hx.MultiplyConfig(compressor=hx.CompressorKind(a.tag), policy=hx.EpsRank(c["tol"]))
     _, dA = multiply.operand_directory(A)
     _, dB = multiply.operand_directory(B)
     full = _lib.Plan(hmatrix.tree_arrays(bct), dA, dA if B is A else dB, None,
