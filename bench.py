@@ -516,7 +516,10 @@ def bench_ours(args, rank, world, local):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e = {"value": F_tot / float(tt.item()) / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(tt.item()) * 1e3}
+               "ms_per_step": float(tt.item()) * 1e3,
+               "note": "every step uploads the host operand pool (packed and page-locked "
+                       "once at setup, like the reference's assembly) and downloads every "
+                       "output block into the HMatrix"}
         if world == 1:
             # relative error of the product against A*B, through the GPU H-matrix x block
             # products: the reference's estimator (two-sided block subspace iteration on

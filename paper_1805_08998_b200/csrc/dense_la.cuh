@@ -44,8 +44,34 @@ struct SelJob {
   int l;               // sketch width (number of singular values)
   int mu;              // min(m, n)
   int exact;           // 1: the sketch spans the whole block (no unsampled tail)
-  int resid;           // 1: *fro2 is ||T - Q Q^T T||_F^2 measured directly
+  int resid;           // 1: *fro2 is ||T - Q Q^T T||_F^2 measured directly; 2: estimated
+                       // from Gaussian probes (implicit route)
 };
+
+// epsilon-rank (select_rank, lowrank.py:75-90) of singular values sig[0..l) plus an
+// unsampled tail mass `extra` (squared): l + 1 if even dropping the unsampled mass fails.
+__device__ __forceinline__ int eps_rank_tail(const double* sig, int l, double extra,
+                                             double eps) {
+  // tails from the back: tail[r] = sqrt(extra + sum_{i>=r} s_i^2), summed smallest first
+  // like the reference's reversed cumsum; total = tail[0]
+  double tot2 = extra;
+  for (int i = l - 1; i >= 0; --i) tot2 += sig[i] * sig[i];
+  const double thr = eps * sqrt(tot2);
+  int r = l + 1;
+  if (sqrt(extra) <= thr) r = l;
+  double acc = extra;
+  for (int i = l - 1; i >= 0; --i) {
+    acc += sig[i] * sig[i];
+    if (sqrt(acc) <= thr) r = i;
+  }
+  return r;
+}
+
+// A probe estimate of the unsampled tail (8 Gaussian probes: a scaled chi-square with 8
+// degrees of freedom, 95 % of it within [0.27, 1.94] of the truth) decides the rank only if
+// every value in [EST_LO, EST_HI] x the estimate gives the same rank; otherwise the sketch
+// is widened, which moves the near-threshold singular values into the sampled part.
+constexpr double EST_LO = 0.25, EST_HI = 2.5;
 
 struct SmallJob {
   const double* P;   // rows x q (ld_p) or nullptr for identity (out = C)
@@ -211,19 +237,10 @@ __device__ __forceinline__ void select_one(const SelJob& jb, int policy, double 
   double s2 = 0.0;
   for (int i = 0; i < l; ++i) s2 += jb.sig[i] * jb.sig[i];
   double extra = jb.exact ? 0.0 : (jb.resid ? fmax(0.0, *jb.fro2) : fmax(0.0, *jb.fro2 - s2));
-  // tails from the back: tail[r] = sqrt(extra + sum_{i>=r} s_i^2), summed smallest first
-  // like the reference's reversed cumsum; total = tail[0]
-  double tot2 = extra;
-  for (int i = l - 1; i >= 0; --i) tot2 += jb.sig[i] * jb.sig[i];
-  const double total = sqrt(tot2);
-  const double thr = eps * total;
-  int r = l + 1;  // l + 1: even dropping only the unsampled mass fails
-  if (sqrt(extra) <= thr) r = l;
-  double acc = extra;
-  for (int i = l - 1; i >= 0; --i) {
-    acc += jb.sig[i] * jb.sig[i];
-    if (sqrt(acc) <= thr) r = i;
-  }
+  int r = eps_rank_tail(jb.sig, l, extra, eps);
+  const bool unsure = jb.resid == 2 && !jb.exact && extra > 0.0 &&
+                      eps_rank_tail(jb.sig, l, EST_LO * extra, eps) !=
+                          eps_rank_tail(jb.sig, l, EST_HI * extra, eps);
   if (randomized_rule) {
     double acc2 = 0.0;
     int hits = 0, rr = l + 1;
@@ -247,7 +264,7 @@ __device__ __forceinline__ void select_one(const SelJob& jb, int policy, double 
     rank_out = min(r, l);
     retry_out = 0;
   } else {
-    retry_out = (r > l - oversample && l < jb.mu) ? 1 : 0;
+    retry_out = ((r > l - oversample || unsure) && l < jb.mu) ? 1 : 0;
     rank_out = min(r, l);
   }
 }

@@ -547,6 +547,10 @@ struct hx_ctx {
   // of the same product (hx_ctx_reset_hints between products), for the same policy
   int rank_hint[32];
   int8_t class_retry[32];  // a block of the class needed a wider sketch (retry round)
+  // matrix-free compressors: the most columns a block of the class produced (before the
+  // final truncation) in earlier chunks; the next chunks size their column budget from it
+  // instead of rerunning capped blocks with four times the budget
+  int iter_hint[32];
   double hint_key[4] = {-1, -1, -1, -1};
   int64_t omega_rows = 0;
   int omega_cols = 0;
@@ -1073,8 +1077,11 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
   std::vector<int> kcap(nf);
   for (int i = 0; i < nf; ++i) {
     const FarBlock& f = fb[size_t(i)];
+    int k0 = iter_kcap0(f.mu);
+    const int h = c->iter_hint[ilog2(f.mu)];
+    if (h >= 0) k0 = std::max(k0, (h + 8 + 7) & ~7);
     kcap[size_t(i)] = cfg->policy == 1 ? std::min(f.mu, std::max(cfg->k_max, 1))
-                                       : std::min(f.mu, iter_kcap0(f.mu));
+                                       : std::min(f.mu, k0);
   }
   auto a16 = [](int64_t x) { return (x + 15) & ~int64_t(15); };
   std::vector<IterOut> outs(static_cast<size_t>(nf));
@@ -1182,7 +1189,11 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     if (next.empty()) break;
     active.swap(next);
   }
-  for (int i = 0; i < nf; ++i) matvecs += outs[size_t(i)].matvecs;
+  for (int i = 0; i < nf; ++i) {
+    matvecs += outs[size_t(i)].matvecs;
+    int& h = c->iter_hint[ilog2(fb[size_t(i)].mu)];
+    h = std::max(h, outs[size_t(i)].k);
+  }
   // ---- exact recompressions: ACA's truncate(eps / 2) (compressors.py:245-246,
   // lowrank.py:93-113) and the Lanczos core SVD (:359-365); the sketch route's kernels
   int64_t psz = 0;
@@ -1393,6 +1404,7 @@ extern "C" int hx_ctx_reset_hints(hx_ctx* c) {
   if (!c) return fail(HX_EINVAL, "null context");
   std::fill(c->rank_hint, c->rank_hint + 32, -1);
   std::fill(c->class_retry, c->class_retry + 32, int8_t(0));
+  std::fill(c->iter_hint, c->iter_hint + 32, -1);
   return HX_OK;
 }
 
@@ -1515,6 +1527,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         std::copy(key, key + 4, c->hint_key);
         std::fill(c->rank_hint, c->rank_hint + 32, -1);
         std::fill(c->class_retry, c->class_retry + 32, int8_t(0));
+        std::fill(c->iter_hint, c->iter_hint + 32, -1);
       }
     }
     static const bool use_hints = std::getenv("HX_NO_RANK_HINT") == nullptr;
@@ -2197,7 +2210,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         FarBlock& f = fb[active[a]];
         const int exact = (f.dense || (!f.implicit && f.l == f.mu)) ? 1 : 0;
         if (f.implicit)
-          sj.push_back(SelJob{f.sig, c->est.p + a, f.l, f.mu, 0, 1});
+          sj.push_back(SelJob{f.sig, c->est.p + a, f.l, f.mu, 0, 2});
         else if (explicit_tail && !exact)
           sj.push_back(SelJob{f.sig, c->resid.p + a, f.l, f.mu, 0, 1});
         else

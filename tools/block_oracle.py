@@ -96,6 +96,7 @@ def main():
                     help="above --values-max: exact rank bracket from the GPU factors and the "
                          "exactly measured residual, besides the Lanczos comparison")
     ap.add_argument("--batch", type=int, default=2048, help="columns per application of S")
+    ap.add_argument("--blocks", default="", help="check exactly these block ids (comma list)")
     ap.add_argument("--near", type=int, default=8)
     ap.add_argument("--seed", type=int, default=1)
     a = ap.parse_args()
@@ -124,6 +125,8 @@ def main():
         pick = rng.choice(ids, size=min(a.per_class, len(ids)), replace=False)
         sample += [int(b) for b in pick]
     sample += [int(b) for b in rng.choice(near, size=min(a.near, len(near)), replace=False)]
+    if a.blocks:
+        sample = [int(x) for x in a.blocks.split(",")]
     worst_rank, worst_far, worst_near = 0, 0.0, 0.0
     t1 = time.time()
     for b in sample:
