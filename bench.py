@@ -483,56 +483,6 @@ def bench_ours(args, rank, world, local):
     F_tot, B_tot = ph["F"], ph["B"]
     value = F_tot / (ms_max * 1e-3) / 1e9
 
-    # e2e through the public API with host operands
-    e2e = None
-    rel_err = None
-    if not args.no_e2e:
-        pa, _ = multiply._host_directory(A)
-        pb = pa if B is A else multiply._host_directory(B)[0]
-        h2d = 8 * (pa.size + (0 if B is A else pb.size))
-        for _ in range(2):  # warm-up: page-locked result buffers enter the reuse cache
-            del_me = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
-                                              device_operands=False)
-            del del_me
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        d2h = 0
-        Ce = None
-        for _ in range(args.steps):
-            # the previous step's result is released first (as a caller replacing it
-            # would), so its page-locked buffers are reused instead of pinning new ones
-            Ce = None
-            Ce = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
-                                          device_operands=False)
-            # bytes of the result buffers copied back (every far factor and near block);
-            # the HMatrix builds its leaf views over them on access
-            d2h = 8 * int(Ce.report.out_elems)
-        torch.cuda.synchronize()
-        te = (time.perf_counter() - t0) / args.steps
-        tt = torch.tensor([te], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e = {"value": F_tot / float(tt.item()) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "ms_per_step": float(tt.item()) * 1e3,
-               "note": "every step uploads the host operand pool (packed and page-locked "
-                       "once at setup, like the reference's assembly) and downloads every "
-                       "output block into the HMatrix"}
-        if world == 1:
-            # relative error of the product against A*B, through the GPU H-matrix x block
-            # products: the reference's estimator (two-sided block subspace iteration on
-            # C - A B, multiply.py:266-294) over ||C||_F, and an unbiased probe estimate
-            from paper_1805_08998_b200 import matvec
-            t_err = time.perf_counter()
-            est = matvec.estimate_product_error(A, B, Ce, device=local)
-            fro = hx.frobenius_norm(Ce)
-            probe, _ = matvec.product_error(Ce, A, B, probes=16, device=local)
-            rel_err = {"value": est / fro, "estimator": "estimate_product_error (10 "
-                       "iterations, block 100) / ||C||_F", "probe16": probe,
-                       "tol": c["tol"], "seconds": time.perf_counter() - t_err}
-
     # roofline of the dominant kernel: the materialization launch of grouped_gemm_kernel
     # (one launch per step, FP64 DMMA-bound); algorithmic flops = exact useful products
     # sum over tiles and terms of 2 * rows * cols * k (no padding), from the plan
@@ -581,7 +531,7 @@ def bench_ours(args, rank, world, local):
     t_roof = roofline_time(ph, FP64_DMMA_PEAK_TFLOPS, hbm)
     roofline["whole_product"] = {
         "t_roof_ms": t_roof * 1e3, "frac": t_roof / (ms_max * 1e-3),
-        "frac_e2e": (t_roof / (e2e["ms_per_step"] * 1e-3)) if e2e else None,
+        "frac_e2e": None,
         "phases": {k: {"gflop": ph[k]["F"] / 1e9, "gbytes": ph[k]["B"] / 1e9,
                        "t_roof_ms": 1e3 * max(ph[k]["F"] / (FP64_DMMA_PEAK_TFLOPS * 1e12),
                                               ph[k]["B"] / (hbm * 1e9))}
@@ -611,6 +561,66 @@ def bench_ours(args, rank, world, local):
         alt = {"compressor": args.alt_tag, "ms_per_step": float(ta_.item()),
                "value": (pa_["F"] / (float(ta_.item()) * 1e-3) / 1e9) if pa_ else None,
                "max_far_rank": Ca.report.max_far_rank}
+    # relative error of the product against A*B, through the GPU H-matrix x block
+    # products: the reference's estimator (two-sided block subspace iteration on C - A B,
+    # multiply.py:266-294) over ||C||_F, and an unbiased probe estimate
+    rel_err = None
+    if world == 1 and not args.no_e2e:
+        from paper_1805_08998_b200 import matvec
+        t_err = time.perf_counter()
+        Cr = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask)
+        est = matvec.estimate_product_error(A, B, Cr, device=local)
+        fro = hx.frobenius_norm(Cr)
+        probe, _ = matvec.product_error(Cr, A, B, probes=16, device=local)
+        rel_err = {"value": est / fro, "estimator": "estimate_product_error (10 "
+                   "iterations, block 100) / ||C||_F", "probe16": probe,
+                   "tol": c["tol"], "seconds": time.perf_counter() - t_err}
+        del Cr
+
+    # e2e through the public API with host operands (last GPU phase: the device-resident
+    # pools are released first, the uploads need their room on the large configs)
+    e2e = None
+    if not args.no_e2e:
+        pa, _ = multiply._host_directory(A)
+        pb = pa if B is A else multiply._host_directory(B)[0]
+        h2d = 8 * (pa.size + (0 if B is A else pb.size))
+        for H in (A, B):
+            for name in ("_hx_pool", "_hx_device", "_hx_keep"):
+                H.__dict__.pop(name, None)
+        torch.cuda.empty_cache()
+        for _ in range(2):  # warm-up: page-locked result buffers enter the reuse cache
+            del_me = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
+                                              device_operands=False)
+            del del_me
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        Ce = None
+        for _ in range(args.steps):
+            # the previous step's result is released first (as a caller replacing it
+            # would), so its page-locked buffers are reused instead of pinning new ones
+            Ce = None
+            Ce = multiply.multiply_device(A, B, cfg, device=local, leaf_mask=mask,
+                                          device_operands=False)
+            # bytes of the result buffers copied back (every far factor and near block);
+            # the HMatrix builds its leaf views over them on access
+            d2h = 8 * int(Ce.report.out_elems)
+        torch.cuda.synchronize()
+        te = (time.perf_counter() - t0) / args.steps
+        tt = torch.tensor([te], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e = {"value": F_tot / float(tt.item()) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": float(tt.item()) * 1e3,
+               "note": "every step uploads the host operand pool (packed and page-locked "
+                       "once at setup, like the reference's assembly) and downloads every "
+                       "output block into the HMatrix"}
+        del Ce
+        roofline["whole_product"]["frac_e2e"] = t_roof / (e2e["ms_per_step"] * 1e-3)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

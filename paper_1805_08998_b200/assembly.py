@@ -61,9 +61,11 @@ class _LazyLeaves(LeafDict):
             return
         self._filled = True
         h = self._owner
-        pool = h._hx_pool.download()
-        h._hx_packed = (pool, h._hx_packed[1])
-        dict.update(self, unpack_leaves(h.bct, pool, h._hx_packed[1]))
+        pool, d = h._hx_packed
+        if pool is None:  # still only on the device: one download
+            pool = h._hx_pool.download()
+            h._hx_packed = (pool, d)
+        dict.update(self, unpack_leaves(h.bct, pool, d))
 
     def __contains__(self, key):
         self._fill()
