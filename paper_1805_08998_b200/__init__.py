@@ -14,7 +14,7 @@ from .compressors import CompressorKind
 from .hmatrix import (HMatrix, frobenius_norm, load_hmatrix, save_hmatrix, to_dense,
                       tree_fingerprint)
 from .lowrank import EpsRank, FixedRank, LowRank, select_rank, zero_lowrank
-from .multiply import MultiplyConfig, MultReport, hmult_new
+from .multiply import MultiplyConfig, MultReport, hmult_new, hmult_traditional
 from .assembly import KERNELS, assemble_hmatrix
 
 __version__ = "0.1.0"

@@ -605,13 +605,16 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
     static const bool short2 = std::getenv("HX_WS_SHORT2") != nullptr;
     static const bool npw4 = std::getenv("HX_WS_NPW") && std::atoi(std::getenv("HX_WS_NPW")) == 4;
     if (!grid_s) {
+      // HX_WS_RESERVE: SMs left free of the persistent GEMM CTAs (for the latency-bound
+      // recompression of a concurrent chunk on another context)
+      static const int reserve = std::getenv("HX_WS_RESERVE") ? std::atoi(std::getenv("HX_WS_RESERVE")) : 0;
       auto grid_of = [](auto kern, int threads, int smem) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         int dev = 0, sms = 0, b = 0;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem));
-        return std::max(1, b) * sms;
+        return std::max(1, b) * std::max(1, sms - reserve);
       };
       grid_s4 = grid_of(grouped_gemm_ws_kernel<Ws64s4>, Ws64s4::THREADS, Ws64s4::SMEM);
       grid_l4 = grid_of(grouped_gemm_ws_kernel<Ws64x4>, Ws64x4::THREADS, Ws64x4::SMEM);
@@ -624,6 +627,7 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
       int dev = 0, sms = 0, bs = 0, bl = 0;
       CK(cudaGetDevice(&dev));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+      sms = std::max(1, sms - reserve);
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bs, grouped_gemm_ws_kernel<Ws64s>,
                                                        Ws64s::THREADS, Ws64s::SMEM));
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, grouped_gemm_ws_kernel<Ws64>,

@@ -843,3 +843,15 @@ def hmult_new(h, k, cfg, devices=None):
         from .distributed import multiply_devices
         return multiply_devices(h, k, cfg, devices)
     return multiply_device(h, k, cfg, device=int(devices[0]))
+
+
+def hmult_traditional(h, k, cfg):
+    """The reference's convert-then-truncate product (``multiply.py:259-263``): same config
+    check; the GPU build does not implement it and says so instead of
+    running the new-mode product under the traditional name."""
+    if cfg.mode != "traditional":
+        raise ValueError("config mode must be 'traditional'")
+    if h.bct is not k.bct:
+        raise ValueError("factors must live on the same block-cluster tree")
+    raise NotImplementedError("hmult_traditional (per-pair conversion + fast_truncate_sum) "
+                              "is not built in the B200 product; use hmult_new")

@@ -76,6 +76,21 @@ def test_hmult_new_rejects_other_modes_and_trees():
         hx.hmult_new(h1, h2, cfg)
 
 
+def test_hmult_traditional_checks_then_reports_missing():
+    """multiply.py:259-263's config check; the traditional product itself is not built."""
+    import paper_1805_08998_b200 as hx
+
+    rng = np.random.default_rng(0)
+    pts = rng.uniform(0, 1, (64, 2))
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, 16), 0.8)
+    h = hx.HMatrix(bct, {})
+    with pytest.raises(ValueError, match="config mode must be 'traditional'"):
+        hx.hmult_traditional(h, h, hx.MultiplyConfig(policy=hx.EpsRank(1e-6)))
+    with pytest.raises(NotImplementedError):
+        hx.hmult_traditional(h, h, hx.MultiplyConfig(mode="traditional",
+                                                     policy=hx.EpsRank(1e-6)))
+
+
 def test_tiny_eps_warns_and_clamps():
     """compressors.py:144-149: eps <= machine epsilon -> UserWarning, clamp to 1e-15."""
     from paper_1805_08998_b200.compressors import EPS_FLOOR, clamp_eps
