@@ -419,6 +419,7 @@ def bench_ours(args, rank, world, local):
     B = A if c["kb"] is None else operand(c["kb"])
     _, dA = multiply.operand_directory(A)
     _, dB = multiply.operand_directory(B)
+    pool_gb = 8 * sum(H._hx_device[2] for H in ({id(A): A, id(B): B}.values())) / 1e9
     mask = None
     if world > 1:
         # the partition is priced once (measured planning times) on rank 0 and shipped
@@ -515,7 +516,7 @@ def bench_ours(args, rank, world, local):
     roofline = {"bound": "tensor", "achieved": mat_tflops, "peak": FP64_DMMA_PEAK_TFLOPS,
                 "unit": "TFLOP/s", "frac": mat_tflops / FP64_DMMA_PEAK_TFLOPS,
                 "traffic": traffic,
-                "kernel": "grouped_gemm_kernel<Gemm64> materialization launch",
+                "kernel": "grouped_gemm_ws_kernel<Ws64> materialization launches (per product)",
                 "algorithmic_flops_per_launch": mma[5],
                 "issued_flops_per_launch": mma[2],
                 "peak_source": "FP64 DMMA measured on this pool's B200 (tools/fp64_peak.cu, "
@@ -637,8 +638,7 @@ def bench_ours(args, rank, world, local):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded BASELINE point cloud, GPU ACA-assembled operands)",
             "config": {"workload": configs.NAMES[args.config], "compressor": args.tag,
-                       "l2": "inputs larger than L2 (operand pools "
-                             f"{8 * A._hx_device[2] / 1e9:.2f} GB)",
+                       "l2": f"inputs larger than L2 (operand pools {pool_gb:.2f} GB)",
                        "parallelism": f"output-subtree partition x{world}"},
             "canonical_gflop": F_tot / 1e9, "canonical_gbytes": B_tot / 1e9,
             "phases_ms": iso,
