@@ -974,6 +974,166 @@ def hmult_new_o(A: HMatO, B: HMatO, policy, tag="dense-svd", q=1, seed=0, log=No
     return out
 
 
+# ------------------------------------------------------------- traditional-mode product
+
+def lr_from_dense(a, policy):
+    """``from_dense`` (``lowrank.py:50-54``): truncated SVD of a dense block."""
+    u, s, vt = np.linalg.svd(a, full_matrices=False)
+    r = eps_rank(s, policy)
+    return LR(u[:, :r] * s[:r], vt[:r].T.copy())
+
+
+def lr_norm(t: LR):
+    """``LowRank.norm`` (``lowrank.py:38-43``): Frobenius norm by the k x k Gram trick."""
+    if t.rank == 0:
+        return 0.0
+    g = (t.left.T @ t.left) @ (t.right.T @ t.right)
+    return float(np.sqrt(max(np.trace(g), 0.0)))
+
+
+def truncated_sum_o(terms, policy):
+    """``fast_truncate_sum`` (``lowrank.py:123-138``): fold each term into a running
+    truncated sum (the first two are added before the first truncation)."""
+    if not terms:
+        raise ValueError("need at least one term")
+    if len(terms) == 1:
+        return lr_truncate(terms[0], policy)
+    acc = lr_truncate(LR(np.hstack([terms[0].left, terms[1].left]),
+                         np.hstack([terms[0].right, terms[1].right])), policy)
+    for t in terms[2:]:
+        acc = lr_truncate(LR(np.hstack([acc.left, t.left]), np.hstack([acc.right, t.right])),
+                          policy)
+    return acc
+
+
+def _pad_o(t: LR, r0, r1, c0, c1, m, n):
+    """``_pad_child`` (``multiply.py:103-109``): zero-pad a cell's factors to the block."""
+    left = np.zeros((m, t.rank))
+    right = np.zeros((n, t.rank))
+    left[r0:r1] = t.left
+    right[c0:c1] = t.right
+    return LR(left, right)
+
+
+def pair_hier_o(p: View, q: View, policy):
+    """``_pair_structural_lowrank`` (``multiply.py:140-189``): bottom-up conversion of a
+    pending pair on the grid of its children; each cell folds its middle-cluster
+    contributions, then the cells are folded in row-child-major order."""
+    if not p.inner:
+        return lr_from_dense(p.dense_block() @ q.dense_block(), policy)
+    bt = p.H.bt
+    tree = bt.tree
+    taus = tree.children[bt.tau[p.b]]
+    sigmas = tree.children[bt.sigma[q.b]]
+    rhos = tree.children[bt.sigma[p.b]]
+    m, n = p.shape[0], q.shape[1]
+    pr0, _ = bt.rows(p.b)
+    qc0, _ = bt.cols(q.b)
+    cells = []
+    for tau in taus:
+        for sigma in sigmas:
+            contrib = []
+            for rho in rhos:
+                pc = View(p.H, bt.child_for(p.b, int(tau), int(rho)))
+                qc = View(q.H, bt.child_for(q.b, int(rho), int(sigma)))
+                if pc.lowrank or qc.lowrank:
+                    term, _ = thin_product(pc, qc)
+                elif pc.inner:
+                    term = pair_hier_o(pc, qc, policy)
+                else:
+                    term = lr_from_dense(pc.dense_block() @ qc.dense_block(), policy)
+                if term.rank > 0:
+                    contrib.append(term)
+            if contrib:
+                cell = truncated_sum_o(contrib, policy)
+                t0, t1 = int(tree.lo[tau]) - pr0, int(tree.hi[tau]) - pr0
+                s0, s1 = int(tree.lo[sigma]) - qc0, int(tree.hi[sigma]) - qc0
+                cells.append(_pad_o(cell, t0, t1, s0, s1, m, n))
+    if not cells:
+        return empty_lr(m, n)
+    return truncated_sum_o(cells, policy)
+
+
+class PairOpO(Op):
+    """``_PairProductMap`` (``multiply.py:82-100``): a pending pair as a linear operator."""
+
+    def __init__(self, p: View, q: View):
+        super().__init__()
+        self.p, self.q = p, q
+        self.shape = (p.shape[0], q.shape[1])
+
+    def mat(self, v):
+        return self.p.mat(self.q.mat(v))
+
+    def mat_t(self, w):
+        return self.q.mat_t(self.p.mat_t(w))
+
+
+def convert_pair_o(p: View, q: View, policy, converter, b, seed=0, q_it=1):
+    """``_convert_pair`` (``multiply.py:192-204``): ``(LR, matvec count)``."""
+    if converter == "hier-approx":
+        return pair_hier_o(p, q, policy_of(policy)), 0
+    op = PairOpO(p, q)
+    op.count = 0
+    out = compress_o(op, policy_of(policy), converter, q=q_it, seed=block_seed(seed, b))
+    return out, op.count
+
+
+def hmult_traditional_o(A: HMatO, B: HMatO, policy, converter="hier-approx", seed=0,
+                        q=1, only=None):
+    """``hmult_traditional`` (``multiply.py:207-263`` with ``leaf_traditional``): every
+    pending pair of a far leaf is converted to low rank on its own, then the leaf's terms,
+    largest norm first (stable), are combined by ``fast_truncate_sum``.  Near leaves are
+    evaluated densely as in ``hmult_new``."""
+    bt = A.bt
+    pol = policy_of(policy)
+    rep = ReportO()
+    data, bad = {}, set()
+    t0 = time.perf_counter()
+    need = None
+    if only is not None:
+        need = set()
+        parent = _parents(bt)
+        for b in only:
+            x = b
+            while x >= 0:
+                need.add(x)
+                x = parent[x]
+
+    def walk(s, b):
+        if bt.kind[b] == INNER:
+            for c in bt.children[b]:
+                if need is None or int(c) in need:
+                    walk(descend(s, int(c)), int(c))
+        elif bt.kind[b] == FAR:
+            terms = [t for t in s.lrs if t.rank > 0]
+            for p, qq in s.pend:
+                t, cnt = convert_pair_o(p, qq, pol, converter, b, seed, q)
+                rep.matvec_count += cnt
+                if t.degraded:
+                    rep.degraded_blocks += 1
+                    rep.warnings.append(f"pair conversion degraded on block {b}")
+                terms.append(t)
+            terms = [t for t in terms if t.rank > 0]
+            if terms:
+                terms.sort(key=lambda t: -lr_norm(t))
+                blk = truncated_sum_o(terms, pol)
+            else:
+                blk = empty_lr(*s.shape)
+            rep.far_leaves += 1
+            rep.max_far_rank = max(rep.max_far_rank, blk.rank)
+            data[b] = blk
+        else:
+            rep.near_leaves += 1
+            data[b] = dense_eval(s)
+
+    walk(root_expr(A, B), 0)
+    rep.wall_s = time.perf_counter() - t0
+    out = HMatO(bt, data, bad)
+    out.report = rep
+    return out
+
+
 def _parents(bt: BlockTreeO):
     par = getattr(bt, "_parents", None)
     if par is None:

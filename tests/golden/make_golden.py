@@ -8,6 +8,7 @@ geometry only knows sphere panels, so point clouds enter through a duck-typed
 ``LinearMap`` whose rows/columns come from the point kernel.
 
 Usage:  python tests/golden/make_golden.py      (writes tests/golden/*.npz)
+        python tests/golden/make_golden.py traditional   (only traditional.npz)
 """
 
 import hashlib
@@ -227,8 +228,73 @@ def case_compressors():
     save("compressors.npz", arrays)
 
 
+def trad_case(conv, A, B, tol, keep_dense=False, sample=()):
+    """The reference's traditional-mode product (``hmult_traditional``) with one pair
+    converter: per-leaf ranks / norms, the report and dense or sampled blocks."""
+    cfg = multiply.MultiplyConfig(mode="traditional",
+                                  compressor=compressors.CompressorKind("aca", seed=0),
+                                  policy=lowrank.EpsRank(tol), converter=conv)
+    t0 = time.time()
+    C = multiply.hmult_traditional(A, B, cfg)
+    wall = time.time() - t0
+    ids, kinds, ranks, fros = leaf_table(C)
+    rep = C.report
+    out = {
+        f"{conv}/ids": ids, f"{conv}/kinds": kinds, f"{conv}/ranks": ranks,
+        f"{conv}/fros": fros,
+        f"{conv}/report": np.array([rep.degraded_blocks, rep.max_far_rank,
+                                    rep.matvec_count, rep.far_leaves, rep.near_leaves]),
+    }
+    if keep_dense:
+        out[f"{conv}/dense"] = hmatrix.to_dense(C)
+    for b in sample:
+        p = C.data[b]
+        out[f"{conv}/blk{b}"] = p.to_dense() if isinstance(p, lowrank.LowRank) else p
+    print(f"  traditional {conv}: {wall:.2f}s far={rep.far_leaves} maxr={rep.max_far_rank} "
+          f"mv={rep.matvec_count}", flush=True)
+    return out
+
+
+def case_traditional(specs, convs=("hier-approx", "dense-svd")):
+    """traditional.npz: the traditional-mode products of the product cases (same operands
+    as small2d / ragged3d / cfg1, keys prefixed by the case name)."""
+    arrays = {}
+    for name, n, geom, n_min, eta, ka, kb, eps_a, tol, sample in specs:
+        print(f"traditional {name}: n={n}", flush=True)
+        pts, tree, bct, A, B = product_setup(n, geom, n_min, eta, ka, kb, eps_a)
+        if sample == "auto":
+            picked, seen = [], set()
+            for leaf in bct.leaves:
+                key = (leaf.kind, leaf.tau.size)
+                if key not in seen:
+                    seen.add(key)
+                    picked.append(leaf.id)
+            picked += [leaf.id for leaf in bct.leaves[::157]]
+            sample = tuple(sorted(set(picked)))
+        arrays[f"{name}/sample"] = np.array(sample, dtype=np.int64)
+        for conv in convs:
+            try:
+                out = trad_case(conv, A, B, tol, keep_dense=n <= 512, sample=sample)
+            except Exception as exc:  # recorded: the reference itself rejects the case
+                print(f"  traditional {conv}: reference raised {exc!r}", flush=True)
+                arrays[f"{name}/{conv}/error"] = np.frombuffer(repr(exc).encode(), np.uint8)
+                continue
+            arrays.update({f"{name}/{k}": v for k, v in out.items()})
+    save("traditional.npz", arrays)
+
+
+TRAD_SPECS = (
+    ("small2d", 256, "square", 16, 0.8, "exp", None, 1e-8, 1e-6, ()),
+    ("ragged3d", 200, "cube", 12, 1.0, "exp0.5", "inv", 1e-8, 1e-8, ()),
+    ("cfg1", 2048, "square", 32, 0.8, "exp", None, 1e-8, 1e-6, "auto"),
+)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    if sys.argv[1:] == ["traditional"]:
+        case_traditional(TRAD_SPECS)
+        sys.exit(0)
     case_trees()
     case_compressors()
     all_tags = ("dense-svd", "aca", "bilanczos", "randomized")
