@@ -122,9 +122,16 @@ typedef struct hx_plan_info {
  * HX_PLAN_IMPLICIT(l): far leaves with min(m, n) >= 2^l are never materialized; hx_product
  * sketches them straight from their terms (range pass Z = R^T Omega, Y = L Z; co-range
  * W = L^T Q, B^T = R W) and estimates the unsampled tail from extra probe columns.  The
- * route the canonical work model prices as "sketch". */
+ * route the canonical work model prices as "sketch".
+ * HX_PLAN_TRAD(c): the traditional-mode product (hmult_traditional, multiply.py:259-263):
+ * every pending pair of a far leaf is converted to low rank on its own -- c = 1 by the
+ * hierarchical agglomeration (converter "hier-approx", multiply.py:140-189), c = 2 by one
+ * best approximation of the pair product (converter "dense-svd") -- and each far leaf is
+ * the norm-sorted pairwise truncated sum of its terms (fast_truncate_sum). */
 #define HX_PLAN_DEFER 1
 #define HX_PLAN_LOG 2
+#define HX_PLAN_TRAD_SHIFT 4
+#define HX_PLAN_TRAD(c) ((int)(c) << HX_PLAN_TRAD_SHIFT)
 #define HX_PLAN_IMPLICIT_SHIFT 8
 #define HX_PLAN_IMPLICIT(l) ((int)(l) << HX_PLAN_IMPLICIT_SHIFT)
 int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx_operand* b,

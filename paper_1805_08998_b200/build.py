@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["plan.cpp", "errors.cpp", "hmx1.cpp", "runtime.cu"]
 HEADERS = ["hx_types.h", "hx_internal.h", "gemm.cuh", "gemm_ws.cuh", "dense_la.cuh", "dense_la_warp.cuh",
            "qr_rows.cuh", "gather_gemm.cuh", "assemble.cuh", "iterative.cuh",
-           "np_random.cuh"]
+           "np_random.cuh", "traditional.cuh", "traditional_exec.cuh"]
 OUT = os.path.join(HERE, "libhx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -93,6 +93,23 @@ struct OutLeaf {
   // workspace; the leaf's terms are the groups [g_begin, g_end) of mat_groups
   int8_t implicit;
   int32_t g_begin, g_end;
+  // traditional mode (hmult_traditional): root of the leaf's fold tree in hx_plan::tnodes
+  // (-1 otherwise); the path groups [g_begin, g_end) hold its inherited low-rank terms
+  int32_t troot;
+};
+
+// Traditional-mode conversion tree of a far leaf (multiply.py:140-263).  Items name one
+// term of mat_terms on the node's block; folds combine their children by pairwise
+// truncated summation (fast_truncate_sum, lowrank.py:123-138); a stack truncates the
+// concatenation of its children once (a compressor converter on the pair product).
+enum TKind : int8_t { TN_LR = 0, TN_DD = 1, TN_FOLD = 2, TN_STACK = 3 };
+struct TNode {
+  int8_t kind;
+  int8_t sort;      // leaf root: children in decreasing-norm order (multiply.py:222-224)
+  int32_t term;     // items: index into mat_terms
+  int32_t m, n;
+  int64_t row0, col0;
+  int32_t kid_begin, kid_end;  // children: hx_plan::tkids[kid_begin, kid_end)
 };
 
 void set_error(const std::string& msg);
@@ -160,5 +177,10 @@ struct hx_plan {
   std::vector<int32_t> log_block, log_a, log_b, log_rank;
   bool logged = false;
   std::vector<int8_t> log_kind;
+  // traditional mode: 0 off, 1 hierarchical pair conversion, 2 one truncation per pair
+  int trad = 0;
+  std::vector<hx::TNode> tnodes;
+  std::vector<int32_t> tkids;
+  int64_t trad_matvecs = 0;  // pending pairs converted (matvec count of a compressor converter)
   hx_plan_info info;
 };

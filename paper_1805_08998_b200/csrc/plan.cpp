@@ -84,6 +84,10 @@ struct Out {
   double flops_near = 0, bytes_near = 0;
   int64_t ws_far = 0, ws_near = 0;
   int32_t n_sumsq = 0;
+  // traditional mode: conversion trees (term / node indices local to this output)
+  std::vector<hx::TNode> tnodes;
+  std::vector<int32_t> tkids;
+  int64_t trad_cols = 0;
 };
 
 struct Walk {
@@ -116,6 +120,7 @@ struct Builder {
   std::vector<uint8_t> owned_sub;
   hx::pvec<TRec> recs;
   bool logging = false;  // HX_PLAN_LOG: keep the restrict log (parity tests)
+  int trad = 0;          // HX_PLAN_TRAD: 0 new mode, 1 hierarchical pairs, 2 stacked pairs
   int64_t implicit_min = 0;  // far leaves with min(m, n) >= this take the implicit route
   // sketch width assumed by the implicit route's per-term choice (HX_SKETCH_COLS; 0 sketches
   // every sub-block term, the fully implicit route)
@@ -385,6 +390,7 @@ struct Builder {
     L.edd = edd;
     L.implicit = 0;
     L.g_begin = L.g_end = -1;
+    L.troot = -1;
     L.tile_begin = int32_t(o.tiles.size());
     L.sumsq_begin = o.n_sumsq;
     // implicit route: the terms inherited from the root path (full-leaf extent, most of the
@@ -465,6 +471,129 @@ struct Builder {
     o.leaves.push_back(L);
   }
 
+  // --------------------------------------------------------------- traditional mode
+  int32_t add_node(Out& o, int8_t kind_, int32_t term, int tc, int sc,
+                   const std::vector<int32_t>& kids, int8_t sort = 0) const {
+    hx::TNode x;
+    x.kind = kind_;
+    x.sort = sort;
+    x.term = term;
+    x.m = int32_t(sz(tc));
+    x.n = int32_t(sz(sc));
+    x.row0 = lo(tc);
+    x.col0 = lo(sc);
+    x.kid_begin = int32_t(o.tkids.size());
+    o.tkids.insert(o.tkids.end(), kids.begin(), kids.end());
+    x.kid_end = int32_t(o.tkids.size());
+    o.tnodes.push_back(x);
+    return int32_t(o.tnodes.size() - 1);
+  }
+
+  // Every item of the exact expansion of the pending pair (p, q) on block tc x sc (the
+  // sub-pair recursion of restrict, sumexpr.py:120-154, carried to the leaves): the terms
+  // a compressor converter sees through _PairProductMap (multiply.py:82-100).
+  void pair_items(Walk& w, int tc, int sc, int p, int q, std::vector<int32_t>& items) const {
+    Out& o = w.o;
+    if (dense_pair(p, q)) {
+      const int32_t ti = int32_t(o.terms.size());
+      create_dxd(w, tc, sc, p, q);
+      items.push_back(add_node(o, hx::TN_DD, ti, tc, sc, {}));
+      return;
+    }
+    if (kind(p) != INNER || kind(q) != INNER)
+      throw hx::Unsupported("traditional mode: H-block x dense pending pair (ragged tree)");
+    for (int ti = 0; ti < 2; ++ti)
+      for (int si = 0; si < 2; ++si)
+        for (int ri = 0; ri < 2; ++ri) {
+          const int pc = child_of(p, ti, ri), qc = child_of(q, ri, si);
+          if (pc < 0 || qc < 0) throw std::runtime_error("block tree is not level-conserving");
+          const int tcc = t.tau[pc], scc = t.sigma[qc];
+          if (isF(A, pc) || isF(B, qc)) {
+            const int32_t tix = int32_t(o.terms.size());
+            if (create_lr(w, tcc, scc, pc, qc, -1) > 0)
+              items.push_back(add_node(o, hx::TN_LR, tix, tcc, scc, {}));
+          } else {
+            pair_items(w, tcc, scc, pc, qc, items);
+          }
+        }
+  }
+
+  // _convert_pair (multiply.py:192-204) of the pending pair (p, q) on block tc x sc:
+  // _pair_structural_lowrank (multiply.py:140-189) -- a dense pair is one truncated SVD of
+  // its product; an inner pair folds each cell (tau', sigma') over its middle children
+  // (thin products as they are, inner sub-pairs recursively, dense sub-pairs by SVD) and
+  // then folds the cells in row-child-major order -- or, for the stacked converter, one
+  // best approximation of the whole pair product.
+  int32_t trad_pair(Walk& w, int tc, int sc, int p, int q) const {
+    Out& o = w.o;
+    if (dense_pair(p, q)) {
+      const int32_t ti = int32_t(o.terms.size());
+      create_dxd(w, tc, sc, p, q);
+      const int32_t item = add_node(o, hx::TN_DD, ti, tc, sc, {});
+      return add_node(o, hx::TN_FOLD, -1, tc, sc, {item});  // from_dense(P Q)
+    }
+    if (kind(p) != INNER || kind(q) != INNER)
+      throw hx::Unsupported("traditional mode: H-block x dense pending pair (ragged tree)");
+    if (trad == 2) {
+      std::vector<int32_t> items;
+      pair_items(w, tc, sc, p, q, items);
+      return add_node(o, hx::TN_STACK, -1, tc, sc, items);
+    }
+    std::vector<int32_t> cells;
+    for (int ti = 0; ti < 2; ++ti)
+      for (int si = 0; si < 2; ++si) {
+        std::vector<int32_t> contrib;
+        int tcc = -1, scc = -1;
+        for (int ri = 0; ri < 2; ++ri) {
+          const int pc = child_of(p, ti, ri), qc = child_of(q, ri, si);
+          if (pc < 0 || qc < 0) throw std::runtime_error("block tree is not level-conserving");
+          tcc = t.tau[pc];
+          scc = t.sigma[qc];
+          if (isF(A, pc) || isF(B, qc)) {
+            const int32_t tix = int32_t(o.terms.size());
+            if (create_lr(w, tcc, scc, pc, qc, -1) > 0)
+              contrib.push_back(add_node(o, hx::TN_LR, tix, tcc, scc, {}));
+          } else {
+            contrib.push_back(trad_pair(w, tcc, scc, pc, qc));
+          }
+        }
+        if (!contrib.empty()) cells.push_back(add_node(o, hx::TN_FOLD, -1, tcc, scc, contrib));
+      }
+    return add_node(o, hx::TN_FOLD, -1, tc, sc, cells);
+  }
+
+  // leaf_traditional (multiply.py:216-224): the leaf's inherited terms (its path groups)
+  // plus one converted term per pending pair, folded in decreasing-norm order.
+  void trad_leaf(Walk& w, int c, const PairList& pend) const {
+    Out& o = w.o;
+    const int tc = t.tau[c], sc = t.sigma[c];
+    std::vector<int32_t> kids;
+    for (const auto& pq : pend) {
+      kids.push_back(trad_pair(w, tc, sc, pq.first, pq.second));
+      if (trad == 2) o.trad_cols += sz(sc);  // dense_svd_compress applies S to n columns
+    }
+    hx::OutLeaf L;
+    std::memset(&L, 0, sizeof(L));
+    L.id = c;
+    L.kind = 1;
+    L.m = int32_t(sz(tc));
+    L.n = int32_t(sz(sc));
+    L.row0 = lo(tc);
+    L.col0 = lo(sc);
+    L.ws_off = o.ws_far;
+    L.K = w.path_K;
+    L.implicit = 0;
+    L.g_begin = int32_t(o.tile_groups.size());
+    o.tile_groups.insert(o.tile_groups.end(), w.path.begin(), w.path.end());
+    L.g_end = int32_t(o.tile_groups.size());
+    L.troot = add_node(o, hx::TN_FOLD, -1, tc, sc, kids, 1);
+    L.tile_begin = L.tile_end = int32_t(o.tiles.size());
+    L.sumsq_begin = L.sumsq_end = o.n_sumsq;
+    o.max_out_dim = std::max<int64_t>(o.max_out_dim, std::max(sz(tc), sz(sc)));
+    o.n_far++;
+    o.leaves.push_back(L);
+  }
+
   // DFS below block b (whose own terms are already created).  With `tasks`, inner children
   // at block level `cut` are deferred as parallel tasks instead of descended.
   void visit(Walk& w, int b, int level, const PairList& pend, int cut,
@@ -483,7 +612,10 @@ struct Builder {
       // inner x inner pairs of a leaf are expanded below
       double fdd = 0, edd = 0;
       PairList rest;
-      if (kind(c) != INNER) {
+      const bool trad_leaf_c = trad && kind(c) == FAR;
+      if (trad_leaf_c) {
+        rest.swap(sub);  // every pending pair is converted on its own (multiply.py:216-219)
+      } else if (kind(c) != INNER) {
         for (const auto& pq : sub) {
           if (mixed_pair(pq.first, pq.second)) {
             create_mixed(w, t.tau[c], t.sigma[c], pq.first, pq.second);
@@ -517,6 +649,8 @@ struct Builder {
         } else {
           visit(w, c, level + 1, rest, cut, tasks);
         }
+      } else if (trad_leaf_c) {
+        trad_leaf(w, c, rest);
       } else {
         std::vector<VGroup> vg;
         int64_t K = w.path_K;
@@ -564,9 +698,11 @@ struct Builder {
     const size_t no = outs.size();
     std::vector<int64_t> b_terms(no + 1, 0), b_tg(no + 1, 0), b_tiles(no + 1, 0),
         b_sumsq(no + 1, 0), b_far(no + 1, 0), b_near(no + 1, 0), b_recs(no + 1, 0),
-        b_leaves(no + 1, 0);
+        b_leaves(no + 1, 0), b_nodes(no + 1, 0), b_kids(no + 1, 0);
     for (size_t i = 0; i < no; ++i) {
       const Out& o = outs[i];
+      b_nodes[i + 1] = b_nodes[i] + int64_t(o.tnodes.size());
+      b_kids[i + 1] = b_kids[i] + int64_t(o.tkids.size());
       b_terms[i + 1] = b_terms[i] + int64_t(o.terms.size());
       b_tg[i + 1] = b_tg[i] + int64_t(o.tile_groups.size());
       b_tiles[i + 1] = b_tiles[i] + int64_t(o.tiles.size());
@@ -643,15 +779,33 @@ struct Builder {
           L.tile_end += int32_t(b_tiles[i]);
           L.sumsq_begin += int32_t(b_sumsq[i]);
           L.sumsq_end += int32_t(b_sumsq[i]);
-          if (L.implicit) {
+          if (L.implicit || L.troot >= 0) {
             L.g_begin += int32_t(b_tg[i]);
             L.g_end += int32_t(b_tg[i]);
           }
+          if (L.troot >= 0) L.troot += int32_t(b_nodes[i]);
           P.leaves[size_t(b_leaves[i] + l)] = L;
         }
       }
     }
     lap("merge copy");
+    if (b_nodes[no] > 0) {  // traditional-mode conversion trees
+      P.tnodes.resize(size_t(b_nodes[no]));
+      P.tkids.resize(size_t(b_kids[no]));
+      for (size_t i = 0; i < no; ++i) {
+        const Out& o = outs[i];
+        for (size_t k = 0; k < o.tnodes.size(); ++k) {
+          hx::TNode x = o.tnodes[k];
+          if (x.term >= 0) x.term += int32_t(b_terms[i]);
+          x.kid_begin += int32_t(b_kids[i]);
+          x.kid_end += int32_t(b_kids[i]);
+          P.tnodes[size_t(b_nodes[i]) + k] = x;
+        }
+        for (size_t k = 0; k < o.tkids.size(); ++k)
+          P.tkids[size_t(b_kids[i]) + k] = o.tkids[k] + int32_t(b_nodes[i]);
+        P.trad_matvecs += o.trad_cols;
+      }
+    }
     // restrict log in the reference's visiting order: each subtree's log goes right after
     // the top-part entries logged before the subtree was deferred
     if (logging) {
@@ -1253,6 +1407,8 @@ extern "C" int hx_plan_create(const hx_tree* tree, const hx_operand* a, const hx
       auto bld = std::make_shared<Builder>(plan->tree, plan->opa, plan->opb, leaf_mask, tile,
                                            *plan);
       bld->logging = (flags & HX_PLAN_LOG) != 0;
+      bld->trad = (flags >> HX_PLAN_TRAD_SHIFT) & 3;
+      plan->trad = bld->trad;
       const int ish = (flags >> HX_PLAN_IMPLICIT_SHIFT) & 31;
       bld->implicit_min = ish ? (int64_t(1) << ish) : 0;
       plan->logged = bld->logging;

@@ -34,6 +34,7 @@
 #include "gemm_ws.cuh"
 #include "iterative.cuh"
 #include "qr_rows.cuh"
+#include "traditional.cuh"
 #include "hx_internal.h"
 
 using namespace hx;
@@ -542,6 +543,25 @@ struct hx_ctx {
   DArr<IterOut> iter_outs;
   DArr<UrJob> ur_jobs;
   std::vector<DArr<double>> work;  // one workspace per sketch round
+  // traditional mode (traditional_exec.cuh): wave workspace, ping-pong running sums, kept
+  // values of finished folds, wave work lists
+  DArr<double> trad_ws, trad_tmp[2], trad_nv;
+  std::vector<DArr<double>> trad_keep;
+  DArr<TSeg> trad_segs;
+  DArr<TNormJob> trad_norm_jobs;
+  DArr<const double*> trad_sigp;
+  void trad_release(bool all) {
+    for (auto& k : trad_keep) k.release();
+    trad_keep.clear();
+    if (!all) return;
+    trad_ws.release();
+    trad_tmp[0].release();
+    trad_tmp[1].release();
+    trad_nv.release();
+    trad_segs.release();
+    trad_norm_jobs.release();
+    trad_sigp.release();
+  }
   std::vector<double*> pools;      // operand pools built by hx_assemble (owned)
   // sketch-width hints: the largest rank seen per log2(min(m, n)) class by earlier chunks
   // of the same product (hx_ctx_reset_hints between products), for the same policy
@@ -1343,6 +1363,8 @@ void launch_far_outputs(hx_ctx* c, const std::vector<FarBlock>& fb,
 
 }  // namespace
 
+#include "traditional_exec.cuh"
+
 extern "C" int hx_ctx_create(int device, hx_ctx** out) {
   return guarded([&]() -> int {
     if (!out) return fail(HX_EINVAL, "null out");
@@ -1457,6 +1479,7 @@ extern "C" int hx_ctx_trim(hx_ctx* c) {
     c->tb.release();
     c->te.release();
     for (auto& w : c->work) w.release();
+    c->trad_release(true);
     c->omega_rows = 0;
     c->omega_cols = 0;
     c->omega_seed = ~0ULL;
@@ -1846,8 +1869,12 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     int64_t sketch_cols = 0;  // operator columns the sketch route actually applied
     int rounds = 0;
     std::vector<int> active;
-    const bool iterative = cfg->tag >= 0 && cfg->tag <= 2;
-    if (iterative) {
+    const bool iterative = cfg->tag >= 0 && cfg->tag <= 2 && !P->trad;
+    if (P->trad) {
+      hm.mark("iter-start");
+      matvecs = run_traditional(c, P, cfg, fb, rounds);
+      hm.mark("iter-done");
+    } else if (iterative) {
       hm.mark("iter-start");
       matvecs = recompress_iterative(c, P, cfg, fb, jac_trans, rounds);
       hm.mark("iter-done");
@@ -2244,7 +2271,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     }
     CK(cudaEventRecord(c->ev[3], s));
     for (const FarBlock& f : fb) {
-      if (iterative) break;
+      if (iterative || P->trad) break;
       int& h = c->rank_hint[ilog2(f.mu)];
       h = std::max(h, f.rank);
       if (f.round > 0) c->class_retry[ilog2(f.mu)] = 1;
@@ -2288,6 +2315,7 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
     hm.mark("out-issued");
     CK(cudaEventSynchronize(c->ev[4]));
     hm.mark("synced");
+    c->trad_release(false);  // finished traditional-mode values are in BUF_OUT now
 
     if (st) {
       std::memset(st, 0, sizeof(*st));
@@ -2703,6 +2731,7 @@ extern "C" void hx_ctx_free(hx_ctx* c) {
     b.release();
   }
   for (auto& w : c->work) w.release();
+  c->trad_release(true);
   for (double* p : c->pools) cudaFree(p);
   for (int i = 0; i < 3; ++i) {
     c->terms[i].release();

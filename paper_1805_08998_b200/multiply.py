@@ -540,7 +540,7 @@ def overlap_default(overlap=None):
 
 def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0,
                     device_operands=True, fetch=True, chunks=None, implicit_min=None,
-                    overlap=None, device_pools=None):
+                    overlap=None, device_pools=None, trad=0):
     """Run the product on one GPU and return the product ``HMatrix``.
 
     ``device_operands``: attach operand pools already resident on this device (GPU
@@ -550,17 +550,19 @@ def multiply_device(h, k, cfg, device=0, leaf_mask=None, sketch0=0, oversample=0
     measurement of bench.py.  ``chunks``: number of pipelined chunks (default by size).
     ``device_pools``: ((ptr, n) of A, (ptr, n) of B), packed pools already on this device
     (replicas of a multi-GPU product, ``distributed.py``).  Calls on the same device are
-    serialized (``Device.lock``)."""
+    serialized (``Device.lock``).  ``trad``: 0 the new-mode product; 1 / 2 the
+    traditional-mode product with the hierarchical / one-truncation pair converter
+    (``HX_PLAN_TRAD``)."""
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     with Device.lock(device):
         return _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample,
                                 device_operands, fetch, chunks, implicit_min, overlap,
-                                device_pools)
+                                device_pools, trad)
 
 
 def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_operands,
-                     fetch, chunks, implicit_min, overlap, device_pools):
+                     fetch, chunks, implicit_min, overlap, device_pools, trad=0):
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
     policy = cfg.policy
@@ -624,7 +626,8 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
 
     plan_ms = [0.0]
     timeline = []  # (what, host start, host end) for HX_TIMING
-    iflags = implicit_flags(implicit_min, cfg.compressor.tag)
+    iflags = implicit_flags(implicit_min, cfg.compressor.tag) if not trad else \
+        (int(trad) << TRAD_SHIFT)
 
     def make_plan(group):
         mask = group_mask(h.bct, group, leaf_mask) if (len(queue_all) > 1 or leaf_mask
@@ -845,13 +848,28 @@ def hmult_new(h, k, cfg, devices=None):
     return multiply_device(h, k, cfg, device=int(devices[0]))
 
 
-def hmult_traditional(h, k, cfg):
-    """The reference's convert-then-truncate product (``multiply.py:259-263``): same config
-    check; the GPU build does not implement it and says so instead of
-    running the new-mode product under the traditional name."""
+# HX_PLAN_TRAD converter codes: hierarchical agglomeration of each pending pair
+# (_pair_structural_lowrank, multiply.py:140-189) or one best approximation of the pair
+# product (the dense-svd compressor on _PairProductMap, multiply.py:192-204)
+TRAD_SHIFT = 4
+TRAD_CONVERTERS = {"hier-approx": 1, "dense-svd": 2}
+
+
+def hmult_traditional(h, k, cfg, device=0):
+    """Product H K in the convert-then-truncate discipline (``multiply.py:259-263``): every
+    pending pair of a far leaf is converted to low rank on its own, then the leaf's terms
+    are combined largest norm first by pairwise truncated summation
+    (``fast_truncate_sum``, ``lowrank.py:123-138``); near leaves as in ``hmult_new``.
+
+    Converters ``hier-approx`` (the reference default) and ``dense-svd`` run on the GPU;
+    the matrix-free converters (``aca``, ``bilanczos``, ``randomized`` on the pair product)
+    are not built and raise ``NotImplementedError``."""
     if cfg.mode != "traditional":
         raise ValueError("config mode must be 'traditional'")
     if h.bct is not k.bct:
         raise ValueError("factors must live on the same block-cluster tree")
-    raise NotImplementedError("hmult_traditional (per-pair conversion + fast_truncate_sum) "
-                              "is not built in the B200 product; use hmult_new")
+    code = TRAD_CONVERTERS.get(cfg.converter)
+    if code is None:
+        raise NotImplementedError(f"traditional-mode converter {cfg.converter!r} is not built "
+                                  f"on the GPU (available: {', '.join(TRAD_CONVERTERS)})")
+    return multiply_device(h, k, cfg, device=int(device), trad=code)

@@ -473,3 +473,68 @@ def test_implicit_4096_blocks_matrix_free_oracle(tag):
         q = C.data[int(b)]
         assert abs(q.rank - ref.rank) <= 1, (b, q.rank, ref.rank)
         assert _lr_rel_diff(q.left, q.right, ref.left, ref.right) <= 10 * tol
+
+
+TRAD_CASES = {"small2d": "small2d.npz", "cfg1": "cfg1.npz", "ragged3d": "ragged3d.npz"}
+
+
+@pytest.mark.parametrize("case", ["small2d", "cfg1", "ragged3d"])
+@pytest.mark.parametrize("conv", ["hier-approx", "dense-svd"])
+def test_traditional_parity(golden, case, conv):
+    """hmult_traditional (multiply.py:207-263) on the GPU against the reference's own
+    traditional product (tests/golden/traditional.npz): per-pair hierarchical conversion or
+    one best approximation per pair, then the norm-sorted pairwise truncated sum of every
+    far leaf.  Same contract as the new mode: ranks within +-1, blocks within 10 tol."""
+    import paper_1805_08998_b200 as hx
+
+    g = golden(TRAD_CASES[case])
+    t = golden("traditional.npz")
+    bct, A, B, oa, ob, tol = _operands(g, TRAD_CASES[case])
+    cfg = hx.MultiplyConfig(mode="traditional", converter=conv, policy=hx.EpsRank(tol))
+    C = hx.hmult_traditional(A, B, cfg)
+    key = f"{case}/{conv}"
+    rep = C.report
+    ref_rep = t[f"{key}/report"]
+    assert [rep.degraded_blocks, rep.matvec_count, rep.far_leaves, rep.near_leaves] == \
+        [ref_rep[0], ref_rep[2], ref_rep[3], ref_rep[4]]
+    assert abs(rep.max_far_rank - ref_rep[1]) <= 1
+    lo, hi = bct.tree.lo, bct.tree.hi
+    dense_ref = t.get(f"{key}/dense")
+    for b, r_ref, f_ref in zip(t[f"{key}/ids"], t[f"{key}/ranks"], t[f"{key}/fros"]):
+        b = int(b)
+        p = C.data[b]
+        if r_ref >= 0:
+            assert abs(p.rank - r_ref) <= 1, (b, p.rank, r_ref)
+        if dense_ref is not None:
+            tt, s = bct.tau[b], bct.sigma[b]
+            ref = dense_ref[lo[tt]:hi[tt], lo[s]:hi[s]]
+        elif f"{key}/blk{b}" in t:
+            ref = t[f"{key}/blk{b}"]
+        else:
+            fro = p.norm() if r_ref >= 0 else np.linalg.norm(p)
+            assert abs(fro - f_ref) <= 10 * tol * max(f_ref, 1e-300), (b, fro, f_ref)
+            continue
+        d = np.linalg.norm(_leaf_dense(p) - ref)
+        assert d <= 10 * tol * max(np.linalg.norm(ref), 1e-300) + 1e-300, (b, d)
+
+
+def test_traditional_fixed_rank_and_error(golden):
+    """FixedRank truncation of every fold step (select_rank, lowrank.py:75-90) and the
+    traditional product's global error against the exact dense product (small2d)."""
+    import paper_1805_08998_b200 as hx
+
+    g = golden("small2d.npz")
+    bct, A, B, oa, ob, tol = _operands(g, "small2d.npz")
+    C = hx.hmult_traditional(A, B, hx.MultiplyConfig(mode="traditional",
+                                                     policy=hx.FixedRank(3)))
+    R = O.hmult_traditional_o(oa, ob, O.Fixed(3))
+    for b, p in R.data.items():
+        q = C.data[b]
+        if isinstance(p, O.LR):
+            assert q.rank == p.rank, (b, q.rank, p.rank)
+            ref = p.dense()
+            assert np.linalg.norm(q.to_dense() - ref) <= 1e-7 * max(np.linalg.norm(ref), 1e-300)
+    Ce = hx.hmult_traditional(A, B, hx.MultiplyConfig(mode="traditional", policy=hx.EpsRank(tol)))
+    exact = oa.to_dense() @ ob.to_dense()
+    err = np.linalg.norm(hx.to_dense(Ce) - exact) / np.linalg.norm(exact)
+    assert err <= 10 * tol, err

@@ -76,8 +76,9 @@ def test_hmult_new_rejects_other_modes_and_trees():
         hx.hmult_new(h1, h2, cfg)
 
 
-def test_hmult_traditional_checks_then_reports_missing():
-    """multiply.py:259-263's config check; the traditional product itself is not built."""
+def test_hmult_traditional_checks():
+    """multiply.py:259-263's config check; the matrix-free pair converters are not built
+    and say so (before any device work)."""
     import paper_1805_08998_b200 as hx
 
     rng = np.random.default_rng(0)
@@ -86,9 +87,10 @@ def test_hmult_traditional_checks_then_reports_missing():
     h = hx.HMatrix(bct, {})
     with pytest.raises(ValueError, match="config mode must be 'traditional'"):
         hx.hmult_traditional(h, h, hx.MultiplyConfig(policy=hx.EpsRank(1e-6)))
-    with pytest.raises(NotImplementedError):
-        hx.hmult_traditional(h, h, hx.MultiplyConfig(mode="traditional",
-                                                     policy=hx.EpsRank(1e-6)))
+    for conv in ("aca", "bilanczos", "randomized"):
+        with pytest.raises(NotImplementedError, match="not built"):
+            hx.hmult_traditional(h, h, hx.MultiplyConfig(mode="traditional", converter=conv,
+                                                         policy=hx.EpsRank(1e-6)))
 
 
 def test_tiny_eps_warns_and_clamps():
