@@ -48,10 +48,6 @@ struct WsCfg {
 
 // short-K batches (term formation): 16-slot chunks, 3 stages (60 KB), 3 CTAs per SM
 using Ws64s = WsCfg<16, 3, 2, 3>;
-using Ws64s2 = WsCfg<16, 4, 2, 2>;  // A/B variant: 4 stages, 2 CTAs per SM, no spills
-// A/B variants with 4 producer warps (HX_WS_NPW=4)
-using Ws64s4 = WsCfg<16, 3, 4, 2>;
-using Ws64x4 = WsCfg<32, 3, 4, 2>;
 // long-K batches (materialization, sketches): 32-slot chunks, 3 stages, 2 CTAs per SM
 using Ws64 = WsCfg<32, 3, 2, 2>;
 
@@ -151,7 +147,10 @@ __device__ __forceinline__ void ws_cursor_init(WsCursor& c, const Tile& tl) {
 template <class C>
 __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
                                              const double* safe, int ld, int kc, int lo,
-                                             int hi, int slot0, int n, int tid) {
+                                             int hi, int slot0, int n, int tid, int ilo = 0,
+                                             int ihi = C::TM) {
+  // rows outside [ilo, ihi) are left as they are: the caller guarantees that no consumer
+  // reads them (a chunk made of this one segment, whose fragment mask excludes them)
   constexpr int TM = C::TM;
   if (kc == 0) {
     const bool al = ((reinterpret_cast<uintptr_t>(base) & 15) == 0) && ((ld & 1) == 0) &&
@@ -160,6 +159,7 @@ __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
       constexpr int PR = TM / 2, CL = C::NPT / PR;
       const int p = tid % PR, c = tid / PR;
       const int i = 2 * p;
+      if (i < ilo || i >= ihi) return;
       const int v = (i >= lo && i < hi) ? 16 : 0;
       const double* src = base + i + int64_t(c) * ld;
       unsigned dst = sbase + 8u * unsigned((slot0 + c) * C::LDI + i);
@@ -172,6 +172,7 @@ __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
     } else {
       constexpr int CL = C::NPT / TM;
       const int i = tid % TM, c = tid / TM;
+      if (i < ilo || i >= ihi) return;
       const int v = (i >= lo && i < hi) ? 8 : 0;
       const double* src = base + i + int64_t(c) * ld;
       unsigned dst = sbase + 8u * unsigned((slot0 + c) * C::LDI + i);
@@ -190,9 +191,10 @@ __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
       const int kk = 2 * q;
       if (kk < n) {
         const bool pair = kk + 1 < n;
-        const double* src = base + kk + int64_t(r) * ld;
-        unsigned dst = sbase + 8u * unsigned(r * C::LDK + slot0 + kk);
-        for (int i = r; i < TM; i += RL) {
+        const int i0 = r + (ilo > r ? (ilo - r + RL - 1) / RL * RL : 0);
+        const double* src = base + kk + int64_t(i0) * ld;
+        unsigned dst = sbase + 8u * unsigned(i0 * C::LDK + slot0 + kk);
+        for (int i = i0; i < ihi; i += RL) {
           const bool v = i >= lo && i < hi;
           if (pair) cp_async16(dst, v ? src : safe, v ? 16 : 0);
           else cp_async8(dst, v ? src : safe, v ? 8 : 0);
@@ -204,9 +206,10 @@ __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
       constexpr int RL = C::NPT / C::KC;
       const int kk = tid % C::KC, r = tid / C::KC;
       if (kk < n) {
-        const double* src = base + kk + int64_t(r) * ld;
-        unsigned dst = sbase + 8u * unsigned(r * C::LDK + slot0 + kk);
-        for (int i = r; i < TM; i += RL) {
+        const int i0 = r + (ilo > r ? (ilo - r + RL - 1) / RL * RL : 0);
+        const double* src = base + kk + int64_t(i0) * ld;
+        unsigned dst = sbase + 8u * unsigned(i0 * C::LDK + slot0 + kk);
+        for (int i = i0; i < ihi; i += RL) {
           const bool v = i >= lo && i < hi;
           cp_async8(dst, v ? src : safe, v ? 8 : 0);
           src += int64_t(RL) * ld;
@@ -220,12 +223,26 @@ __device__ __forceinline__ void ws_stage_seg(unsigned sbase, const double* base,
 template <class C>
 __device__ __forceinline__ void ws_stage_cols(unsigned sbase, const double* const* colp,
                                               int64_t off, const double* safe, int lo, int hi,
-                                              int slot0, int n, int tid) {
+                                              int slot0, int n, int tid, bool aligned) {
   constexpr int PK = C::KC / 2, RL = C::NPT / PK;
   const int q = tid % PK, r = tid / PK;
   const int kk = 2 * q;
   if (kk >= n) return;
   const bool pair = kk + 1 < n;
+  if (aligned && ((off | slot0) & 1) == 0) {
+    // every column pointer of the tile is 16-byte aligned (flag set with the table): one
+    // 16-byte copy per slot pair and row, no per-row alignment test
+    unsigned dst = sbase + 8u * unsigned(r * C::LDK + slot0 + kk);
+#pragma unroll 4
+    for (int i = r; i < C::TM; i += RL) {
+      const bool v = i >= lo && i < hi;
+      const double* src = v ? colp[i] + off + kk : safe;
+      if (pair) cp_async16(dst, src, v ? 16 : 0);
+      else cp_async8(dst, src, v ? 8 : 0);
+      dst += 8u * RL * C::LDK;
+    }
+    return;
+  }
   for (int i = r; i < C::TM; i += RL) {
     const bool v = i >= lo && i < hi;
     const unsigned dst = sbase + 8u * unsigned(i * C::LDK + slot0 + kk);
@@ -249,14 +266,24 @@ __device__ __forceinline__ void ws_zero_slots(double* s, int kc, int a, int b, i
   }
 }
 
+// 8-row fragments of tile half w (rows [w WT, w WT + WT)) that meet [lo, hi): bit a set
+// when fragment a does (the consumers skip the others).
+template <class C>
+__device__ __forceinline__ unsigned ws_frag_mask(int lo, int hi, int w) {
+  const int l = max(lo - w * C::WT, 0), h = min(hi - w * C::WT, C::WT);
+  if (h <= l) return 0u;
+  return (2u << ((h - 1) >> 3)) - (1u << (l >> 3));
+}
+
 // Producer: fill one stage from the cursor; returns the descriptor (all producer threads
 // compute it identically).
-template <class C>
+template <class C, bool GC>
 __device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, WsCursor& cur,
                                                  bool& have, const Group* __restrict__ groups,
                                                  const Term* __restrict__ terms,
                                                  const BufPtrs& bufs, const Tile& tl,
-                                                 const double* const* colp, int tid) {
+                                                 const double* const* colp, int tid,
+                                                 bool colp_aligned) {
   WsDesc d;
   d.used = 0;
   d.amask[0] = d.amask[1] = d.bmask[0] = d.bmask[1] = 0;
@@ -280,19 +307,24 @@ __device__ __forceinline__ WsDesc ws_build_chunk(double* sP, double* sQ, WsCurso
         tm.a_kc ? A + cur.k0 + int64_t(i0) * tm.a_ld : A + i0 + int64_t(cur.k0) * tm.a_ld;
     const double* pb =
         tm.b_kc ? B + cur.k0 + int64_t(j0) * tm.b_ld : B + j0 + int64_t(cur.k0) * tm.b_ld;
-    ws_stage_seg<C>(sp, pa, A, tm.a_ld, tm.a_kc, rlo, rhi, d.used, n, tid);
-    if (tm.b_kc == 2)
-      ws_stage_cols<C>(sq, colp, tm.b_off + cur.k0, bufs.p[BUF_A], clo, chi, d.used, n, tid);
+    // a segment that fills the chunk on its own (the stacked cores: K = a cluster size)
+    // stages only the row fragments it covers; the consumers' masks skip the others
+    int ilo = 0, ihi = C::TM;
+    if (n == C::KC) {
+      ilo = rhi > rlo ? (rlo & ~7) : 0;
+      ihi = rhi > rlo ? min((rhi + 7) & ~7, C::TM) : 0;
+    }
+    ws_stage_seg<C>(sp, pa, A, tm.a_ld, tm.a_kc, rlo, rhi, d.used, n, tid, ilo, ihi);
+    if (GC && tm.b_kc == 2)
+      ws_stage_cols<C>(sq, colp, tm.b_off + cur.k0, bufs.p[BUF_A], clo, chi, d.used, n, tid,
+                       colp_aligned);
     else
       ws_stage_seg<C>(sq, pb, B, tm.b_ld, tm.b_kc, clo, chi, d.used, n, tid);
 #pragma unroll
-    for (int w = 0; w < 2; ++w)
-#pragma unroll
-      for (int a = 0; a < C::FR; ++a) {
-        const int f0 = w * C::WT + a * 8;
-        if (f0 < rhi && f0 + 8 > rlo) d.amask[w] |= uint8_t(1u << a);
-        if (f0 < chi && f0 + 8 > clo) d.bmask[w] |= uint8_t(1u << a);
-      }
+    for (int w = 0; w < 2; ++w) {
+      d.amask[w] |= uint8_t(ws_frag_mask<C>(rlo, rhi, w));
+      d.bmask[w] |= uint8_t(ws_frag_mask<C>(clo, chi, w));
+    }
     d.used += n;
     ++nseg;
     cur.k0 += n;
@@ -346,7 +378,9 @@ __device__ __forceinline__ void ws_mma_t(double (&acc)[C::FR][C::FR][2], const d
   }
 }
 
-template <class C>
+// GC: the launch has MODE_GCOL tiles (term formation); launches without a column-record
+// table (materialization, sketches) compile the column-pointer path out.
+template <class C, bool GC>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
     const Tile* __restrict__ tiles, const Group* __restrict__ groups,
     const Term* __restrict__ terms, const __grid_constant__ BufPtrs bufs,
@@ -355,6 +389,7 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
   __shared__ WsDesc desc[C::STAGES];
   __shared__ const double* colp[C::TM];
+  __shared__ unsigned colp_bad[C::NPW];
   __shared__ double red[C::NCW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -374,18 +409,28 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
     unsigned phase = 0;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
       const Tile tl = tiles[t];
-      if (tl.mode == MODE_GCOL) {
+      bool colp_aligned = false;
+      if (GC && tl.mode == MODE_GCOL) {
         // the previous tile's copies were all issued (they captured their source pointers),
         // so the table can be rewritten once every producer is past them
         asm volatile("bar.sync 1, %0;\n" ::"n"(C::NPT));
+        bool bad = false;
         if (tid < tl.cols) {
           const int j = tl.col0 + tid;
           int idx = tl.aux;
           ColRec r = gcols[idx];
           while (j >= r.col + r.k) r = gcols[++idx];
-          colp[tid] = bufs.p[r.buf] + r.src_off + int64_t(j - r.col) * r.ld;
+          const double* p = bufs.p[r.buf] + r.src_off + int64_t(j - r.col) * r.ld;
+          colp[tid] = p;
+          bad = (reinterpret_cast<uintptr_t>(p) & 15) != 0;
         }
+        const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+        if ((tid & 31) == 0) colp_bad[tid >> 5] = anybad;
         asm volatile("bar.sync 1, %0;\n" ::"n"(C::NPT));
+        unsigned allbad = 0;
+#pragma unroll
+        for (int w = 0; w < C::NPW; ++w) allbad |= colp_bad[w];
+        colp_aligned = allbad == 0;
       }
       WsCursor cur;
       ws_cursor_init(cur, tl);
@@ -393,8 +438,8 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
       do {
         mbar_wait(&empty[stage], phase ^ 1u);
         double* sP = smem + stage * C::STAGE;
-        WsDesc d = ws_build_chunk<C>(sP, sP + C::OPSZ, cur, have, groups, terms, bufs, tl,
-                                     colp, tid);
+        WsDesc d = ws_build_chunk<C, GC>(sP, sP + C::OPSZ, cur, have, groups, terms, bufs, tl,
+                                     colp, tid, colp_aligned);
         d.tile = t;
         d.last = have ? 0 : 1;
         if (tid == 0) desc[stage] = d;
@@ -441,28 +486,67 @@ __global__ void __launch_bounds__(C::THREADS, C::MINB) grouped_gemm_ws_kernel(
       }
       if (d.last) break;
     }
-    // epilogue (as gemm.cuh)
+    // epilogue.  Plain stores (term formation, materialization) take a branch-free path:
+    // short-K tiles spend a third of the consumers' time here otherwise.
     const Tile tl = tiles[t];
     double* out = bufs.p[tl.out_buf] + tl.out_off;
     double ss = 0.0;
+    if (tl.mode != MODE_ADD && tl.mode != MODE_RESID_SUMSQ) {
+      const int r0 = wm * C::WT + (lane >> 2), c0 = wn * C::WT + (lane & 3) * 2;
+      double* base = out + r0 + int64_t(c0) * tl.out_ld;
+      const bool sq = tl.mode == MODE_STORE_SUMSQ;
+      const bool full = tl.rows == C::TM && tl.cols == C::TM;
+      if (full) {
 #pragma unroll
-    for (int a = 0; a < C::FR; ++a) {
-      const int r = wm * C::WT + a * 8 + (lane >> 2);
+        for (int b = 0; b < C::FR; ++b)
 #pragma unroll
-      for (int b = 0; b < C::FR; ++b) {
+          for (int h = 0; h < 2; ++h) {
+            double* p = base + int64_t(b * 8 + h) * tl.out_ld;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = wn * C::WT + b * 8 + (lane & 3) * 2 + h;
-          if (r < tl.rows && c < tl.cols) {
-            double* dst = out + r + int64_t(c) * tl.out_ld;
-            double v = acc[a][b][h];
-            if (tl.mode == MODE_RESID_SUMSQ) {
-              v = *dst - v;
-            } else {
-              if (tl.mode == MODE_ADD) v += *dst;
-              *dst = v;
+            for (int a = 0; a < C::FR; ++a) p[a * 8] = acc[a][b][h];
+          }
+      } else {
+        const int nr = tl.rows - r0, nc = tl.cols - c0;  // this lane's rows a * 8 < nr
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            double* p = base + int64_t(b * 8 + h) * tl.out_ld;
+            const bool cok = b * 8 + h < nc;
+#pragma unroll
+            for (int a = 0; a < C::FR; ++a)
+              if (cok && a * 8 < nr) {
+                p[a * 8] = acc[a][b][h];
+                ss += acc[a][b][h] * acc[a][b][h];
+              }
+          }
+      }
+      if (sq && full) {
+#pragma unroll
+        for (int a = 0; a < C::FR; ++a)
+#pragma unroll
+          for (int b = 0; b < C::FR; ++b) ss += acc[a][b][0] * acc[a][b][0] + acc[a][b][1] * acc[a][b][1];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < C::FR; ++a) {
+        const int r = wm * C::WT + a * 8 + (lane >> 2);
+#pragma unroll
+        for (int b = 0; b < C::FR; ++b) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int c = wn * C::WT + b * 8 + (lane & 3) * 2 + h;
+            if (r < tl.rows && c < tl.cols) {
+              double* dst = out + r + int64_t(c) * tl.out_ld;
+              double v = acc[a][b][h];
+              if (tl.mode == MODE_RESID_SUMSQ) {
+                v = *dst - v;
+              } else {
+                if (tl.mode == MODE_ADD) v += *dst;
+                *dst = v;
+              }
+              ss += v * v;
             }
-            ss += v * v;
           }
         }
       }

@@ -621,12 +621,10 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
   // warp-specialized persistent kernel (gemm_ws.cuh) unless HX_GEMM_WS=0
   static const bool use_ws = !(std::getenv("HX_GEMM_WS") && std::getenv("HX_GEMM_WS")[0] == '0');
   if (tile == 64 && use_ws) {
-    static int grid_s = 0, grid_l = 0, grid_s2 = 0, grid_s4 = 0, grid_l4 = 0;
-    static const bool short2 = std::getenv("HX_WS_SHORT2") != nullptr;
-    static const bool npw4 = std::getenv("HX_WS_NPW") && std::atoi(std::getenv("HX_WS_NPW")) == 4;
-    if (!grid_s) {
-      // HX_WS_RESERVE: SMs left free of the persistent GEMM CTAs (for the latency-bound
-      // recompression of a concurrent chunk on another context)
+    // grids: one CTA per resident slot.  HX_WS_RESERVE: SMs left free of the persistent
+    // GEMM CTAs (for the latency-bound recompression of a concurrent chunk on another context)
+    static int grid[2][2] = {{0, 0}, {0, 0}};  // [short K][column records]
+    if (!grid[0][0]) {
       static const int reserve = std::getenv("HX_WS_RESERVE") ? std::atoi(std::getenv("HX_WS_RESERVE")) : 0;
       auto grid_of = [](auto kern, int threads, int smem) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -636,46 +634,25 @@ void launch_gemm(hx_ctx* c, int tile, const Tile* tiles, const Group* groups, co
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, smem));
         return std::max(1, b) * std::max(1, sms - reserve);
       };
-      grid_s4 = grid_of(grouped_gemm_ws_kernel<Ws64s4>, Ws64s4::THREADS, Ws64s4::SMEM);
-      grid_l4 = grid_of(grouped_gemm_ws_kernel<Ws64x4>, Ws64x4::THREADS, Ws64x4::SMEM);
-      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64s>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64s::SMEM));
-      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64s2>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64s2::SMEM));
-      CK(cudaFuncSetAttribute(grouped_gemm_ws_kernel<Ws64>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64::SMEM));
-      int dev = 0, sms = 0, bs = 0, bl = 0;
-      CK(cudaGetDevice(&dev));
-      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-      sms = std::max(1, sms - reserve);
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bs, grouped_gemm_ws_kernel<Ws64s>,
-                                                       Ws64s::THREADS, Ws64s::SMEM));
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bl, grouped_gemm_ws_kernel<Ws64>,
-                                                       Ws64::THREADS, Ws64::SMEM));
-      grid_s = std::max(1, bs) * sms;
-      grid_l = std::max(1, bl) * sms;
-      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bs, grouped_gemm_ws_kernel<Ws64s2>,
-                                                       Ws64s2::THREADS, Ws64s2::SMEM));
-      grid_s2 = std::max(1, bs) * sms;
+      grid[0][0] = grid_of(grouped_gemm_ws_kernel<Ws64, false>, Ws64::THREADS, Ws64::SMEM);
+      grid[0][1] = grid_of(grouped_gemm_ws_kernel<Ws64, true>, Ws64::THREADS, Ws64::SMEM);
+      grid[1][0] = grid_of(grouped_gemm_ws_kernel<Ws64s, false>, Ws64s::THREADS, Ws64s::SMEM);
+      grid[1][1] = grid_of(grouped_gemm_ws_kernel<Ws64s, true>, Ws64s::THREADS, Ws64s::SMEM);
     }
-    if (npw4 && short_k && use_short)
-      grouped_gemm_ws_kernel<Ws64s4><<<std::min(n_tiles, grid_s4), Ws64s4::THREADS,
-                                       Ws64s4::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
-                                                           n_tiles, gcols);
-    else if (npw4)
-      grouped_gemm_ws_kernel<Ws64x4><<<std::min(n_tiles, grid_l4), Ws64x4::THREADS,
-                                       Ws64x4::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
-                                                           n_tiles, gcols);
-    else if (short_k && use_short && short2)
-      grouped_gemm_ws_kernel<Ws64s2><<<std::min(n_tiles, grid_s2), Ws64s2::THREADS,
-                                       Ws64s2::SMEM, st>>>(tiles, groups, terms, bp, sumsq,
-                                                           n_tiles, gcols);
-    else if (short_k && use_short)
-      grouped_gemm_ws_kernel<Ws64s><<<std::min(n_tiles, grid_s), Ws64s::THREADS, Ws64s::SMEM,
-                                      st>>>(tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+    const bool sk = short_k && use_short, gc = gcols != nullptr;
+    const int g = std::min(n_tiles, grid[sk][gc]);
+    if (sk && gc)
+      grouped_gemm_ws_kernel<Ws64s, true><<<g, Ws64s::THREADS, Ws64s::SMEM, st>>>(
+          tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+    else if (sk)
+      grouped_gemm_ws_kernel<Ws64s, false><<<g, Ws64s::THREADS, Ws64s::SMEM, st>>>(
+          tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+    else if (gc)
+      grouped_gemm_ws_kernel<Ws64, true><<<g, Ws64::THREADS, Ws64::SMEM, st>>>(
+          tiles, groups, terms, bp, sumsq, n_tiles, gcols);
     else
-      grouped_gemm_ws_kernel<Ws64><<<std::min(n_tiles, grid_l), Ws64::THREADS, Ws64::SMEM,
-                                     st>>>(tiles, groups, terms, bp, sumsq, n_tiles, gcols);
+      grouped_gemm_ws_kernel<Ws64, false><<<g, Ws64::THREADS, Ws64::SMEM, st>>>(
+          tiles, groups, terms, bp, sumsq, n_tiles, gcols);
     CK(cudaGetLastError());
     c->launches++;
     return;
