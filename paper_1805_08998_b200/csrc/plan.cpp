@@ -95,6 +95,16 @@ struct Walk {
   int32_t self;
   std::vector<GRef> path;  // groups of the current root path
   int64_t path_K = 0;
+  // pending-pair lists of the recursion, two per depth, reused across the whole descent (a
+  // fresh std::vector per visited block made the allocator a third of the descent time)
+  std::vector<PairList> pool = std::vector<PairList>(512);
+  PairList& scratch(int depth, int which) {
+    if (size_t(2 * depth + which) >= pool.size())
+      throw std::runtime_error("block tree deeper than 256 levels");
+    PairList& v = pool[size_t(2 * depth + which)];
+    v.clear();
+    return v;
+  }
 };
 
 struct Task {
@@ -333,7 +343,7 @@ struct Builder {
   // Expansion of the pending inner x inner pairs of a far leaf over virtual sub-blocks
   // (exact).
   void expand(Walk& w, int tc, int sc, const PairList& pend, std::vector<VGroup>& vg,
-              int64_t& K, double& fdd, double& edd) const {
+              int64_t& K, double& fdd, double& edd, int depth) const {
     if (pend.empty()) return;
     if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0)
       throw hx::Unsupported("H-block x dense pending pair at a leaf (ragged cluster trees)");
@@ -342,7 +352,7 @@ struct Builder {
       for (int si = 0; si < 2; ++si) {
         const int tcc = t.c_child[2 * tc + ti], scc = t.c_child[2 * sc + si];
         const int32_t gb = int32_t(o.terms.size());
-        PairList sub;
+        PairList& sub = w.scratch(depth, 0);
         int64_t Kv = 0;
         split_pairs(w, tc, sc, ti, si, pend, sub, -1, Kv);
         K += Kv;
@@ -367,7 +377,7 @@ struct Builder {
           vg.push_back(VGroup{GRef{w.self, int32_t(o.groups.size() - 1)}, lo(tcc),
                               lo(tcc) + sz(tcc), lo(scc), lo(scc) + sz(scc)});
         }
-        if (!leaf_level) expand(w, tcc, scc, sub, vg, K, fdd, edd);
+        if (!leaf_level) expand(w, tcc, scc, sub, vg, K, fdd, edd, depth + 1);
       }
   }
 
@@ -604,14 +614,14 @@ struct Builder {
       const int c = t.child[4 * b + ci];
       if (c < 0 || !owned_sub[c]) continue;
       const int32_t gb = int32_t(o.terms.size());
-      PairList sub;
+      PairList& sub = w.scratch(level, 0);
       int64_t Kc = 0;
       split_pairs(w, tc, sc, ci >> 1, ci & 1, pend, sub, c, Kc);
       o.n_terms_real += int64_t(o.terms.size()) - gb;
       // DxD pairs of a leaf join the leaf's own group (on ragged trees as sub-views);
       // inner x inner pairs of a leaf are expanded below
       double fdd = 0, edd = 0;
-      PairList rest;
+      PairList& rest = w.scratch(level, 1);
       const bool trad_leaf_c = trad && kind(c) == FAR;
       if (trad_leaf_c) {
         rest.swap(sub);  // every pending pair is converted on its own (multiply.py:216-219)
@@ -644,8 +654,7 @@ struct Builder {
       w.path_K += Kc;
       if (kind(c) == INNER) {
         if (tasks && level + 1 >= cut) {
-          tasks->push_back(Task{c, std::move(rest), w.path, w.path_K,
-                                int64_t(o.log_block.size())});
+          tasks->push_back(Task{c, rest, w.path, w.path_K, int64_t(o.log_block.size())});
         } else {
           visit(w, c, level + 1, rest, cut, tasks);
         }
@@ -656,7 +665,7 @@ struct Builder {
         int64_t K = w.path_K;
         // inner x inner pairs pending at a leaf (far, or near above the leaf level on a
         // ragged tree) are expanded exactly over virtual sub-blocks
-        expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd);
+        expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd, level + 1);
         const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
         if (kind(c) == NEAR) {
           o.flops_near += fdd + 2.0 * mm * nn * double(K);
@@ -1155,6 +1164,13 @@ struct Builder {
       // the thin factors side by side as columns of G; patch the materialization terms
       int64_t col = 0;
       for (int32_t i = g.b0; i < g.b1; ++i) {
+        // the group's records and their materialization terms are scattered (creation
+        // order): fetch a few ahead
+        if (i + 8 < g.b1) {
+          const TRec& rn = recs[order[i + 8]];
+          __builtin_prefetch(&rn, 0, 1);
+          if (i + 4 < g.b1) __builtin_prefetch(&P.mat_terms[recs[order[i + 4]].mat], 1, 1);
+        }
         const TRec& r = recs[order[i]];
         hx::ColRec& cp = P.gcols[size_t(g.o_gather + (i - g.b0))];
         cp.buf = g.side == 0 ? hx::BUF_B : hx::BUF_A;
