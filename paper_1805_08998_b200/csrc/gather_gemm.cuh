@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "gemm.cuh"
+#include "gemm_ws.cuh"
 
 namespace hx {
 
@@ -144,6 +145,228 @@ __global__ void __launch_bounds__(C::THREADS) gather_gemm_kernel(
         const int cc = wn * C::WT + b * 8 + (lane & 3) * 2 + h;
         if (r < tl.rows && cc < tl.cols) out[r + int64_t(cc) * tl.out_ld] = acc[a][b][h];
       }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Warp-specialized, persistent version (the structure of gemm_ws.cuh).  The sketch products
+// are thin (cols = the sketch width, 16-64) and long (K = the block dimension), so the
+// kernel is bound by streaming the gathered A rows: 2 producer warps keep a 3-deep ring of
+// 32-slot chunks in flight per CTA with cp.async (no CTA barrier in the main loop), rows and
+// columns beyond the tile's 8-aligned extent are not staged at all, and the 4 consumer
+// warps split the tile by rows (16 each) so that all of them work whatever the width.
+struct GwsDesc {
+  int32_t used, last;
+};
+
+template <class C>
+__device__ __forceinline__ void gws_stage(unsigned sbase, const double* const* rowp,
+                                          const int* kb, const int* ke, const double* safe,
+                                          int nrows, int nrows8, int kk0, bool fast, int tid) {
+  constexpr int PK = C::KC / 2, RL = C::NPT / PK;
+  const int q = tid % PK, r0 = tid / PK;
+  const int kk = kk0 + 2 * q;
+  unsigned dst = sbase + 8u * unsigned(r0 * C::LDK + 2 * q);
+  if (fast) {
+    // every row covers the chunk and is 16-byte aligned, or is a zero row
+#pragma unroll 4
+    for (int r = r0; r < nrows8; r += RL) {
+      const double* p = r < nrows ? rowp[r] : nullptr;  // nullptr: a zero (pad) row
+      cp_async16(dst, p ? p + kk : safe, p ? 16 : 0);
+      dst += 8u * RL * C::LDK;
+    }
+    return;
+  }
+  for (int r = r0; r < nrows8; r += RL) {
+    bool v0 = false, v1 = false;
+    const double* src = safe;
+    if (r < nrows && rowp[r] != nullptr) {
+      v0 = kk >= kb[r] && kk < ke[r];
+      v1 = kk + 1 >= kb[r] && kk + 1 < ke[r];
+      src = rowp[r] + kk;
+    }
+    if (v0 && v1 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
+      cp_async16(dst, src, 16);
+    } else {
+      cp_async8(dst, v0 ? src : safe, v0 ? 8 : 0);
+      cp_async8(dst + 8u, v1 ? src + 1 : safe, v1 ? 8 : 0);
+    }
+    dst += 8u * RL * C::LDK;
+  }
+}
+
+// consumer warp cw: rows [16 cw, 16 cw + 16) x NFC column fragments
+template <class C, int NFC>
+__device__ __forceinline__ void gws_mma(double (&acc)[2][8][2], const double* sP,
+                                        const double* sQ, int used, int cw, int lane,
+                                        unsigned amask) {
+  const int ksteps = (used + 3) >> 2;
+  const int r = lane >> 2, q = lane & 3;
+  const double* pa = sP + (cw * 16 + r) * C::LDK + q;
+  const double* pb = sQ + r * C::LDK + q;
+  for (int ks = 0; ks < ksteps; ++ks) {
+    double af[2], bf[NFC];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) af[a] = (amask >> a) & 1u ? pa[a * 8 * C::LDK + ks * 4] : 0.0;
+#pragma unroll
+    for (int b = 0; b < NFC; ++b) bf[b] = pb[b * 8 * C::LDK + ks * 4];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < NFC; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[a], bf[b]);
+  }
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::THREADS, C::MINB) gather_gemm_ws_kernel(
+    const GTile* __restrict__ tiles, const GSeg* __restrict__ segs,
+    const __grid_constant__ BufPtrs bufs, int n_tiles) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
+  __shared__ GwsDesc desc[C::STAGES];
+  __shared__ const double* arow[C::TM];
+  __shared__ const double* brow[C::TM];
+  __shared__ int akb[C::TM], ake[C::TM], bkb[C::TM], bke[C::TM];
+  __shared__ int slow_rows;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 2u * C::NPT);
+      mbar_init(&empty[s], unsigned(C::NCW));
+    }
+  }
+  __syncthreads();
+
+  if (warp < C::NPW) {
+    // ------------------------------------------------------------------ producers
+    const int tid = threadIdx.x;
+    int stage = 0;
+    unsigned phase = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      const GTile tl = tiles[t];
+      // the previous tile's copies were all issued: the row tables can be rewritten
+      asm volatile("bar.sync 1, %0;\n" ::"n"(C::NPT));
+      if (tid == 0) slow_rows = 0;
+      __syncwarp();
+      if (warp == 0) {
+        // segments -> rows: a warp-wide scan of the segments' row counts
+        int base = 0;
+        for (int s0 = tl.seg_begin; s0 < tl.seg_end && base < C::TM; s0 += 32) {
+          GSeg sg;
+          sg.rows = 0;
+          if (s0 + lane < tl.seg_end) sg = segs[s0 + lane];
+          int incl = sg.rows;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += v;
+          }
+          const int start = base + incl - sg.rows;
+          if (sg.rows > 0) {
+            const bool pad = sg.ke <= sg.kb;  // zero rows (alignment padding)
+            const double* p0 = pad ? nullptr : bufs.p[sg.buf] + sg.off - sg.kb;
+            const bool full_range = sg.kb == 0 && sg.ke == tl.klen && (sg.ld & 1) == 0 &&
+                                    (reinterpret_cast<uintptr_t>(p0) & 15) == 0;
+            if (!pad && !full_range) slow_rows = 1;
+            for (int x = 0; x < sg.rows && start + x < C::TM; ++x) {
+              akb[start + x] = pad ? 0 : sg.kb;
+              ake[start + x] = pad ? 0 : sg.ke;
+              arow[start + x] = pad ? nullptr : p0 + int64_t(x) * sg.ld;
+            }
+          }
+          base += __shfl_sync(0xffffffffu, incl, 31);
+        }
+      } else {
+        const double* B = bufs.p[tl.b_buf] + tl.b_off;
+        for (int j = lane; j < C::TM; j += 32) {
+          brow[j] = B + int64_t(j) * tl.b_ld;
+          bkb[j] = 0;
+          bke[j] = tl.klen;
+        }
+      }
+      asm volatile("bar.sync 1, %0;\n" ::"n"(C::NPT));
+      const double* safe = bufs.p[tl.b_buf] + tl.b_off;
+      const bool a_fast = slow_rows == 0;
+      const bool b_fast = (tl.b_ld & 1) == 0 && (reinterpret_cast<uintptr_t>(safe) & 15) == 0;
+      const int rows8 = (tl.rows + 7) & ~7, cols8 = (tl.cols + 7) & ~7;
+      const int nch = max(1, (tl.klen + C::KC - 1) / C::KC);
+      for (int c = 0; c < nch; ++c) {
+        mbar_wait(&empty[stage], phase ^ 1u);
+        double* sP = smem + stage * C::STAGE;
+        const unsigned sp = static_cast<unsigned>(__cvta_generic_to_shared(sP));
+        const unsigned sq = static_cast<unsigned>(__cvta_generic_to_shared(sP + C::OPSZ));
+        const int kk0 = c * C::KC;
+        const bool inside = kk0 + C::KC <= tl.klen;
+        gws_stage<C>(sp, arow, akb, ake, safe, tl.rows, rows8, kk0, a_fast && inside, tid);
+        gws_stage<C>(sq, brow, bkb, bke, safe, tl.cols, cols8, kk0, b_fast && inside, tid);
+        if (tid == 0) {
+          desc[stage].used = max(0, min(C::KC, tl.klen - kk0));
+          desc[stage].last = c + 1 == nch;
+        }
+        mbar_cp_async_arrive(&full[stage]);
+        mbar_arrive(&full[stage]);
+        if (++stage == C::STAGES) {
+          stage = 0;
+          phase ^= 1u;
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers
+  const int cw = warp - C::NPW;
+  int stage = 0;
+  unsigned phase = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const GTile tl = tiles[t];
+    const int nfc = (tl.cols + 7) >> 3;
+    unsigned amask = 0;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+      if (cw * 16 + a * 8 < tl.rows) amask |= 1u << a;
+    double acc[2][8][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    while (true) {
+      mbar_wait(&full[stage], phase);
+      const GwsDesc d = desc[stage];
+      const double* sP = smem + stage * C::STAGE;
+      const double* sQ = sP + C::OPSZ;
+      if (d.used > 0 && amask) {
+        switch (nfc) {
+          case 1: gws_mma<C, 1>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 2: gws_mma<C, 2>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 3: gws_mma<C, 3>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 4: gws_mma<C, 4>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 5: gws_mma<C, 5>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 6: gws_mma<C, 6>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          case 7: gws_mma<C, 7>(acc, sP, sQ, d.used, cw, lane, amask); break;
+          default: gws_mma<C, 8>(acc, sP, sQ, d.used, cw, lane, amask); break;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[stage]);
+      if (++stage == C::STAGES) {
+        stage = 0;
+        phase ^= 1u;
+      }
+      if (d.last) break;
+    }
+    double* out = bufs.p[tl.out_buf] + tl.out_off;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const int r = cw * 16 + a * 8 + (lane >> 2);
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int cc = b * 8 + (lane & 3) * 2 + h;
+          if (r < tl.rows && cc < tl.cols) out[r + int64_t(cc) * tl.out_ld] = acc[a][b][h];
+        }
+    }
   }
 }
 

@@ -2153,14 +2153,28 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       auto gather_batch = [&](int b) {
         const size_t n = ga.count(b);
         if (!n) return;
-        static bool gattr = false;
-        if (!gattr) {
+        // warp-specialized persistent kernel unless HX_GATHER_WS=0
+        static const bool ws = !(std::getenv("HX_GATHER_WS") && std::getenv("HX_GATHER_WS")[0] == '0');
+        static int ggrid = 0;
+        if (!ggrid) {
           CK(cudaFuncSetAttribute(gather_gemm_kernel<Gemm64>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, Gemm64::SMEM));
-          gattr = true;
+          CK(cudaFuncSetAttribute(gather_gemm_ws_kernel<Ws64>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, Ws64::SMEM));
+          int dev = 0, sms = 0, b = 0;
+          CK(cudaGetDevice(&dev));
+          CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+          CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, gather_gemm_ws_kernel<Ws64>,
+                                                           Ws64::THREADS, Ws64::SMEM));
+          ggrid = std::max(1, b) * sms;
         }
-        gather_gemm_kernel<Gemm64><<<int(n), Gemm64::THREADS, Gemm64::SMEM, s>>>(
-            c->gtiles.p + ga.cuts[size_t(b)], c->gsegs.p, bp, int(n));
+        if (ws)
+          gather_gemm_ws_kernel<Ws64><<<int(std::min<size_t>(n, size_t(ggrid))), Ws64::THREADS,
+                                        Ws64::SMEM, s>>>(c->gtiles.p + ga.cuts[size_t(b)],
+                                                         c->gsegs.p, bp, int(n));
+        else
+          gather_gemm_kernel<Gemm64><<<int(n), Gemm64::THREADS, Gemm64::SMEM, s>>>(
+              c->gtiles.p + ga.cuts[size_t(b)], c->gsegs.p, bp, int(n));
         CK(cudaGetLastError());
         c->launches++;
       };

@@ -59,7 +59,8 @@ def main():
     torch.cuda.profiler.stop()
     r = out.report
     walls = []
-    for _ in range(3):
+    import os
+    for _ in range(int(os.environ.get("HX_PP_EXTRA", "3"))):
         walls.append(hx.multiply.multiply_device(A, B, cfg, fetch=False).report.wall_s * 1e3)
     print(f"plan {r.plan_ms:.0f} dev {r.device_ms:.1f} form {r.form_ms:.1f} "
           f"mat {r.materialize_ms:.1f} recomp {r.recompress_ms:.1f} wall(3 more) "
