@@ -1,0 +1,3 @@
+#!/bin/bash
+cd "$(dirname "$0")/.."
+for rep in 1 2; do for v in 512 256 128; do echo "== HX_IMPLICIT=$v (run $rep)"; HX_IMPLICIT=$v HX_OVERLAP=0 timeout 600 python tools/phase_profile.py 2 --tag dense-svd 2>&1 | grep "^plan"; done; done
