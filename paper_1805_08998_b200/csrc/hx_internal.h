@@ -93,9 +93,21 @@ struct OutLeaf {
   // workspace; the leaf's terms are the groups [g_begin, g_end) of mat_groups
   int8_t implicit;
   int32_t g_begin, g_end;
+  // implicit route: the leaf's materialized part T_sub is block-sparse, the dense blocks
+  // [tsub_begin, tsub_end) of hx_plan::tsub (none: everything is sketched)
+  int32_t tsub_begin, tsub_end;
   // traditional mode (hmult_traditional): root of the leaf's fold tree in hx_plan::tnodes
   // (-1 otherwise); the path groups [g_begin, g_end) hold its inherited low-rank terms
   int32_t troot;
+};
+
+// One dense block of an implicit leaf's T_sub: the small sub-block terms of the leaf that
+// are materialized rather than sketched, gathered by their outermost small virtual block
+// (h x w, column-major at BUF_TILE + off, ld h; global coordinates r0, c0).
+struct TSubBlock {
+  int64_t off;
+  int64_t r0, c0;
+  int32_t h, w;
 };
 
 // Traditional-mode conversion tree of a far leaf (multiply.py:140-263).  Items name one
@@ -149,6 +161,7 @@ struct hx_plan {
   hx::hvec<hx::Group> core_groups, fac_groups, mat_groups;
   std::vector<hx::Group> mat_groups_all;  // one per creation block (real or virtual)
   hx::pvec<hx::OutLeaf> leaves;
+  hx::pvec<hx::TSubBlock> tsub;  // T_sub blocks of the implicit leaves
   int64_t core_elems = 0, term_elems = 0, tile_elems = 0, gather_elems = 0;
   hx::hvec<hx::ColRec> gcols;  // thin factors of each X-group (virtual G)
   std::vector<hx::TransRec> dtrans;  // transposed dense blocks (dense x H-block terms)

@@ -76,6 +76,7 @@ struct Out {
   std::vector<GRef> tile_groups;  // per tile: the groups of its root path and sub-blocks
   std::vector<Tile> tiles;        // g_begin/g_end index tile_groups; ws offsets local
   std::vector<hx::OutLeaf> leaves;
+  std::vector<hx::TSubBlock> tsub;  // offsets local to the task's far workspace
   std::vector<int32_t> log_block, log_a, log_b, log_rank;
   std::vector<int8_t> log_kind;
   int64_t n_terms_real = 0, n_terms_expand = 0, n_dxd = 0, created[3] = {0, 0, 0};
@@ -118,6 +119,13 @@ struct Task {
 struct VGroup {
   GRef g;
   int64_t r0, r1, c0, c1;
+  int32_t blk;  // T_sub block of the leaf holding this group (index into TBlk list), -1: sketched size
+};
+
+// Outermost small (materialized rather than sketched) virtual block below a far leaf.
+struct TBlk {
+  int64_t r0, r1, c0, c1;
+  bool used;
 };
 
 struct Builder {
@@ -143,6 +151,10 @@ struct Builder {
   Builder(const hx_tree& t_, const hx_operand& a, const hx_operand& b, const uint8_t* m,
           int tile, hx_plan& plan)
       : t(t_), A(a), B(b), mask(m), T(tile), P(plan) {}
+
+  // implicit route: a sub-block term on an h x w extent costs ~4 (h + w) L flops per unit of
+  // rank to sketch (range and co-range passes, L ~ 56 columns) against 2 h w to materialize
+  bool sketched_ext(double h, double wd) const { return h * wd >= 4.0 * sketch_cols * (h + wd); }
 
   int64_t lo(int c) const { return t.c_lo[c]; }
   int64_t sz(int c) const { return t.c_hi[c] - t.c_lo[c]; }
@@ -343,7 +355,8 @@ struct Builder {
   // Expansion of the pending inner x inner pairs of a far leaf over virtual sub-blocks
   // (exact).
   void expand(Walk& w, int tc, int sc, const PairList& pend, std::vector<VGroup>& vg,
-              int64_t& K, double& fdd, double& edd, int depth) const {
+              int64_t& K, double& fdd, double& edd, int depth, std::vector<TBlk>& tb,
+              int32_t blk_root) const {
     if (pend.empty()) return;
     if (t.c_child[2 * tc] < 0 || t.c_child[2 * sc] < 0)
       throw hx::Unsupported("H-block x dense pending pair at a leaf (ragged cluster trees)");
@@ -372,17 +385,24 @@ struct Builder {
           }
         }
         const int32_t ge = int32_t(o.terms.size());
+        // the outermost sub-block too small to sketch collects every group below it
+        int32_t child_root = blk_root;
+        if (child_root < 0 && !sketched_ext(double(sz(tcc)), double(sz(scc)))) {
+          child_root = int32_t(tb.size());
+          tb.push_back(TBlk{lo(tcc), lo(tcc) + sz(tcc), lo(scc), lo(scc) + sz(scc), false});
+        }
         if (ge > gb) {
           o.groups.push_back(Group{gb, ge});
           vg.push_back(VGroup{GRef{w.self, int32_t(o.groups.size() - 1)}, lo(tcc),
-                              lo(tcc) + sz(tcc), lo(scc), lo(scc) + sz(scc)});
+                              lo(tcc) + sz(tcc), lo(scc), lo(scc) + sz(scc), child_root});
+          if (child_root >= 0) tb[size_t(child_root)].used = true;
         }
-        if (!leaf_level) expand(w, tcc, scc, sub, vg, K, fdd, edd, depth + 1);
+        if (!leaf_level) expand(w, tcc, scc, sub, vg, K, fdd, edd, depth + 1, tb, child_root);
       }
   }
 
   void emit_leaf_tiles(Walk& w, int b, bool far, const std::vector<VGroup>& vg, int64_t K,
-                       double fdd, double edd) const {
+                       double fdd, double edd, const std::vector<TBlk>& tb) const {
     Out& o = w.o;
     const int tc = t.tau[b], sc = t.sigma[b];
     const int64_t m = sz(tc), n = sz(sc);
@@ -409,26 +429,72 @@ struct Builder {
     // sketch (range and co-range passes, L ~ 56 columns) against 2 h w to materialize; the
     // tiles materialize the remaining small sub-block terms into T_sub (none: no T_sub)
     const bool impl = far && implicit_min > 0 && std::min(m, n) >= implicit_min;
-    auto sketched = [this](const VGroup& v) {
-      const double h = double(v.r1 - v.r0), wd = double(v.c1 - v.c0);
-      return h * wd >= 4.0 * sketch_cols * (h + wd);
-    };
-    bool tsub = !impl;
+    L.tsub_begin = L.tsub_end = int32_t(o.tsub.size());
     if (impl) {
       L.implicit = 1;
       L.g_begin = int32_t(o.tile_groups.size());
       o.tile_groups.insert(o.tile_groups.end(), w.path.begin(), w.path.end());
-      for (const VGroup& v : vg) {
-        if (sketched(v))
-          o.tile_groups.push_back(v.g);
-        else
-          tsub = true;
-      }
+      for (const VGroup& v : vg)
+        if (v.blk < 0) o.tile_groups.push_back(v.g);
       L.g_end = int32_t(o.tile_groups.size());
-    }
-    if (!tsub) {  // everything is sketched: no tiles, no m x n workspace
-      L.tile_end = L.tile_begin;
-      L.sumsq_end = L.sumsq_begin;
+      // T_sub: one dense block per used small sub-block, tiled like a leaf of its own; the
+      // rest of the leaf (config 4's 65536-leaves: ~97 % of their 10^6 tiles) is neither
+      // stored nor multiplied
+      thread_local std::vector<std::vector<int32_t>> by_blk;
+      if (by_blk.size() < tb.size()) by_blk.resize(tb.size());
+      for (size_t q = 0; q < tb.size(); ++q) by_blk[q].clear();
+      for (int32_t vi = 0; vi < int32_t(vg.size()); ++vi)
+        if (vg[size_t(vi)].blk >= 0) by_blk[size_t(vg[size_t(vi)].blk)].push_back(vi);
+      std::vector<GRef> cur, prev;
+      for (size_t q = 0; q < tb.size(); ++q) {
+        const TBlk& B = tb[q];
+        if (!B.used) continue;
+        const int64_t h = B.r1 - B.r0, wd = B.c1 - B.c0;
+        hx::TSubBlock rec{ws, B.r0, B.c0, int32_t(h), int32_t(wd)};
+        o.tsub.push_back(rec);
+        int32_t prev_gb = -1, prev_ge = -1;
+        prev.clear();
+        for (int64_t j = 0; j < wd; j += T)
+          for (int64_t i = 0; i < h; i += T) {
+            const int64_t r0 = B.r0 + i, r1 = B.r0 + std::min<int64_t>(h, i + T);
+            const int64_t c0 = B.c0 + j, c1 = B.c0 + std::min<int64_t>(wd, j + T);
+            cur.clear();
+            for (int32_t vi : by_blk[q]) {
+              const VGroup& v = vg[size_t(vi)];
+              if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0) cur.push_back(v.g);
+            }
+            int32_t gb, ge;
+            if (prev_gb >= 0 && cur == prev) {
+              gb = prev_gb;
+              ge = prev_ge;
+            } else {
+              gb = int32_t(o.tile_groups.size());
+              o.tile_groups.insert(o.tile_groups.end(), cur.begin(), cur.end());
+              ge = int32_t(o.tile_groups.size());
+              prev = cur;
+              prev_gb = gb;
+              prev_ge = ge;
+            }
+            Tile tl;
+            std::memset(&tl, 0, sizeof(tl));
+            tl.out_off = rec.off + i + j * h;
+            tl.out_ld = int32_t(h);
+            tl.row0 = int32_t(r0);
+            tl.col0 = int32_t(c0);
+            tl.rows = int16_t(r1 - r0);
+            tl.cols = int16_t(c1 - c0);
+            tl.g_begin = gb;
+            tl.g_end = ge;
+            tl.out_buf = hx::BUF_TILE;
+            tl.mode = hx::MODE_STORE_SUMSQ;
+            tl.aux = o.n_sumsq++;
+            o.tiles.push_back(tl);
+          }
+        ws = align16(ws + h * wd);
+      }
+      L.tsub_end = int32_t(o.tsub.size());
+      L.tile_end = int32_t(o.tiles.size());
+      L.sumsq_end = o.n_sumsq;
       o.max_out_dim = std::max<int64_t>(o.max_out_dim, std::max(m, n));
       o.leaves.push_back(L);
       return;
@@ -436,17 +502,42 @@ struct Builder {
     ws = align16(ws + m * n);
     int32_t prev_gb = -1, prev_ge = -1;
     std::vector<GRef> cur, prev;
+    // sub-block groups by tile (CSR over the leaf's tile grid, column-major like the tile
+    // loop; creation order kept within a tile): a scan of every group per tile is quadratic
+    // on the largest leaves (config 4: 10^6 tiles x 10^4 groups per 65536-leaf)
+    const int64_t nti = (m + T - 1) / T, ntj = (n + T - 1) / T;
+    thread_local std::vector<int32_t> vstart, vfill, vlist;
+    vstart.assign(size_t(nti * ntj) + 1, 0);
+    auto tile_range = [&](const VGroup& v, int64_t& i0, int64_t& i1, int64_t& j0, int64_t& j1) {
+      i0 = (v.r0 - lo(tc)) / T;
+      i1 = (v.r1 - 1 - lo(tc)) / T;
+      j0 = (v.c0 - lo(sc)) / T;
+      j1 = (v.c1 - 1 - lo(sc)) / T;
+    };
+    for (const VGroup& v : vg) {
+      int64_t i0, i1, j0, j1;
+      tile_range(v, i0, i1, j0, j1);
+      for (int64_t j = j0; j <= j1; ++j)
+        for (int64_t i = i0; i <= i1; ++i) vstart[size_t(i + j * nti) + 1]++;
+    }
+    for (size_t k = 0; k < size_t(nti * ntj); ++k) vstart[k + 1] += vstart[k];
+    vfill.assign(vstart.begin(), vstart.end() - 1);
+    vlist.resize(size_t(vstart.back()));
+    for (int32_t vi = 0; vi < int32_t(vg.size()); ++vi) {
+      const VGroup& v = vg[size_t(vi)];
+      int64_t i0, i1, j0, j1;
+      tile_range(v, i0, i1, j0, j1);
+      for (int64_t j = j0; j <= j1; ++j)
+        for (int64_t i = i0; i <= i1; ++i) vlist[size_t(vfill[size_t(i + j * nti)]++)] = vi;
+    }
     for (int64_t j = 0; j < n; j += T) {
       for (int64_t i = 0; i < m; i += T) {
         const int64_t r0 = lo(tc) + i, r1 = lo(tc) + std::min<int64_t>(m, i + T);
         const int64_t c0 = lo(sc) + j, c1 = lo(sc) + std::min<int64_t>(n, j + T);
-        if (impl)
-          cur.clear();
-        else
-          cur.assign(w.path.begin(), w.path.end());
-        for (const VGroup& v : vg)
-          if (v.r0 < r1 && v.r1 > r0 && v.c0 < c1 && v.c1 > c0 && !(impl && sketched(v)))
-            cur.push_back(v.g);
+        cur.assign(w.path.begin(), w.path.end());
+        const size_t tix = size_t(i / T + (j / T) * nti);
+        for (int32_t q = vstart[tix]; q < vstart[tix + 1]; ++q)
+          cur.push_back(vg[size_t(vlist[size_t(q)])].g);
         int32_t gb, ge;
         if (cur == prev) {
           gb = prev_gb;
@@ -662,10 +753,11 @@ struct Builder {
         trad_leaf(w, c, rest);
       } else {
         std::vector<VGroup> vg;
+        std::vector<TBlk> tb;
         int64_t K = w.path_K;
         // inner x inner pairs pending at a leaf (far, or near above the leaf level on a
         // ragged tree) are expanded exactly over virtual sub-blocks
-        expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd, level + 1);
+        expand(w, t.tau[c], t.sigma[c], rest, vg, K, fdd, edd, level + 1, tb, -1);
         const double mm = double(sz(t.tau[c])), nn = double(sz(t.sigma[c]));
         if (kind(c) == NEAR) {
           o.flops_near += fdd + 2.0 * mm * nn * double(K);
@@ -674,7 +766,7 @@ struct Builder {
         } else {
           o.n_far++;
         }
-        emit_leaf_tiles(w, c, kind(c) == FAR, vg, K, fdd, edd);
+        emit_leaf_tiles(w, c, kind(c) == FAR, vg, K, fdd, edd, tb);
       }
       w.path_K = save_K;
       if (has) w.path.pop_back();
@@ -707,7 +799,7 @@ struct Builder {
     const size_t no = outs.size();
     std::vector<int64_t> b_terms(no + 1, 0), b_tg(no + 1, 0), b_tiles(no + 1, 0),
         b_sumsq(no + 1, 0), b_far(no + 1, 0), b_near(no + 1, 0), b_recs(no + 1, 0),
-        b_leaves(no + 1, 0), b_nodes(no + 1, 0), b_kids(no + 1, 0);
+        b_leaves(no + 1, 0), b_nodes(no + 1, 0), b_kids(no + 1, 0), b_tsub(no + 1, 0);
     for (size_t i = 0; i < no; ++i) {
       const Out& o = outs[i];
       b_nodes[i + 1] = b_nodes[i] + int64_t(o.tnodes.size());
@@ -720,11 +812,13 @@ struct Builder {
       b_near[i + 1] = b_near[i] + o.ws_near;
       b_recs[i + 1] = b_recs[i] + int64_t(o.recs.size());
       b_leaves[i + 1] = b_leaves[i] + int64_t(o.leaves.size());
+      b_tsub[i + 1] = b_tsub[i] + int64_t(o.tsub.size());
     }
     P.mat_terms.resize(size_t(b_terms[no]));
     P.mat_groups.resize(size_t(b_tg[no]));
     P.mat_tiles.resize(size_t(b_tiles[no]));
     P.leaves.resize(size_t(b_leaves[no]));
+    P.tsub.resize(size_t(b_tsub[no]));
     recs.resize(size_t(b_recs[no]));
     ws_far_total = b_far[no];
     ws_near_total = b_near[no];
@@ -793,11 +887,19 @@ struct Builder {
             L.g_end += int32_t(b_tg[i]);
           }
           if (L.troot >= 0) L.troot += int32_t(b_nodes[i]);
+          for (int32_t k = L.tsub_begin; k < L.tsub_end; ++k) {
+            hx::TSubBlock tb = o.tsub[size_t(k)];
+            tb.off += wb;
+            P.tsub[size_t(b_tsub[i]) + size_t(k)] = tb;
+          }
+          L.tsub_begin += int32_t(b_tsub[i]);
+          L.tsub_end += int32_t(b_tsub[i]);
           P.leaves[size_t(b_leaves[i] + l)] = L;
         }
       }
     }
     lap("merge copy");
+    if (!P.tsub.empty()) P.needs_eye = true;  // the iterative route applies T_sub blocks as T_b I
     if (b_nodes[no] > 0) {  // traditional-mode conversion trees
       P.tnodes.resize(size_t(b_nodes[no]));
       P.tkids.resize(size_t(b_kids[no]));
@@ -1352,7 +1454,7 @@ struct Builder {
         outs[0].bytes_near += 8.0 * (edd + m * m);
         outs[0].n_near++;
         std::vector<VGroup> vg;
-        emit_leaf_tiles(w, 0, false, vg, 0, fdd, edd);
+        emit_leaf_tiles(w, 0, false, vg, 0, fdd, edd, {});
       }
     } else {
       std::vector<Task> tasks;

@@ -1070,6 +1070,26 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
         koff += x.k;
         terms.push_back(e);
       }
+      // the block-sparse T_sub: every dense block as a term T_b I (identity from BUF_EYE)
+      for (int32_t q = L.tsub_begin; q < L.tsub_end; ++q) {
+        const TSubBlock& tb = P->tsub[size_t(q)];
+        if (tb.w > EYE_LD) throw hx::Unsupported("T_sub block wider than the identity buffer");
+        IterTerm e;
+        e.P = bp0.p[BUF_TILE] + tb.off;
+        e.ps = 1;
+        e.pk = tb.h;
+        e.Q = bp0.p[BUF_EYE];
+        e.qs = EYE_LD;
+        e.qk = 1;
+        e.k = tb.w;
+        e.ri = int32_t(tb.r0 - L.row0);
+        e.rn = tb.h;
+        e.ci = int32_t(tb.c0 - L.col0);
+        e.cn = tb.w;
+        e.koff = koff;
+        koff += tb.w;
+        terms.push_back(e);
+      }
       ksum[size_t(i)] = koff;
     }
     tend[size_t(i)] = int(terms.size());
@@ -1115,11 +1135,7 @@ int64_t recompress_iterative(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
       const int64_t kc = kcap[size_t(i)];
       double* p = wb + off[a];
       IterJob jb;
-      jb.T = f.implicit ? (P->leaves[size_t(f.leaf)].tile_end >
-                                   P->leaves[size_t(f.leaf)].tile_begin
-                               ? c->buf(BUF_TILE) + f.t_off
-                               : nullptr)
-                        : c->buf(BUF_TILE) + f.t_off;
+      jb.T = f.implicit ? nullptr : c->buf(BUF_TILE) + f.t_off;
       jb.ldT = f.m;
       jb.m = f.m;
       jb.n = f.n;
@@ -1993,8 +2009,8 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
           const OutLeaf& L = P->leaves[f.leaf];
           std::vector<Term> ts;
           std::vector<std::pair<int, int>> band;
-          ts.reserve(f.it.size() + 1);
-          band.reserve(f.it.size() + 1);
+          ts.reserve(f.it.size() + size_t(L.tsub_end - L.tsub_begin));
+          band.reserve(f.it.size() + size_t(L.tsub_end - L.tsub_begin));
           for (int q : f.worder) {  // (lr, row band): terms sharing a band are adjacent
             const ImplTerm& x = f.it[size_t(q)];
             Term y = mk(x.t.a_buf, x.t.a_off, x.t.a_ld, x.t.a_kc, BUF_CORE, f.zoff + x.zrow,
@@ -2003,12 +2019,14 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             ts.push_back(y);
             band.emplace_back(x.ri, x.rn);
           }
-          if (L.tile_end > L.tile_begin) {  // + T_sub Omega (the materialized sub-blocks)
-            Term y = mk(BUF_TILE, f.t_off, f.m, 0, BUF_OMEGA, 0, int32_t(c->omega_rows), 1,
-                        f.n, f.m, l + PR);
-            y.r_lo = int32_t(L.row0);
+          for (int32_t q = L.tsub_begin; q < L.tsub_end; ++q) {
+            // + T_sub Omega: one term per dense block of the block-sparse T_sub
+            const TSubBlock& tb = P->tsub[size_t(q)];
+            Term y = mk(BUF_TILE, tb.off, tb.h, 0, BUF_OMEGA, tb.c0 - L.col0,
+                        int32_t(c->omega_rows), 1, tb.w, tb.h, l + PR);
+            y.r_lo = int32_t(tb.r0);
             ts.push_back(y);
-            band.emplace_back(0, f.m);
+            band.emplace_back(int(tb.r0 - L.row0), tb.h);
           }
           gm.cover_banded(ts, band, BUF_WORK, woff(f.Y), f.m, f.m, l + PR, int(L.row0), 0, true);
         } else {
@@ -2101,11 +2119,13 @@ extern "C" int hx_product(hx_ctx* c, hx_plan* P, const hx_product_cfg* cfg,
             ts.push_back(y);
             band.emplace_back(x.ci, x.cn);
           }
-          if (L.tile_end > L.tile_begin) {  // + T_sub^T Q
-            Term y = mk(BUF_TILE, f.t_off, f.m, 1, BUF_WORK, woff(f.Y), f.m, 1, f.m, f.n, l);
-            y.r_lo = int32_t(L.col0);
+          for (int32_t q = L.tsub_begin; q < L.tsub_end; ++q) {  // + T_sub^T Q, block by block
+            const TSubBlock& tb = P->tsub[size_t(q)];
+            Term y = mk(BUF_TILE, tb.off, tb.h, 1, BUF_WORK, woff(f.Y) + (tb.r0 - L.row0), f.m, 1,
+                        tb.h, tb.w, l);
+            y.r_lo = int32_t(tb.c0);
             ts.push_back(y);
-            band.emplace_back(0, f.n);
+            band.emplace_back(int(tb.c0 - L.col0), tb.w);
           }
           gm.cover_banded(ts, band, BUF_WORK, woff(f.Bt), f.n, f.n, l, int(L.col0), 0, true);
         } else {

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--eager", action="store_true", help="fill the batches in the plan call")
     ap.add_argument("--sizes", action="store_true", help="materialization flops by leaf size")
     ap.add_argument("--chunk", type=int, default=-1, help="plan only this chunk of 3")
+    ap.add_argument("--implicit", type=int, default=512, help="implicit-route threshold (0: off)")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     t0 = time.time()
@@ -61,7 +62,9 @@ def main():
         mask = multiply.group_mask(bct, groups[a.chunk])
     for _ in range(a.reps):
         t0 = time.perf_counter()
-        p = _lib.Plan(ta, d, d, mask, 64, flags=0 if a.eager else _lib.Plan.DEFER)
+        from paper_1805_08998_b200 import multiply as _m
+        p = _lib.Plan(ta, d, d, mask, 64, flags=(0 if a.eager else _lib.Plan.DEFER) |
+                      _m.implicit_flags(a.implicit))
         t1 = time.perf_counter()
         msg = f"plan {1e3 * (t1 - t0):.1f} ms"
         if a.fill:
