@@ -110,3 +110,36 @@ def test_plan_term_log_ragged_tree(golden):
     assert mine.shape == ref.shape
     assert np.array_equal(mine, ref)
     assert plan.info.n_dxd > 0
+
+
+def test_plan_implicit_route_block_sparse_tsub(golden):
+    """Implicit route (HX_PLAN_IMPLICIT): the restrict log does not depend on the route, and
+    the materialized part of an implicit leaf is the set of its small sub-block terms' dense
+    blocks (block-sparse T_sub), never a leaf-sized buffer: the tile workspace can only
+    shrink against the fully materialized plan."""
+    import paper_1805_08998_b200 as hx
+    from paper_1805_08998_b200 import _lib, hmatrix, multiply
+
+    g = golden("small2d.npz")
+    n, n_min, eta, eps_a, tol = g["params"]
+    pts = g["points"]
+    bct = hx.build_block_cluster_tree(hx.build_cluster_tree(pts, int(n_min)), eta)
+    obt = O.BlockTreeO(O.ClusterTreeO(pts, int(n_min)), eta)
+    A = O.assemble_o("exp", obt, O.Eps(eps_a), pts)
+    pool, d = hmatrix.pack_operand(hx.HMatrix(bct, A.data))
+    ta = hmatrix.tree_arrays(bct)
+    tile = multiply.plan_tile(bct)
+    dense = _lib.Plan(ta, d, d, tile=tile, flags=_lib.Plan.LOG)
+    logs = dense.term_log()
+    for impl in (32, 64):
+        p = _lib.Plan(ta, d, d, tile=tile, flags=_lib.Plan.LOG | multiply.implicit_flags(impl))
+        lg = p.term_log()
+        for k in ("block", "kind", "a", "b", "rank"):
+            assert np.array_equal(lg[k], logs[k])
+        assert p.info.n_far == dense.info.n_far and p.info.n_near == dense.info.n_near
+        assert p.info.mat_terms == dense.info.mat_terms
+        assert p.info.tile_elems <= dense.info.tile_elems
+        lv, lvd = p.leaves(), dense.leaves()
+        assert np.array_equal(lv["ids"], lvd["ids"]) and np.array_equal(lv["K"], lvd["K"])
+        p.close()
+    dense.close()
