@@ -1076,14 +1076,26 @@ struct Builder {
     tg0 = std::chrono::steady_clock::now();
     const int nn = t.n_nodes;
     const size_t nr = recs.size();
-    // counting sort of the terms by (side, X)
-    std::vector<int32_t> cnt(2 * size_t(nn) + 1, 0);
+    // counting sort of the terms by (side, X), over the keys that occur (a masked plan --
+    // one chunk of 65 on config 4 -- touches a small part of the 2 n_nodes key space, and
+    // per-thread histograms over all of it cost more than the sort itself)
     auto key = [&](const TRec& r) { return r.side * nn + (r.side == 0 ? r.pc : r.qc); };
+    const int nk_all = 2 * nn;
+    std::vector<uint8_t> used(size_t(nk_all), 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < int64_t(nr); ++i) used[size_t(key(recs[size_t(i)]))] = 1;
+    std::vector<int32_t> kid(size_t(nk_all), -1), ckey;
+    for (int k = 0; k < nk_all; ++k)
+      if (used[size_t(k)]) {
+        kid[size_t(k)] = int32_t(ckey.size());
+        ckey.push_back(k);
+      }
+    const int nk = int(ckey.size());
+    std::vector<int32_t> cnt(size_t(nk) + 1, 0);
     // parallel counting sort: per-thread histograms over contiguous slices of recs, then
     // (key, thread)-ordered offsets, so the order is the same as a sequential stable sort
-    const int nk = 2 * nn;
     const int nth = std::max(1, std::min(omp_get_max_threads(), int(nr / 65536) + 1));
-    std::vector<int32_t> hist(size_t(nth) * size_t(nk), 0);
+    std::vector<int32_t> hist(size_t(nth) * size_t(std::max(nk, 1)), 0);
     std::vector<int32_t> block_sum(size_t(nth), 0);
     order.resize(nr);
 #pragma omp parallel num_threads(nth)
@@ -1091,8 +1103,8 @@ struct Builder {
       const int nth = omp_get_num_threads();  // the team actually granted
       const int th = omp_get_thread_num();
       const size_t a = nr * size_t(th) / size_t(nth), e = nr * size_t(th + 1) / size_t(nth);
-      int32_t* h = &hist[size_t(th) * size_t(nk)];
-      for (size_t i = a; i < e; ++i) h[key(recs[i])]++;
+      int32_t* h = &hist[size_t(th) * size_t(std::max(nk, 1))];
+      for (size_t i = a; i < e; ++i) h[kid[size_t(key(recs[i]))]]++;
 #pragma omp barrier
       // (key, thread)-ordered exclusive prefix, in parallel over key blocks
       const int kb0 = int(int64_t(nk) * th / nth), kb1 = int(int64_t(nk) * (th + 1) / nth);
@@ -1114,22 +1126,18 @@ struct Builder {
       }
       if (th == nth - 1) cnt[size_t(nk)] = run;
 #pragma omp barrier
-      for (size_t i = a; i < e; ++i) order[size_t(h[key(recs[i])]++)] = int32_t(i);
+      for (size_t i = a; i < e; ++i) order[size_t(h[kid[size_t(key(recs[i]))]]++)] = int32_t(i);
     }
     lap("order");
-    std::vector<int32_t> gpos(size_t(nk) + 1, 0);
-    for (int g = 0; g < nk; ++g) gpos[size_t(g) + 1] = gpos[size_t(g)] + (cnt[g] != cnt[g + 1]);
-    // (a sequential pass of nk adds: cheap next to the histogram work)
     G.clear();
-    G.resize(size_t(gpos[size_t(nk)]));
+    G.resize(size_t(nk));
 #pragma omp parallel for schedule(static)
     for (int g = 0; g < nk; ++g) {
-      if (cnt[g] == cnt[g + 1]) continue;
-      GInfo& gi = G[size_t(gpos[size_t(g)])];
-      gi.b0 = cnt[g];
-      gi.b1 = cnt[g + 1];
-      gi.side = int8_t(g >= nn ? 1 : 0);
-      gi.X = g - gi.side * nn;
+      GInfo& gi = G[size_t(g)];
+      gi.b0 = cnt[size_t(g)];
+      gi.b1 = cnt[size_t(g) + 1];
+      gi.side = int8_t(ckey[size_t(g)] >= nn ? 1 : 0);
+      gi.X = ckey[size_t(g)] - gi.side * nn;
     }
     const int64_t ng = int64_t(G.size());
     lap("sort");
