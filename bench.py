@@ -423,7 +423,7 @@ def bench_ours(args, rank, world, local):
     mask = None
     if world > 1:
         # the partition is priced once (measured planning times) on rank 0 and shipped
-        masks = [distributed.partition(A, B, world)[0] if rank == 0 else None]
+        masks = [distributed.partition(A, B, world, tag=args.tag)[0] if rank == 0 else None]
         dist.broadcast_object_list(masks, src=0)
         mask = masks[0][rank]
     setup_s = time.time() - t_setup

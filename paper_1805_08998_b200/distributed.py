@@ -43,7 +43,7 @@ def leaf_costs(leaves):
     return 2 * m * n * K + leaves["fdd"] + np.where(leaves["kind"] == 1, 60 * m * n, 0.0)
 
 
-def partition(h, k, world, measured=True):
+def partition(h, k, world, measured=True, tag="dense-svd"):
     """Per-rank leaf masks of the output (``multiply.subtree_partition``): units priced by
     their own plans (``plan_unit_costs``, host planning time included) when ``measured``,
     else by the summed leaf costs.  Returns (masks, per-rank load)."""
@@ -60,7 +60,7 @@ def partition(h, k, world, measured=True):
     full.close()
     cost = np.zeros(block_arrays(bct).n_nodes)
     cost[lv["ids"]] = leaf_costs(lv)
-    unit_cost = (lambda us: plan_unit_costs(h, k, us)) if measured else None
+    unit_cost = (lambda us: plan_unit_costs(h, k, us, tag=tag)) if measured else None
     _, _, load, masks = subtree_partition(bct, cost, world, unit_cost=unit_cost)
     return masks, load
 
@@ -138,7 +138,7 @@ def multiply_devices(h, k, cfg, devices, masks=None, fetch=True, **kw):
     devices = [int(d) for d in devices]
     world = len(devices)
     if masks is None:
-        masks, _ = partition(h, k, world)
+        masks, _ = partition(h, k, world, tag=cfg.compressor.tag)
     keep_a, ptr_a = _replicate_pool(h, devices)
     keep_b, ptr_b = (keep_a, ptr_a) if k is h else _replicate_pool(k, devices)
     shards = [None] * world
@@ -255,7 +255,7 @@ def hmult_new_spmd(h, k, cfg, bct, group=None, device=None, product=None, measur
     A = broadcast_operand(h, bct, 0, group, device)
     B = A if same[0] else broadcast_operand(k, bct, 0, group, device)
     world = dist.get_world_size(group)
-    masks = [partition(A, B, world, measured)[0] if rank == 0 else None]
+    masks = [partition(A, B, world, measured, tag=cfg.compressor.tag)[0] if rank == 0 else None]
     dist.broadcast_object_list(masks, src=0, group=group)
     mask = masks[0][rank]
     if product is None:

@@ -401,37 +401,46 @@ def subtree_partition(bct, leaf_cost, world, min_units_per_rank=8, unit_cost=Non
 FORM_BPS = 3.8e12
 MAT_FPS = 28e12
 FAR_S = 2.4e-6
+SKETCH_BPS = 2.0e12  # gathered sketch products of the implicit leaves
 # a rank's wall time is the larger of its device time and its host planning time (the two
 # overlap chunk by chunk); the planning time of a unit is measured on its own plan
 
 
-def plan_unit_costs(h, k, units, tile=None):
+def plan_unit_costs(h, k, units, tile=None, tag="dense-svd"):
     """Estimated seconds of each unit (a subtree's masked plan): the larger of its device
-    time (formation bytes, materialization flops of its near and far leaves, a per-far-leaf
-    recompression term) and its host planning time (measured: the time its plan took, work
-    lists included).  For the multi-GPU partition (these plans are made once, outside the
-    timed step)."""
+    time (formation bytes, materialization flops of its near and materialized far leaves,
+    the sketch passes of its implicit leaves, a per-far-leaf recompression term) and its
+    host planning time (measured: the time its plan took, work lists included).  The plans
+    take the route the product of compressor ``tag`` takes (implicit above its threshold).
+    For the multi-GPU partition (these plans are made once, outside the timed step)."""
     arr = block_arrays(h.bct)
     leaf = arr.kind_code != 0
     _, da = operand_directory(h)
     _, db = (None, da) if k is h else operand_directory(k)
     ta = tree_arrays(h.bct)
     tile = tile or plan_tile(h.bct)
+    iflags = implicit_flags(None, tag)
+    imin = (1 << ((iflags >> 8) & 31)) if iflags else 0  # HX_PLAN_IMPLICIT_SHIFT
     out = []
     if units:  # warm-up: the first plan also grows the page-locked plan-array cache
         m = np.zeros(arr.n_nodes, dtype=np.uint8)
         m[units[0][0]:units[0][1]] = leaf[units[0][0]:units[0][1]]
-        _lib.Plan(ta, da, db, m, tile).close()
+        _lib.Plan(ta, da, db, m, tile, flags=iflags).close()
     for b0, b1 in units:
         m = np.zeros(arr.n_nodes, dtype=np.uint8)
         m[b0:b1] = leaf[b0:b1]
         t0 = time.perf_counter()
-        p = _lib.Plan(ta, da, db, m, tile)  # all work lists filled: the unit's host work
+        p = _lib.Plan(ta, da, db, m, tile, flags=iflags)  # work lists filled: the host work
         host = time.perf_counter() - t0
         lv = p.leaves()
         far = lv["kind"] == 1
-        mat = float(np.sum(2.0 * lv["m"] * lv["n"] * lv["K"] + lv["fdd"]))
-        dev = p.info.bytes_form / FORM_BPS + mat / MAT_FPS + FAR_S * float(far.sum())
+        mm, nn, K = lv["m"].astype(float), lv["n"].astype(float), lv["K"].astype(float)
+        impl = far & (np.minimum(lv["m"], lv["n"]) >= imin) if imin else np.zeros(len(far), bool)
+        mat = float(np.sum(np.where(impl, 0.0, 2.0 * mm * nn * K + lv["fdd"])))
+        # implicit leaves: range and co-range passes stream the stacked factors twice
+        sk_bytes = float(np.sum(np.where(impl, 2.0 * 8.0 * K * (mm + nn), 0.0)))
+        dev = p.info.bytes_form / FORM_BPS + mat / MAT_FPS + sk_bytes / SKETCH_BPS + \
+            8.0 * float(p.info.tile_elems) / FORM_BPS + FAR_S * float(far.sum())
         out.append(max(dev, host))
         p.close()
     return out

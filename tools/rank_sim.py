@@ -73,7 +73,7 @@ def main():
                 m[lv["ids"][owner == r]] = 1
                 masks.append(m)
         else:
-            uc = None if a.leafcost else (lambda us: multiply.plan_unit_costs(A, B, us))
+            uc = None if a.leafcost else (lambda us: multiply.plan_unit_costs(A, B, us, tag=a.tag))
             _, units, load, masks = multiply.subtree_partition(bct, cost, w, unit_cost=uc)
         per = []
         for r in range(w):
