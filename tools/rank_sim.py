@@ -48,6 +48,8 @@ def main():
     ap.add_argument("--ranks", default="", help="only these ranks (comma list)")
     ap.add_argument("--skip-full", action="store_true")
     ap.add_argument("--tag", default="dense-svd")
+    ap.add_argument("--save-masks", default="", help="write the partition (npz) and exit")
+    ap.add_argument("--load-masks", default="", help="use a saved partition (one process per rank)")
     a = ap.parse_args()
     c = configs.CONFIGS[a.cfg]
     bct, A, B = configs.build_operands(c)
@@ -72,9 +74,16 @@ def main():
                 m = np.zeros(bct.n_nodes, np.uint8)
                 m[lv["ids"][owner == r]] = 1
                 masks.append(m)
+        elif a.load_masks:
+            z = np.load(a.load_masks)
+            masks, load = list(z["masks"]), z["load"]
         else:
             uc = None if a.leafcost else (lambda us: multiply.plan_unit_costs(A, B, us, tag=a.tag))
             _, units, load, masks = multiply.subtree_partition(bct, cost, w, unit_cost=uc)
+        if a.save_masks:
+            np.savez_compressed(a.save_masks, masks=np.stack(masks), load=np.asarray(load))
+            print(f"partition for world {w} saved to {a.save_masks}", flush=True)
+            return
         per = []
         for r in range(w):
             if only is not None and r not in only:
