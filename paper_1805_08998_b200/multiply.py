@@ -257,35 +257,51 @@ def _subtree_end(arr):
     return np.arange(n) + size
 
 
-def _tree_meta(bct):
+def _tree_meta(bct, implicit_min=0):
+    """(end of each node's subtree in pre-order, cumulative leaf weight).  The weight of a
+    leaf is its area -- what its materialized block and most of its term factors scale
+    with -- except for far leaves on the implicit route (min(m, n) >= ``implicit_min`` > 0),
+    which are never materialized: their workspace is the sketch panels, ~64 (m + n).  Chunks
+    sized by plain area put a few huge implicit leaves (config 4: 65536 x 65536) on a par with
+    10^6 small blocks and had to be re-planned when they came out ten times too large."""
     arr = block_arrays(bct)
-    meta = getattr(arr, "_hx_meta", None)
+    cache = getattr(arr, "_hx_meta", None)
+    if cache is None:
+        cache = {}
+        try:
+            arr._hx_meta = cache
+        except AttributeError:  # pragma: no cover
+            pass
+    meta = cache.get(int(implicit_min))
     if meta is None:
         kind = arr.kind_code
         lo, hi = arr.tree.lo, arr.tree.hi
-        area = np.where(kind != 0,
-                        (hi[arr.tau] - lo[arr.tau]) * (hi[arr.sigma] - lo[arr.sigma]), 0)
-        meta = (_subtree_end(arr), np.concatenate([[0], np.cumsum(area)]))
-        try:
-            arr._hx_meta = meta
-        except AttributeError:  # pragma: no cover
-            pass
+        m = hi[arr.tau] - lo[arr.tau]
+        n = hi[arr.sigma] - lo[arr.sigma]
+        area = np.where(kind != 0, m * n, 0)
+        if implicit_min > 0:
+            impl = (kind == 1) & (np.minimum(m, n) >= implicit_min)
+            area = np.where(impl, np.minimum(64 * (m + n), m * n), area)
+        end = cache[0][0] if 0 in cache else _subtree_end(arr)
+        meta = (end, np.concatenate([[0], np.cumsum(area)]))
+        cache[int(implicit_min)] = meta
     return meta
 
 
-def chunk_units(bct):
+def chunk_units(bct, implicit_min=0):
     """Disjoint pre-order id ranges covering every leaf: the subtrees rooted at the first
-    block level holding a far leaf, and the leaves above it; with their leaf areas."""
+    block level holding a far leaf, and the leaves above it; with their leaf weights
+    (``_tree_meta``)."""
     arr = block_arrays(bct)
     kind, level = arr.kind_code, arr.level
     far_lv = level[kind == 1]
     lf = int(far_lv.min()) if far_lv.size else int(level.max())
-    end, carea = _tree_meta(bct)
+    end, carea = _tree_meta(bct, implicit_min)
     roots = np.flatnonzero((level == lf) | ((level < lf) & (kind != 0)))
     return [(int(b), int(end[b]), float(carea[end[b]] - carea[b])) for b in roots]
 
 
-def split_chunk(bct, group):
+def split_chunk(bct, group, implicit_min=0):
     """Halve a chunk (list of units); a single unit splits into its child subtrees (their
     common ancestors' terms are then planned for each part)."""
     if len(group) > 1:
@@ -293,7 +309,7 @@ def split_chunk(bct, group):
         return [group[:h], group[h:]]
     b0, b1, _ = group[0]
     arr = block_arrays(bct)
-    end, carea = _tree_meta(bct)
+    end, carea = _tree_meta(bct, implicit_min)
     kids = [int(c) for c in arr.child[b0] if c >= 0]
     if not kids:
         return [group]
@@ -301,10 +317,10 @@ def split_chunk(bct, group):
     return parts
 
 
-def chunk_groups(bct, n_chunks, first=1.0, weights=None):
+def chunk_groups(bct, n_chunks, first=1.0, weights=None, implicit_min=0):
     """About `n_chunks` chunks of consecutive units; chunk i gets a share of the leaf area
     proportional to weights[i] (default: the first one `first`, the others 1)."""
-    units = chunk_units(bct)
+    units = chunk_units(bct, implicit_min)
     total = sum(u[2] for u in units)
     n_chunks = max(1, n_chunks)
     env = os.environ.get("HX_CHUNK_WEIGHTS")
@@ -629,14 +645,17 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
     # with overlap the first chunk is small: its planning is the only exposed part
     weights = list(OVERLAP_WEIGHTS) if (chunks is None and use_overlap and not adaptive and
                                         nch == len(OVERLAP_WEIGHTS)) else None
+    iflags = implicit_flags(implicit_min, cfg.compressor.tag) if not trad else \
+        (int(trad) << TRAD_SHIFT)
+    # memory-bound products size their chunks by workspace weight (implicit leaves count by
+    # their sketch panels, not their area: _tree_meta); products that fit keep plain areas
+    wmin = (1 << ((iflags >> 8) & 31)) if (adaptive and not trad and (iflags >> 8) & 31) else 0
     queue = collections.deque(chunk_groups(h.bct, nch, first=0.2 if use_overlap else 1.0,
-                                           weights=weights))
+                                           weights=weights, implicit_min=wmin))
     budget = 0.8 * available_bytes(dev) - 4e9
 
     plan_ms = [0.0]
     timeline = []  # (what, host start, host end) for HX_TIMING
-    iflags = implicit_flags(implicit_min, cfg.compressor.tag) if not trad else \
-        (int(trad) << TRAD_SHIFT)
 
     def make_plan(group):
         mask = group_mask(h.bct, group, leaf_mask) if (len(queue_all) > 1 or leaf_mask
@@ -721,11 +740,11 @@ def _multiply_device(h, k, cfg, device, leaf_mask, sketch0, oversample, device_o
                 rate = pb / max(area, 1.0)
                 last_rate[0] = max(last_rate[0], rate)
                 units = group if len(group) > 1 else \
-                    [p[0] for p in split_chunk(h.bct, group)]
+                    [p[0] for p in split_chunk(h.bct, group, wmin)]
                 parts = regroup_units([units], rate, 0.7 * budget) if len(units) > 1 \
                     else [units]
                 if len(parts) == 1:
-                    parts = split_chunk(h.bct, units)
+                    parts = split_chunk(h.bct, units, wmin)
                 if len(parts) == 1:
                     break
                 group_split[0] = True
