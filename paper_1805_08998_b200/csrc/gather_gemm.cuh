@@ -221,6 +221,8 @@ template <class C>
 __global__ void __launch_bounds__(C::THREADS, C::MINB) gather_gemm_ws_kernel(
     const GTile* __restrict__ tiles, const GSeg* __restrict__ segs,
     const __grid_constant__ BufPtrs bufs, int n_tiles) {
+  static_assert(C::NPW == 2 && C::NCW == 4 && C::TM == 64,
+                "warp 0 builds the A row table, warp 1 the B table; 4 consumers x 16 rows");
   extern __shared__ __align__(16) double smem[];
   __shared__ __align__(8) uint64_t full[C::STAGES], empty[C::STAGES];
   __shared__ GwsDesc desc[C::STAGES];
